@@ -1,0 +1,229 @@
+/*
+ * mlpv.h -- C ABI of the B200-native MLP safety checker (arXiv 1907.12933, data-parallel core).
+ *
+ * The paper checks, symbolically, (a) the four covering methods SS / DS / SV / DV between pairs
+ * of inputs (§III.B) and (b) `checkNN`: whether an image within a proximity
+ * bound of a dataset image changes the classification (§III.C).  `checkNN`
+ * takes "an ANN with its weights and bias descriptions", "the image to be checked" and "a
+ * parameter that limits the proximity".  This library replaces the symbolic
+ * search by exhaustive enumeration (or Philox sampling) of a discretised perturbation space
+ * around each base image, evaluated on the GPU: for every candidate it runs the MLP forward pass
+ * (Eq. 1-2), takes the argmax, tests the safety property
+ * and accumulates SS / VS / SV / VV pair coverage between adjacent layers, base versus candidate.
+ * The paper's DS-Cover is called VS here and DV-Cover is called VV.
+ *
+ * Conventions for every entry point:
+ *   - all functions return mlpv_status; no exception crosses the ABI;
+ *   - argument errors are detected synchronously, before any GPU work, and described by
+ *     mlpv_last_error(handle) (mlpv_last_error(NULL) for errors of mlpv_create / mlpv_decode);
+ *   - a CUDA failure is sticky: the handle reports MLPV_E_CUDA from then on;
+ *   - a handle is bound to one device and is not thread-safe (one host thread at a time);
+ *   - "device" pointers are CUDA global-memory pointers on the handle's device; "host" pointers
+ *     are ordinary process memory; `stream` is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Numerics (readings C16-C19):
+ *   MLPV_NUM_FP32  fp32 weights / inputs, fp32 biases, sigmoid or ReLU hidden layers, fp32 math.
+ *   MLPV_NUM_BF16  bf16 weights / inputs, fp32 biases, ReLU hidden layers; tensor-core contraction
+ *                  with fp32 accumulation; hidden activations carried at ~fp32 precision.
+ *   MLPV_NUM_Q4_12 int16 Q4.12 weights / inputs, int32 Q8.24 accumulators and biases, hidden
+ *                  requant u16 = sat16((acc + 2^11) >> 12), PL-sigmoid or ReLU; bit-exact.
+ *   MLPV_NUM_INT8  int8 weights, u8 inputs, int32 accumulators and biases, hidden
+ *                  y = min(255, max(0, (acc + 2^(sh-1)) >> sh)) (ReLU + requant); bit-exact.
+ * Potentials ("u", the pre-activation of Eq. 1; for the output layer, the logits) are what every
+ * predicate reads (reading C1).  Fixed-point potentials are int32 accumulators.
+ */
+#ifndef MLPV_H
+#define MLPV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLPV_MAX_LAYERS 8      /* weight layers L */
+#define MLPV_MAX_CLASSES 16    /* n_L */
+
+typedef struct mlpv_ctx *mlpv_t;
+
+typedef enum {
+    MLPV_OK = 0,
+    MLPV_E_INVALID = 1,      /* bad argument value (NULL pointer, out-of-range field, non-finite) */
+    MLPV_E_SHAPE = 2,        /* inconsistent sizes */
+    MLPV_E_UNSUPPORTED = 3,  /* valid but not built (numeric x activation x perturbation x shape) */
+    MLPV_E_OVERFLOW = 4,     /* fixed-point worst-case accumulator bound >= 2^31 */
+    MLPV_E_OOM = 5,          /* device allocation failed */
+    MLPV_E_CUDA = 6          /* CUDA runtime / launch failure (sticky) */
+} mlpv_status;
+
+typedef enum { MLPV_NUM_FP32 = 0, MLPV_NUM_BF16 = 1, MLPV_NUM_Q4_12 = 2, MLPV_NUM_INT8 = 3 } mlpv_numeric;
+typedef enum { MLPV_ACT_SIGMOID = 0, MLPV_ACT_PL_SIGMOID = 1, MLPV_ACT_RELU = 2 } mlpv_act;
+
+/* The network ("weights and bias descriptions").  Host memory, read during
+ * mlpv_create only (deep-copied to device memory owned by the handle).
+ *   sizes[L+1]: n_0 (input pixels) .. n_L (classes, 1 <= n_L <= 16).
+ *   W[l]: row-major n_{l+1} x n_l, element type by numeric: float | uint16 bf16 bits | int16 | int8.
+ *   b[l]: n_{l+1} elements: float (FP32, BF16) | int32 in accumulator units (Q4_12, INT8). */
+typedef struct {
+    int32_t n_layers;
+    const int32_t *sizes;
+    const void *const *W;
+    const void *const *b;
+    mlpv_act hidden_act;
+} mlpv_net;
+
+/* Quantisation parameters (host, read during mlpv_create).
+ *   requant_shift[L-1]: INT8 only, the per-hidden-layer shift sh_l >= 0 (reading C18).
+ *   sigmoid_knots[129]: PL_SIGMOID only; Q4.12 knots over [-8, 8], step 1/8 (reading C17).
+ *   acc_scale[L]: real value of one accumulator unit of layer l+1; used to convert the real
+ *     thresholds of mlpv_coverage_spec / mlpv_property into accumulator units by round-to-nearest-
+ *     even.  NULL means 1.0 (float numerics) or 2^-24 (Q4_12); required for INT8. */
+typedef struct {
+    mlpv_numeric numeric;
+    const int32_t *requant_shift;
+    const int16_t *sigmoid_knots;
+    const double *acc_scale;
+} mlpv_quant;
+
+/* Perturbation spaces (reading C14; the discrete stand-in for the restriction R of
+ * PAPER.md:453-461).  Index c of base input b names one candidate image:
+ *   TUPLE_REPLACE  (tuple t = 1 or 2) pixels i<j ranked lexicographically (i outer), q levels:
+ *                  c = rank(i,j) * q^2 + l_i * q + l_j;  x'_i = levels[l_i], x'_j = levels[l_j].
+ *   SUBSET_OFFSET  K strictly ascending pixels P, q levels, P[0] most significant digit:
+ *                  c = sum_k d_k q^(K-1-k);  x'_{P_k} = clamp(x_{P_k} + levels[d_k]) to [0, 4096]
+ *                  (Q4_12) or [0, 255] (INT8).  Fixed-point numerics only.
+ *   SUBSET_REPLACE as SUBSET_OFFSET with x'_{P_k} = levels[d_k].
+ *   PHILOX_LATTICE every pixel p takes level l_p in [0,15]: for 32-pixel block j,
+ *                  (w0..w3) = Philox4x32-10(counter = (c_lo, c_hi, b, j), key = (seed_lo, seed_hi)),
+ *                  pixel 32j + 8w + n takes nibble n (LSB first) of word w.
+ *                  BF16: x'_p = RNE_bf16(clamp(x_p + RNE_bf16(l_p*step + origin), 0, 1)), exact sums.
+ *                  INT8: x'_p = clamp(x_p + l_p*step + origin, 0, 255), integer step / origin.
+ *                  c < n_samples <= 2^32.  BF16 and INT8 numerics only.
+ * `levels` element type: float (FP32) | uint16 bf16 bits (BF16) | int16 (Q4_12, INT8).
+ * Every call processes the half-open index range [index_begin, index_end) of EVERY base input;
+ * disjoint ranges merge by sum / min / OR (mlpv_merge). */
+typedef enum {
+    MLPV_PERT_TUPLE_REPLACE = 0,
+    MLPV_PERT_SUBSET_OFFSET = 1,
+    MLPV_PERT_SUBSET_REPLACE = 2,
+    MLPV_PERT_PHILOX_LATTICE = 3
+} mlpv_pert_kind;
+
+typedef struct {
+    mlpv_pert_kind kind;
+    int32_t tuple;
+    int32_t n_pixels;
+    const int32_t *pixels;       /* host */
+    int32_t n_levels;
+    const void *levels;          /* host */
+    uint64_t seed;
+    uint64_t n_samples;
+    double lattice_step, lattice_origin;
+    uint64_t index_begin, index_end;
+} mlpv_pert;
+
+/* Safety property (reading C12).  Class = argmax of the logits, lowest index
+ * on ties; the base class is the argmax of the base image's own forward pass.
+ *   ARGMAX_UNCHANGED   violated iff class(x') != base class (the assert Y^d = N(I)).
+ *   TARGET_NEVER       violated iff class(x') == target.
+ *   THRESHOLD_LITERAL  violated iff y_D < V and y_i > V for some i != D (l_image_misclassified,
+ *                      existential reading), D = target, or the base class if target < 0;
+ *                      V in real units. */
+typedef enum {
+    MLPV_PROP_ARGMAX_UNCHANGED = 0,
+    MLPV_PROP_TARGET_NEVER = 1,
+    MLPV_PROP_THRESHOLD_LITERAL = 2
+} mlpv_prop_kind;
+
+typedef struct { mlpv_prop_kind kind; int32_t target; double V; } mlpv_property;
+
+/* Coverage.  For each configured pair p = (k, k+1), 1 <= k < L:
+ *   sc(n) = sign(u) != sign(u_base), sign(u) = [u >= 0];
+ *   vc(n) = !sc(n) && |u - u_base| >= d_value;                  (reading C5)
+ *   dc(k) = no sc in layer k && max_i |u - u_base| >= d_distance (reading C7, L-inf);
+ *   SS(i,j) = sc(k,i) && exactly one sc in layer k && sc(k+1,j);  SV(i,j) likewise with vc(k+1,j);
+ *   VS(j) = dc(k) && sc(k+1,j);  VV(j) = dc(k) && vc(k+1,j)   (column masks, reading C8).
+ * Word layout per pair (mlpv_coverage_layout): SS [n_k * wpr] | SV [n_k * wpr] | VS [wpr] |
+ * VV [wpr] uint32 words, wpr = ceil(n_{k+1} / 32), bit j of row i at word i*wpr + j/32, bit j%32.
+ * Float numerics: near_tie is the top-2 logit margin below which a verdict is flagged (C20);
+ * tau[L] (host, may be NULL = 1e-6 + 1e-5 * max|u_base| per layer, from this call's base
+ * traces) is the predicate-ambiguity width: a candidate with a sign, value or distance predicate
+ * of pair p within tau of its decision boundary contributes to cov_all only, not cov_certain. */
+typedef struct {
+    int32_t n_pairs;
+    const int32_t *lower_layer;  /* host [n_pairs] */
+    double d_value, d_distance;
+    double near_tie;
+    const double *tau;           /* host [L] or NULL */
+} mlpv_coverage_spec;
+
+/* Results: caller-allocated DEVICE buffers.  mlpv_check initialises them (counts 0, indices
+ * UINT64_MAX = none, words 0) on `stream` before accumulating.  first_cex is the lowest violating
+ * index of each base input's own space (reading C22).  Fixed-point numerics: flagged = 0,
+ * first_cex_unflagged = first_cex, cov_certain = cov_all. */
+typedef struct {
+    uint64_t *checked, *violated, *flagged;      /* [n_base] */
+    uint64_t *first_cex, *first_cex_unflagged;   /* [n_base] */
+    uint32_t *cov_all, *cov_certain;             /* [n_words] (may be NULL if n_pairs == 0) */
+} mlpv_result;
+
+/* Create a handle on `device`: validates the net (sizes >= 1, 1 <= L <= 8, n_L <= 16, finite
+ * values, numeric x activation built, fixed-point bound sum_j |w_j| x_max + |b| < 2^31 for every
+ * neuron) and deep-copies it to device memory it owns.  Caller buffers may be freed on return. */
+mlpv_status mlpv_create(const mlpv_net *net, const mlpv_quant *quant, int device, mlpv_t *out);
+
+/* Frees the handle's device memory (synchronises the device first). NULL is a no-op. */
+void mlpv_destroy(mlpv_t h);
+
+/* Message of the last error on h (or of the last mlpv_create / mlpv_decode failure on this
+ * thread if h == NULL); "" if none.  Owned by the library. */
+const char *mlpv_last_error(mlpv_t h);
+
+/* Coverage word count and per-pair word offsets (pair_offsets[4p + m], m = SS, SV, VS, VV). */
+mlpv_status mlpv_coverage_layout(mlpv_t h, const mlpv_coverage_spec *cov, size_t *n_words,
+                                 size_t *pair_offsets /* host [4 * n_pairs] or NULL */);
+
+/* Size of one base input's index space. */
+mlpv_status mlpv_space_size(mlpv_t h, const mlpv_pert *pert, uint64_t *size);
+
+/* The check (the data-parallel checkNN + covering methods).  base_inputs: device
+ * [n_base x n_0] in the input element type.  Enqueues all work on `stream` and returns without
+ * synchronising.  Work = n_base * (index_end - index_begin) candidates. */
+mlpv_status mlpv_check(mlpv_t h, const void *base_inputs, int32_t n_base, const mlpv_pert *pert,
+                       const mlpv_property *prop, const mlpv_coverage_spec *cov,
+                       const mlpv_result *res, void *stream);
+
+/* Parity hook: potentials of every layer (layers 1..L concatenated, T = n_1 + .. + n_L values per
+ * candidate) for candidates `indices` (device [n]) of base `base_id` of base_inputs (device
+ * [n_base x n_0]), computed by the same kernels and arithmetic as mlpv_check.  out: device
+ * [n x T], float (FP32, BF16) or int32 (Q4_12, INT8). */
+mlpv_status mlpv_eval(mlpv_t h, const void *base_inputs, int32_t n_base, int32_t base_id,
+                      const mlpv_pert *pert, const uint64_t *indices, int64_t n, void *out,
+                      void *stream);
+
+/* Counterexample reconstruction on the host: the candidate image `index` of base `base_id`
+ * (base_input and image_out: host [n_0] in the input element type). */
+mlpv_status mlpv_decode(mlpv_numeric numeric, const mlpv_pert *pert, const void *base_input,
+                        int32_t n_0, int32_t base_id, uint64_t index, void *image_out);
+
+/* Merge n_parts partial results of disjoint index ranges (device, laid out part-major:
+ * counts [n_parts x n_base], words [n_parts x n_words]) into `out` by sum / min / OR on `stream`.
+ * Used after the cross-GPU all-gather and for resumed sub-range runs. */
+mlpv_status mlpv_merge(const mlpv_result *parts, int32_t n_parts, int32_t n_base, size_t n_words,
+                       const mlpv_result *out, void *stream);
+
+/* Neuron coverage (reading C9): covered[4 * T] bytes (device; method-major,
+ * T = n_1 + .. + n_L, 1 = covered) and counts[4] (device uint32: covered neurons per method) from
+ * the pair words.  A neuron is covered iff it is an endpoint of a covered pair; a VS / VV column j
+ * covers every neuron of layer k and n_{k+1,j}. */
+mlpv_status mlpv_neuron_coverage(mlpv_t h, const mlpv_coverage_spec *cov, const uint32_t *words,
+                                 uint8_t *covered, uint32_t *counts, void *stream);
+
+/* Library version string. */
+const char *mlpv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLPV_H */

@@ -1,0 +1,640 @@
+// k_small.cu -- CUDA-core kernels for subset / tuple perturbation spaces of small nets
+// (BASELINE configs 1-3) and the per-base prologue (K0) shared by every path.
+//
+// Hot path per candidate (one thread = one candidate):
+//   a2 decode the index (pair rank / mixed radix, reading C14)
+//   a4 layer 1 as a rank-|S| update of the base potentials, u1 = u1_base + sum_k Delta[k][l_k]
+//      (Eq. 1; exact in Z/2^32 for the fixed-point numerics)
+//   a5/a6 hidden activation (Eq. 2 sigmoid, PL-sigmoid C17, ReLU+requant C18) and the remaining
+//      dense layers on CUDA cores (FFMA / IMAD / DP4A) with weights resident in shared memory
+//   a7 argmax (lowest index on ties), top-2 margin, property
+//   a8 sign / value / distance predicates and SS / SV / VS / VV pair bits
+//   a9 block-level reduction of counts, lowest-index counterexample and coverage words.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mlpv_internal.cuh"
+
+namespace mlpv {
+
+// --------------------------------------------------------------------------- numeric traits
+template <int NUM> struct NT;
+template <> struct NT<MLPV_NUM_FP32> { using P = float; };   // potential type
+template <> struct NT<MLPV_NUM_Q4_12> { using P = int32_t; };
+template <> struct NT<MLPV_NUM_INT8> { using P = int32_t; };
+
+__device__ __forceinline__ float wload_f(const void* W, int numeric, size_t i) {
+  if (numeric == MLPV_NUM_FP32) return static_cast<const float*>(W)[i];
+  // bf16 bits -> fp32 (exact)
+  return __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(W)[i]) << 16);
+}
+__device__ __forceinline__ int32_t wload_i(const void* W, int numeric, size_t i) {
+  if (numeric == MLPV_NUM_Q4_12) return static_cast<const int16_t*>(W)[i];
+  return static_cast<const int8_t*>(W)[i];
+}
+__device__ __forceinline__ float in_f(const void* x, int numeric, size_t i) {
+  if (numeric == MLPV_NUM_FP32) return static_cast<const float*>(x)[i];
+  return __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(x)[i]) << 16);
+}
+__device__ __forceinline__ int32_t in_i(const void* x, int numeric, size_t i) {
+  if (numeric == MLPV_NUM_Q4_12) return static_cast<const int16_t*>(x)[i];
+  return static_cast<const uint8_t*>(x)[i];
+}
+__device__ __forceinline__ float lvl_f(const void* lv, int numeric, int q) {
+  if (numeric == MLPV_NUM_FP32) return static_cast<const float*>(lv)[q];
+  return __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(lv)[q]) << 16);
+}
+__device__ __forceinline__ int32_t lvl_i(const void* lv, int q) { return static_cast<const int16_t*>(lv)[q]; }
+
+// C17 piecewise-linear sigmoid on a Q4.12 potential
+__device__ __forceinline__ int32_t pl_sigmoid(const int16_t* T, int32_t u16) {
+  int32_t t = u16 + 32768;
+  int32_t i = t >> 9, f = t & 511;
+  int32_t y0 = T[i], y1 = T[i + 1];
+  return y0 + (((y1 - y0) * f + 256) >> 9);
+}
+
+// hidden activation of a fixed-point potential (C16 / C18)
+__device__ __forceinline__ int32_t act_fixed(int numeric, int act, int32_t acc, int sh, const int16_t* knots) {
+  if (numeric == MLPV_NUM_Q4_12) {
+    int32_t u16 = (acc + 2048) >> 12;                 // arithmetic shift = floor; round half up
+    u16 = max(-32768, min(32767, u16));
+    return act == MLPV_ACT_PL_SIGMOID ? pl_sigmoid(knots, u16) : max(u16, 0);
+  }
+  int32_t r = sh > 0 ? (1 << (sh - 1)) : 0;
+  return max(0, min(255, (acc + r) >> sh));
+}
+
+__device__ __forceinline__ float act_float(int act, float u) {
+  return act == MLPV_ACT_SIGMOID ? 1.0f / (1.0f + expf(-u)) : fmaxf(u, 0.0f);   // Eq. 2
+}
+
+// --------------------------------------------------------------------------- K0: base prologue
+// One CTA per base input: full forward of the base image (same arithmetic as the candidates for
+// the fixed-point numerics, fp32 for the float numerics), base class, and the layer-1 delta
+// tables Delta[s][l][i] = W1[i, p_s] * (x'_{p_s}(l) - x_{p_s}) of subset / tuple spaces.
+__global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, const void* levels, BaseWS ws) {
+  extern __shared__ float sm_f[];
+  const int b = blockIdx.x;
+  const int n0 = net.sizes[0];
+  int maxw = 0;
+  for (int l = 0; l <= net.L; l++) maxw = max(maxw, net.sizes[l]);
+  float* hf = sm_f;                               // [maxw]
+  float* hn = sm_f + maxw;                        // [maxw]
+  int32_t* hi = reinterpret_cast<int32_t*>(sm_f);
+  int32_t* hin = reinterpret_cast<int32_t*>(sm_f + maxw);
+  const bool fixed = net.numeric == MLPV_NUM_Q4_12 || net.numeric == MLPV_NUM_INT8;
+  const size_t in_sz = net.numeric == MLPV_NUM_FP32 ? 4 : (net.numeric == MLPV_NUM_INT8 ? 1 : 2);
+  const char* x = static_cast<const char*>(bases) + in_sz * (size_t)n0 * b;
+  for (int j = threadIdx.x; j < n0; j += blockDim.x) {
+    if (fixed) hi[j] = in_i(x, net.numeric, j);
+    else hf[j] = in_f(x, net.numeric, j);
+  }
+  __syncthreads();
+  const int T = net.trace_len;
+  for (int l = 1; l <= net.L; l++) {
+    const int nl = net.sizes[l], fan = net.sizes[l - 1];
+    for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+      if (fixed) {
+        int32_t acc = static_cast<const int32_t*>(net.b[l - 1])[i];
+        for (int j = 0; j < fan; j++) acc += wload_i(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hi[j];
+        static_cast<int32_t*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
+        if (l < net.L) hin[i] = act_fixed(net.numeric, net.act, acc, net.shift[l - 1], net.knots);
+      } else {
+        float acc = 0.f;
+        for (int j = 0; j < fan; j++) acc = fmaf(wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j), hf[j], acc);
+        acc += static_cast<const float*>(net.b[l - 1])[i];
+        static_cast<float*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
+        if (l < net.L) hn[i] = act_float(net.act, acc);
+      }
+    }
+    __syncthreads();
+    if (l < net.L) {
+      for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+        if (fixed) hi[i] = hin[i]; else hf[i] = hn[i];
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int nL = net.sizes[net.L];
+    int c = 0;
+    if (fixed) {
+      const int32_t* y = static_cast<const int32_t*>(ws.trace) + (size_t)b * T + net.loff[net.L];
+      for (int i = 1; i < nL; i++) if (y[i] > y[c]) c = i;
+    } else {
+      const float* y = static_cast<const float*>(ws.trace) + (size_t)b * T + net.loff[net.L];
+      for (int i = 1; i < nL; i++) if (y[i] > y[c]) c = i;
+    }
+    ws.cls[b] = c;
+  }
+  // delta tables (subset / tuple spaces only)
+  if (ws.delta == nullptr) return;
+  const int n1 = net.sizes[1], q = pert.n_levels, S = ws.S;
+  const size_t per_base = (size_t)S * q * n1;
+  for (size_t e = threadIdx.x; e < per_base; e += blockDim.x) {
+    const int i = (int)(e % n1);
+    const int lq = (int)((e / n1) % q);
+    const int s = (int)(e / ((size_t)n1 * q));
+    const int p = pert.kind == MLPV_PERT_TUPLE_REPLACE ? s : pert.pixels[s];
+    if (fixed) {
+      const int32_t xp = in_i(x, net.numeric, p);
+      int32_t xn;
+      if (pert.kind == MLPV_PERT_SUBSET_OFFSET) {
+        const int32_t hi_ = net.numeric == MLPV_NUM_Q4_12 ? 4096 : 255;
+        xn = max(0, min(hi_, xp + lvl_i(levels, lq)));
+      } else {
+        xn = lvl_i(levels, lq);
+      }
+      static_cast<int32_t*>(ws.delta)[(size_t)b * per_base + e] = wload_i(net.W[0], net.numeric, (size_t)i * n0 + p) * (xn - xp);
+    } else {
+      const float xp = in_f(x, net.numeric, p);
+      const float xn = lvl_f(levels, net.numeric, lq);
+      static_cast<float*>(ws.delta)[(size_t)b * per_base + e] = wload_f(net.W[0], net.numeric, (size_t)i * n0 + p) * (xn - xp);
+    }
+  }
+}
+
+cudaError_t launch_base_prologue(const DevNet& net, const void* bases, int n_base, const DevPert& pert,
+                                 const void* levels_dev, BaseWS ws, cudaStream_t st) {
+  int maxw = 0;
+  for (int l = 0; l <= net.L; l++) maxw = maxw > net.sizes[l] ? maxw : net.sizes[l];
+  size_t smem = sizeof(float) * 2 * (size_t)maxw;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_base_prologue, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_base_prologue<<<n_base, 256, smem, st>>>(net, bases, pert, levels_dev, ws);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------- K1: small-net kernel
+struct SmallArgs {
+  DevNet net;
+  DevPert pert;
+  DevProp prop;
+  DevCov cov;
+  DevResult res;
+  BaseWS ws;
+  int n_base;
+  const uint64_t* eval_idx;   // eval mode: candidate indices of base eval_base
+  int64_t eval_n;
+  int eval_base;
+  void* eval_out;             // [eval_n x T]
+  int tbl_in_smem;            // delta table of the block's base staged in smem
+};
+
+__device__ __forceinline__ uint32_t dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, int32_t c) {
+  int32_t d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_u8x4), "r"(b_s8x4), "r"(c));
+  return (uint32_t)d;
+}
+
+// pair rank -> (i, j), i < j < n0, lexicographic (i outer)
+__device__ __forceinline__ void unrank_pair(uint32_t pr, int n0, int& i, int& j) {
+  // cum(i) = i*(2*n0 - i - 1)/2 pairs precede row i
+  const double a = 2.0 * n0 - 1.0;
+  int ii = (int)floor((a - sqrt(a * a - 8.0 * (double)pr)) * 0.5);
+  ii = max(0, min(n0 - 2, ii));
+  auto cum = [n0](int r) -> uint32_t { return (uint32_t)((int64_t)r * (2 * n0 - r - 1) / 2); };
+  while (ii + 1 <= n0 - 2 && cum(ii + 1) <= pr) ii++;
+  while (ii > 0 && cum(ii) > pr) ii--;
+  i = ii;
+  j = ii + 1 + (int)(pr - cum(ii));
+}
+
+template <typename P>
+__device__ __forceinline__ bool sgn(P u) { return u >= P(0); }
+
+// Coverage of one pair (k, k+1) for one candidate; bits OR-ed into the block's smem words.
+// lo/up: candidate potentials; blo/bup: base potentials (smem).  Float numerics also evaluate
+// the ambiguity of the predicates used (reading C20) to decide cov_certain.
+template <typename P, int ML, int MU>
+__device__ __forceinline__ void cover_pair(const P (&lo)[ML], const P (&up)[MU], const P* blo, const P* bup,
+                                           int nlo, int nup, P tg, P th, float tau_lo, float tau_up,
+                                           uint32_t* sm_all, uint32_t* sm_cert, const uint32_t off[4], bool fl) {
+  int nsc = 0, istar = -1;
+  P linf = P(0);
+#pragma unroll
+  for (int i = 0; i < ML; i++) {
+    if (i < nlo) {
+      const bool c = sgn(lo[i]) != sgn(blo[i]);
+      if (c) { if (istar < 0) istar = i; nsc++; }
+      P d = lo[i] - blo[i];
+      d = d < P(0) ? -d : d;
+      linf = d > linf ? d : linf;
+    }
+  }
+  const bool dc = (nsc == 0) && (linf >= th);
+  if (!(nsc == 1 || dc)) return;           // no cover of this pair can hold
+  // ambiguity (float numerics)
+  bool amb = false;
+  if (fl) {
+#pragma unroll
+    for (int i = 0; i < ML; i++)
+      if (i < nlo && (fabsf((float)lo[i]) < tau_lo || fabsf((float)blo[i]) < tau_lo)) amb = true;
+    if (nsc == 0 && fabsf((float)(linf - th)) < tau_lo) amb = true;
+  }
+  const int wpr = (nup + 31) >> 5;
+#pragma unroll
+  for (int j = 0; j < MU; j++) {
+    if (j < nup) {
+      const bool sc = sgn(up[j]) != sgn(bup[j]);
+      P d = up[j] - bup[j];
+      d = d < P(0) ? -d : d;
+      const bool vc = !sc && d >= tg;
+      if (fl && (fabsf((float)up[j]) < tau_up || fabsf((float)bup[j]) < tau_up || fabsf((float)(d - tg)) < tau_up)) amb = true;
+      const uint32_t bit = 1u << (j & 31);
+      const int wj = j >> 5;
+      if (nsc == 1) {
+        if (sc) atomicOr(&sm_all[off[0] + istar * wpr + wj], bit);
+        if (vc) atomicOr(&sm_all[off[1] + istar * wpr + wj], bit);
+      } else {
+        if (sc) atomicOr(&sm_all[off[2] + wj], bit);
+        if (vc) atomicOr(&sm_all[off[3] + wj], bit);
+      }
+    }
+  }
+  if (fl && !amb) {
+    // replay the same bits into the certain set
+#pragma unroll
+    for (int j = 0; j < MU; j++) {
+      if (j < nup) {
+        const bool sc = sgn(up[j]) != sgn(bup[j]);
+        P d = up[j] - bup[j];
+        d = d < P(0) ? -d : d;
+        const bool vc = !sc && d >= tg;
+        const uint32_t bit = 1u << (j & 31);
+        const int wj = j >> 5;
+        if (nsc == 1) {
+          if (sc) atomicOr(&sm_cert[off[0] + istar * wpr + wj], bit);
+          if (vc) atomicOr(&sm_cert[off[1] + istar * wpr + wj], bit);
+        } else {
+          if (sc) atomicOr(&sm_cert[off[2] + wj], bit);
+          if (vc) atomicOr(&sm_cert[off[3] + wj], bit);
+        }
+      }
+    }
+  }
+}
+
+// Dense layer l >= 2 on CUDA cores: u[i] = b[i] + sum_j W[i][j] h[j]
+template <int NUM, int MI, int MO>
+__device__ __forceinline__ void dense(typename NT<NUM>::P (&u)[MO], const float (&hf)[MI], const int32_t (&hi)[MI],
+                                      const uint32_t (&hp)[(MI + 3) / 4], const void* Wsm, const void* bsm,
+                                      int nin, int nout) {
+  if constexpr (NUM == MLPV_NUM_FP32) {
+    const float* W = static_cast<const float*>(Wsm);
+#pragma unroll
+    for (int i = 0; i < MO; i++) {
+      if (i < nout) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < MI; j++) if (j < nin) acc = fmaf(W[i * nin + j], hf[j], acc);
+        u[i] = acc + static_cast<const float*>(bsm)[i];
+      }
+    }
+  } else if constexpr (NUM == MLPV_NUM_Q4_12) {
+    const int16_t* W = static_cast<const int16_t*>(Wsm);
+#pragma unroll
+    for (int i = 0; i < MO; i++) {
+      if (i < nout) {
+        int32_t acc = static_cast<const int32_t*>(bsm)[i];
+#pragma unroll
+        for (int j = 0; j < MI; j++) if (j < nin) acc += (int32_t)W[i * nin + j] * hi[j];
+        u[i] = acc;
+      }
+    }
+  } else {
+    // int8 rows packed as s8x4 words, row stride (nin+3)/4 words
+    const uint32_t* W = static_cast<const uint32_t*>(Wsm);
+    const int wpr = (nin + 3) >> 2;
+#pragma unroll
+    for (int i = 0; i < MO; i++) {
+      if (i < nout) {
+        int32_t acc = static_cast<const int32_t*>(bsm)[i];
+#pragma unroll
+        for (int w = 0; w < (MI + 3) / 4; w++) if (w < wpr) acc = (int32_t)dp4a_us(hp[w], W[i * wpr + w], acc);
+        u[i] = acc;
+      }
+    }
+  }
+}
+
+template <int NUM, int MI>
+__device__ __forceinline__ void activate(const typename NT<NUM>::P (&u)[MI], float (&hf)[MI], int32_t (&hi)[MI],
+                                         uint32_t (&hp)[(MI + 3) / 4], int n, int act, int sh, const int16_t* knots) {
+  if constexpr (NUM == MLPV_NUM_FP32) {
+#pragma unroll
+    for (int i = 0; i < MI; i++) hf[i] = i < n ? act_float(act, u[i]) : 0.f;
+  } else {
+#pragma unroll
+    for (int i = 0; i < MI; i++) hi[i] = i < n ? act_fixed(NUM, act, u[i], sh, knots) : 0;
+    if constexpr (NUM == MLPV_NUM_INT8) {
+#pragma unroll
+      for (int w = 0; w < (MI + 3) / 4; w++) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) if (4 * w + k < MI) v |= (uint32_t)hi[4 * w + k] << (8 * k);
+        hp[w] = v;
+      }
+    }
+  }
+}
+
+// M1..M3: compile-time maxima of n_1..n_3 (register arrays); L in {2, 3}.
+template <int NUM, int L, int M1, int M2, int M3>
+__global__ void __launch_bounds__(256) k_small(SmallArgs a) {
+  using P = typename NT<NUM>::P;
+  constexpr bool FL = NUM == MLPV_NUM_FP32;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const DevNet& net = a.net;
+  const int T = net.trace_len;
+  const int n0 = net.sizes[0], n1 = net.sizes[1], n2 = net.sizes[2], n3 = L == 3 ? net.sizes[3] : 0;
+  const int nL = net.sizes[L];
+  const bool eval = a.eval_idx != nullptr;
+  const int b = eval ? a.eval_base : blockIdx.y;
+  const int q = a.pert.n_levels;
+
+  // ---- shared-memory carve-up
+  uint8_t* sp = smem;
+  auto take = [&](size_t bytes) { uint8_t* r = sp; sp += (bytes + 15) & ~size_t(15); return r; };
+  P* s_base = reinterpret_cast<P*>(take(sizeof(P) * T));
+  void* s_W2 = take(NUM == MLPV_NUM_FP32 ? 4 * (size_t)n2 * n1 : (NUM == MLPV_NUM_Q4_12 ? 2 * (size_t)n2 * n1 : 4 * (size_t)n2 * ((n1 + 3) / 4)));
+  void* s_b2 = take(4 * (size_t)n2);
+  void* s_W3 = take(L == 3 ? (NUM == MLPV_NUM_FP32 ? 4 * (size_t)n3 * n2 : (NUM == MLPV_NUM_Q4_12 ? 2 * (size_t)n3 * n2 : 4 * (size_t)n3 * ((n2 + 3) / 4))) : 0);
+  void* s_b3 = take(L == 3 ? 4 * (size_t)n3 : 0);
+  int16_t* s_knots = reinterpret_cast<int16_t*>(take(net.knots ? 129 * 2 : 0));
+  uint32_t* s_cov = reinterpret_cast<uint32_t*>(take(eval ? 0 : 4 * (size_t)a.cov.n_words * (FL ? 2 : 1)));
+  const size_t per_base = (size_t)a.ws.S * q * n1;
+  P* s_delta = reinterpret_cast<P*>(take(a.tbl_in_smem ? sizeof(P) * per_base : 0));
+  __shared__ unsigned long long s_cnt[3];
+  __shared__ unsigned long long s_cex[2];
+
+  // ---- stage per-base data
+  for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] = static_cast<const P*>(a.ws.trace)[(size_t)b * T + t];
+  {
+    if constexpr (NUM == MLPV_NUM_FP32) {
+      for (int t = threadIdx.x; t < n2 * n1; t += blockDim.x) static_cast<float*>(s_W2)[t] = static_cast<const float*>(net.W[1])[t];
+      if (L == 3) for (int t = threadIdx.x; t < n3 * n2; t += blockDim.x) static_cast<float*>(s_W3)[t] = static_cast<const float*>(net.W[2])[t];
+    } else if constexpr (NUM == MLPV_NUM_Q4_12) {
+      for (int t = threadIdx.x; t < n2 * n1; t += blockDim.x) static_cast<int16_t*>(s_W2)[t] = static_cast<const int16_t*>(net.W[1])[t];
+      if (L == 3) for (int t = threadIdx.x; t < n3 * n2; t += blockDim.x) static_cast<int16_t*>(s_W3)[t] = static_cast<const int16_t*>(net.W[2])[t];
+    } else {
+      const int w1 = (n1 + 3) / 4, w2 = (n2 + 3) / 4;
+      for (int t = threadIdx.x; t < n2 * w1; t += blockDim.x) {
+        const int i = t / w1, w = t % w1;
+        uint32_t v = 0;
+        for (int k = 0; k < 4; k++) if (4 * w + k < n1) v |= (uint32_t)(uint8_t)static_cast<const int8_t*>(net.W[1])[i * n1 + 4 * w + k] << (8 * k);
+        static_cast<uint32_t*>(s_W2)[t] = v;
+      }
+      if (L == 3)
+        for (int t = threadIdx.x; t < n3 * w2; t += blockDim.x) {
+          const int i = t / w2, w = t % w2;
+          uint32_t v = 0;
+          for (int k = 0; k < 4; k++) if (4 * w + k < n2) v |= (uint32_t)(uint8_t)static_cast<const int8_t*>(net.W[2])[i * n2 + 4 * w + k] << (8 * k);
+          static_cast<uint32_t*>(s_W3)[t] = v;
+        }
+    }
+    for (int t = threadIdx.x; t < n2; t += blockDim.x) static_cast<uint32_t*>(s_b2)[t] = static_cast<const uint32_t*>(net.b[1])[t];
+    if (L == 3) for (int t = threadIdx.x; t < n3; t += blockDim.x) static_cast<uint32_t*>(s_b3)[t] = static_cast<const uint32_t*>(net.b[2])[t];
+    if (net.knots) for (int t = threadIdx.x; t < 129; t += blockDim.x) s_knots[t] = net.knots[t];
+    if (!eval) for (int t = threadIdx.x; t < (int)a.cov.n_words * (FL ? 2 : 1); t += blockDim.x) s_cov[t] = 0;
+    if (a.tbl_in_smem)
+      for (size_t t = threadIdx.x; t < per_base; t += blockDim.x) s_delta[t] = static_cast<const P*>(a.ws.delta)[(size_t)b * per_base + t];
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_cex[threadIdx.x] = kNone;
+  }
+  __syncthreads();
+  const P* delta = a.tbl_in_smem ? s_delta : static_cast<const P*>(a.ws.delta) + (size_t)b * per_base;
+  const int base_cls = a.ws.cls[b];
+  P tg[3], th[3];
+  float tau[3];
+#pragma unroll
+  for (int l = 0; l < 3; l++) {
+    if constexpr (FL) { tg[l] = a.cov.tg_f[l]; th[l] = a.cov.th_f[l]; }
+    else { tg[l] = (P)a.cov.tg_i[l]; th[l] = (P)a.cov.th_i[l]; }
+    tau[l] = a.cov.tau_dev ? a.cov.tau_dev[l] : a.cov.tau[l];
+  }
+  bool pair_on[2] = {false, false};
+  uint32_t poff[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+  for (int p = 0; p < a.cov.n_pairs; p++) {
+    const int k = a.cov.lower[p];
+    if (k >= 1 && k <= 2) {
+      pair_on[k - 1] = true;
+      for (int m = 0; m < 4; m++) poff[k - 1][m] = a.cov.off[p][m];
+    }
+  }
+  const uint64_t begin = a.pert.begin, end = a.pert.end;
+  const uint64_t nwork = eval ? (uint64_t)a.eval_n : end - begin;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long my_chk = 0, my_v = 0, my_f = 0, my_cex = kNone, my_cexu = kNone;
+
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nwork; t += stride) {
+    const uint64_t c = eval ? a.eval_idx[t] : begin + t;
+    // ---- a2 + a4: decode and incremental layer 1
+    P U1[M1], U2[M2], U3[M3 > 0 ? M3 : 1];
+#pragma unroll
+    for (int i = 0; i < M1; i++) U1[i] = i < n1 ? s_base[i] : P(0);
+    if (a.pert.kind == MLPV_PERT_TUPLE_REPLACE) {
+      if (a.pert.tuple == 2) {
+        const uint32_t pr = (uint32_t)(c / a.pert.q2);
+        const uint32_t rem = (uint32_t)(c % a.pert.q2);
+        const int li = rem / q, lj = rem % q;
+        int pi, pj;
+        unrank_pair(pr, n0, pi, pj);
+        const P* d0 = delta + ((size_t)pi * q + li) * n1;
+        const P* d1 = delta + ((size_t)pj * q + lj) * n1;
+#pragma unroll
+        for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i] + d1[i];
+      } else {
+        const int pi = (int)(c / q), li = (int)(c % q);
+        const P* d0 = delta + ((size_t)pi * q + li) * n1;
+#pragma unroll
+        for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i];
+      }
+    } else {
+      uint64_t cc = c;
+      for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
+        const int d = (int)(cc % (uint64_t)q);
+        cc /= (uint64_t)q;
+        const P* dk = delta + ((size_t)k * q + d) * n1;
+#pragma unroll
+        for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+      }
+    }
+    // ---- a5/a6: hidden activations and dense layers
+    {
+      float h1f[M1]; int32_t h1i[M1]; uint32_t h1p[(M1 + 3) / 4];
+      activate<NUM, M1>(U1, h1f, h1i, h1p, n1, net.act, net.shift[0], s_knots);
+      dense<NUM, M1, M2>(U2, h1f, h1i, h1p, s_W2, s_b2, n1, n2);
+    }
+    if constexpr (L == 3) {
+      float h2f[M2]; int32_t h2i[M2]; uint32_t h2p[(M2 + 3) / 4];
+      activate<NUM, M2>(U2, h2f, h2i, h2p, n2, net.act, net.shift[1], s_knots);
+      dense<NUM, M2, M3>(U3, h2f, h2i, h2p, s_W3, s_b3, n2, n3);
+    }
+    if (eval) {
+      P* o = static_cast<P*>(a.eval_out) + t * T;
+#pragma unroll
+      for (int i = 0; i < M1; i++) if (i < n1) o[net.loff[1] + i] = U1[i];
+#pragma unroll
+      for (int i = 0; i < M2; i++) if (i < n2) o[net.loff[2] + i] = U2[i];
+      if constexpr (L == 3) {
+#pragma unroll
+        for (int i = 0; i < M3; i++) if (i < n3) o[net.loff[3] + i] = U3[i];
+      }
+      continue;
+    }
+    // ---- a7: argmax, margin, property
+    const P* Y = (L == 3) ? U3 : U2;
+    constexpr int MY = (L == 3) ? (M3 > 0 ? M3 : 1) : M2;
+    int cls = 0;
+    P top1 = Y[0];
+#pragma unroll
+    for (int i = 1; i < MY; i++) if (i < nL && Y[i] > top1) { top1 = Y[i]; cls = i; }
+    bool viol, flag = false;
+    if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+      const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
+      const P V = FL ? (P)a.prop.V_f : (P)a.prop.V_i;
+      bool any = false;
+      P yD = Y[0];
+#pragma unroll
+      for (int i = 0; i < MY; i++) {
+        if (i < nL) {
+          if (i == D) yD = Y[i];
+          if (i != D && Y[i] > V) any = true;
+          if (FL && fabsf((float)(Y[i] - V)) < a.cov.near_tie) flag = true;
+        }
+      }
+      viol = (yD < V) && any;
+    } else {
+      if constexpr (FL) {
+        float top2 = -3.0e38f;
+#pragma unroll
+        for (int i = 0; i < MY; i++) if (i < nL && i != cls && Y[i] > top2) top2 = Y[i];
+        if (nL > 1 && (float)top1 - top2 < a.cov.near_tie) flag = true;
+      }
+      viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? (cls == a.prop.target) : (cls != base_cls);
+    }
+    my_chk++;
+    if (flag) my_f++;
+    if (viol) {
+      my_v++;
+      if (c < my_cex) my_cex = c;
+      if (!flag && c < my_cexu) my_cexu = c;
+    }
+    // ---- a8: coverage
+    uint32_t* s_cert = FL ? s_cov + a.cov.n_words : s_cov;
+    if (pair_on[0])
+      cover_pair<P, M1, M2>(U1, U2, s_base + net.loff[1], s_base + net.loff[2], n1, n2, tg[1], th[0], tau[0], tau[1],
+                            s_cov, s_cert, poff[0], FL);
+    if constexpr (L == 3) {
+      if (pair_on[1])
+        cover_pair<P, M2, (M3 > 0 ? M3 : 1)>(U2, U3, s_base + net.loff[2], s_base + net.loff[3], n2, n3, tg[2], th[1],
+                                             tau[1], tau[2], s_cov, s_cert, poff[1], FL);
+    }
+  }
+  if (eval) return;
+  // ---- a9: block reduction
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    my_chk += __shfl_xor_sync(full, my_chk, o);
+    my_v += __shfl_xor_sync(full, my_v, o);
+    my_f += __shfl_xor_sync(full, my_f, o);
+    unsigned long long x = __shfl_xor_sync(full, my_cex, o);
+    my_cex = x < my_cex ? x : my_cex;
+    x = __shfl_xor_sync(full, my_cexu, o);
+    my_cexu = x < my_cexu ? x : my_cexu;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_cnt[0], my_chk);
+    atomicAdd(&s_cnt[1], my_v);
+    atomicAdd(&s_cnt[2], my_f);
+    atomicMin(&s_cex[0], my_cex);
+    atomicMin(&s_cex[1], my_cexu);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.res.checked[b]), s_cnt[0]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.res.violated[b]), s_cnt[1]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.res.flagged[b]), s_cnt[2]);
+    if (s_cex[0] != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&a.res.first_cex[b]), s_cex[0]);
+    if (s_cex[1] != kNone) atomicMin(reinterpret_cast<unsigned long long*>(&a.res.first_cex_unflagged[b]), s_cex[1]);
+  }
+  for (int w = threadIdx.x; w < (int)a.cov.n_words; w += blockDim.x) {
+    if (s_cov[w]) atomicOr(&a.res.cov_all[w], s_cov[w]);
+    if (FL) { if (s_cov[a.cov.n_words + w]) atomicOr(&a.res.cov_certain[w], s_cov[a.cov.n_words + w]); }
+    else if (s_cov[w]) atomicOr(&a.res.cov_certain[w], s_cov[w]);
+  }
+}
+
+template <int NUM, int L, int M1, int M2, int M3>
+static cudaError_t run_small(SmallArgs& a, int num_sms, cudaStream_t st) {
+  using P = typename NT<NUM>::P;
+  const DevNet& net = a.net;
+  const int n1 = net.sizes[1], n2 = net.sizes[2], n3 = L == 3 ? net.sizes[3] : 0;
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  size_t smem = al(sizeof(P) * net.trace_len);
+  smem += al(NUM == MLPV_NUM_FP32 ? 4 * (size_t)n2 * n1 : (NUM == MLPV_NUM_Q4_12 ? 2 * (size_t)n2 * n1 : 4 * (size_t)n2 * ((n1 + 3) / 4)));
+  smem += al(4 * (size_t)n2);
+  if (L == 3) {
+    smem += al(NUM == MLPV_NUM_FP32 ? 4 * (size_t)n3 * n2 : (NUM == MLPV_NUM_Q4_12 ? 2 * (size_t)n3 * n2 : 4 * (size_t)n3 * ((n2 + 3) / 4)));
+    smem += al(4 * (size_t)n3);
+  }
+  if (net.knots) smem += al(129 * 2);
+  const bool eval = a.eval_idx != nullptr;
+  if (!eval) smem += al(4 * (size_t)a.cov.n_words * (NUM == MLPV_NUM_FP32 ? 2 : 1));
+  const size_t tbl = sizeof(P) * (size_t)a.ws.S * a.pert.n_levels * n1;
+  a.tbl_in_smem = (smem + al(tbl) <= 160 * 1024) ? 1 : 0;
+  if (a.tbl_in_smem) smem += al(tbl);
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  auto kern = k_small<NUM, L, M1, M2, M3>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int threads = 256;
+  dim3 grid;
+  if (eval) {
+    grid = dim3((unsigned)((a.eval_n + threads - 1) / threads), 1);
+  } else {
+    const uint64_t range = a.pert.end - a.pert.begin;
+    const uint64_t need = (range + threads * 8 - 1) / (threads * 8);     // >= 8 candidates per thread
+    const int want = (4 * num_sms + a.n_base - 1) / a.n_base;             // ~4 waves of CTAs overall
+    uint64_t gx = need < (uint64_t)want ? need : (uint64_t)want;
+    if (gx < 1) gx = 1;
+    grid = dim3((unsigned)gx, (unsigned)a.n_base);
+  }
+  if (grid.x == 0) return cudaSuccess;
+  kern<<<grid, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_small(const DevNet& net, const void* bases, int n_base, const DevPert& pert,
+                         const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
+                         const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
+                         int num_sms, cudaStream_t st, bool* supported) {
+  (void)bases;
+  SmallArgs a{};
+  a.net = net; a.pert = pert; a.prop = prop; a.cov = cov; a.res = res; a.ws = ws; a.n_base = n_base;
+  a.eval_idx = eval_idx; a.eval_n = eval_n; a.eval_base = eval_base; a.eval_out = eval_out;
+  *supported = true;
+  const int L = net.L, n1 = net.sizes[1], n2 = net.sizes[2], n3 = L >= 3 ? net.sizes[3] : 0;
+  if (L == 2 && n1 <= 16 && n2 <= 16) {
+    if (net.numeric == MLPV_NUM_FP32) return run_small<MLPV_NUM_FP32, 2, 16, 16, 0>(a, num_sms, st);
+    if (net.numeric == MLPV_NUM_Q4_12) return run_small<MLPV_NUM_Q4_12, 2, 16, 16, 0>(a, num_sms, st);
+    if (net.numeric == MLPV_NUM_INT8) return run_small<MLPV_NUM_INT8, 2, 16, 16, 0>(a, num_sms, st);
+  }
+  if (L == 3 && n1 <= 16 && n2 <= 16 && n3 <= 16) {
+    if (net.numeric == MLPV_NUM_FP32) return run_small<MLPV_NUM_FP32, 3, 16, 16, 16>(a, num_sms, st);
+    if (net.numeric == MLPV_NUM_Q4_12) return run_small<MLPV_NUM_Q4_12, 3, 16, 16, 16>(a, num_sms, st);
+    if (net.numeric == MLPV_NUM_INT8) return run_small<MLPV_NUM_INT8, 3, 16, 16, 16>(a, num_sms, st);
+  }
+  if (L == 3 && n1 <= 64 && n2 <= 32 && n3 <= 16 && net.numeric == MLPV_NUM_INT8)
+    return run_small<MLPV_NUM_INT8, 3, 64, 32, 16>(a, num_sms, st);
+  *supported = false;
+  return cudaSuccess;
+}
+
+}  // namespace mlpv

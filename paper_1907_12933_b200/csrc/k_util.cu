@@ -1,0 +1,132 @@
+// k_util.cu -- small device kernels around the check: result initialisation, merge of partial
+// results (cross-GPU all-gather and resumed sub-ranges), neuron coverage
+// and the float ambiguity widths tau (reading C20).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mlpv_internal.cuh"
+
+namespace mlpv {
+
+__global__ void k_init_result(DevResult r, int n_base, uint32_t n_words) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n_base) {
+    r.checked[t] = 0; r.violated[t] = 0; r.flagged[t] = 0;
+    r.first_cex[t] = kNone; r.first_cex_unflagged[t] = kNone;
+  }
+  for (uint32_t w = t; w < n_words; w += gridDim.x * blockDim.x) {
+    if (r.cov_all) r.cov_all[w] = 0;
+    if (r.cov_certain) r.cov_certain[w] = 0;
+  }
+}
+
+cudaError_t launch_init_result(const DevResult& r, int n_base, uint32_t n_words, cudaStream_t st) {
+  const int n = n_base > (int)n_words ? n_base : (int)n_words;
+  const int blocks = (n + 255) / 256 > 0 ? ((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024) : 1;
+  k_init_result<<<blocks, 256, 0, st>>>(r, n_base, n_words);
+  return cudaGetLastError();
+}
+
+__global__ void k_merge(MergeParts mp, int n_parts, int n_base, size_t n_words, DevResult out) {
+  const DevResult* parts = mp.p;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t b = t; b < (size_t)n_base; b += stride) {
+    unsigned long long c = 0, v = 0, f = 0, x = kNone, xu = kNone;
+    for (int p = 0; p < n_parts; p++) {
+      c += parts[p].checked[b]; v += parts[p].violated[b]; f += parts[p].flagged[b];
+      x = parts[p].first_cex[b] < x ? parts[p].first_cex[b] : x;
+      xu = parts[p].first_cex_unflagged[b] < xu ? parts[p].first_cex_unflagged[b] : xu;
+    }
+    out.checked[b] = c; out.violated[b] = v; out.flagged[b] = f;
+    out.first_cex[b] = x; out.first_cex_unflagged[b] = xu;
+  }
+  for (size_t w = t; w < n_words; w += stride) {
+    uint32_t a = 0, ce = 0;
+    for (int p = 0; p < n_parts; p++) {
+      if (parts[p].cov_all) a |= parts[p].cov_all[w];
+      if (parts[p].cov_certain) ce |= parts[p].cov_certain[w];
+    }
+    if (out.cov_all) out.cov_all[w] = a;
+    if (out.cov_certain) out.cov_certain[w] = ce;
+  }
+}
+
+cudaError_t launch_merge(const MergeParts& parts_dev, int n_parts, int n_base, size_t n_words,
+                         const DevResult& out, cudaStream_t st) {
+  const size_t n = (size_t)n_base > n_words ? (size_t)n_base : n_words;
+  unsigned blocks = (unsigned)((n + 255) / 256);
+  if (blocks < 1) blocks = 1;
+  if (blocks > 1024) blocks = 1024;
+  k_merge<<<blocks, 256, 0, st>>>(parts_dev, n_parts, n_base, n_words, out);
+  return cudaGetLastError();
+}
+
+// One thread per (method, neuron).  Reading C9: neuron (l, i) is covered by method m iff it is
+// an endpoint of a covered pair of m.
+__global__ void k_neuron_cov(DevNet net, DevCov cov, const uint32_t* words, uint8_t* covered, uint32_t* counts) {
+  const int T = net.trace_len;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * T) return;
+  const int m = t / T, g = t % T;
+  int l = 1;
+  while (l < net.L && g >= net.loff[l + 1]) l++;
+  const int i = g - net.loff[l];
+  bool cov_ = false;
+  for (int p = 0; p < cov.n_pairs && !cov_; p++) {
+    const int k = cov.lower[p], nk = net.sizes[k], nu = net.sizes[k + 1], wpr = (nu + 31) >> 5;
+    const uint32_t o = cov.off[p][m];
+    if (m < 2) {                                   // SS, SV: explicit pairs
+      if (l == k) {
+        for (int w = 0; w < wpr && !cov_; w++) cov_ = words[o + i * wpr + w] != 0;
+      } else if (l == k + 1) {
+        for (int r = 0; r < nk && !cov_; r++) cov_ = (words[o + r * wpr + (i >> 5)] >> (i & 31)) & 1;
+      }
+    } else {                                       // VS, VV: column masks
+      if (l == k) {
+        for (int w = 0; w < wpr && !cov_; w++) cov_ = words[o + w] != 0;
+      } else if (l == k + 1) {
+        cov_ = (words[o + (i >> 5)] >> (i & 31)) & 1;
+      }
+    }
+  }
+  covered[t] = cov_ ? 1 : 0;
+  if (cov_) atomicAdd(&counts[m], 1u);
+}
+
+cudaError_t launch_neuron_cov(const DevNet& net, const DevCov& cov, const uint32_t* words,
+                              uint8_t* covered, uint32_t* counts, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, 4 * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  const int n = 4 * net.trace_len;
+  k_neuron_cov<<<(n + 255) / 256, 256, 0, st>>>(net, cov, words, covered, counts);
+  return cudaGetLastError();
+}
+
+// tau_l = 1e-6 + 1e-5 * max over bases of max |u_l^base| (float potentials), one block per layer
+__global__ void k_tau(DevNet net, const float* trace, int n_base, float* tau) {
+  const int l = blockIdx.x + 1;
+  const int T = net.trace_len, n = net.sizes[l];
+  float m = 0.f;
+  for (size_t e = threadIdx.x; e < (size_t)n_base * n; e += blockDim.x) {
+    const size_t b = e / n, i = e % n;
+    m = fmaxf(m, fabsf(trace[b * T + net.loff[l] + i]));
+  }
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmaxf(m, red[w]);
+    m = fmaxf(m, red[0]);
+    tau[l - 1] = 1e-6f + 1e-5f * m;
+  }
+}
+
+cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* tau_out, cudaStream_t st) {
+  k_tau<<<net.L, 256, 0, st>>>(net, static_cast<const float*>(trace), n_base, tau_out);
+  return cudaGetLastError();
+}
+
+}  // namespace mlpv

@@ -1,0 +1,85 @@
+// mlpv_internal.cuh -- internal types shared by the host library and the sm_100a kernels.
+// Not part of the ABI (include/mlpv.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/mlpv.h"
+
+namespace mlpv {
+
+constexpr int kMaxL = MLPV_MAX_LAYERS;
+constexpr int kMaxPairs = MLPV_MAX_LAYERS - 1;
+constexpr uint64_t kNone = ~0ull;
+
+// Device copy of the network (original row-major layouts) + derived parameters.
+struct DevNet {
+  int L;
+  int sizes[kMaxL + 1];
+  int numeric, act;
+  const void* W[kMaxL];       // device, row-major n_l x n_{l-1}
+  const void* b[kMaxL];       // device, float | int32
+  int shift[kMaxL];           // INT8 requant shifts
+  const int16_t* knots;       // device [129] (PL sigmoid) or nullptr
+  int trace_len;              // n_1 + .. + n_L
+  int loff[kMaxL + 1];        // offset of layer l (1-based) in a trace
+};
+
+// Per-call coverage description, thresholds already in potential units.
+struct DevCov {
+  int n_pairs;
+  int lower[kMaxPairs];
+  uint32_t off[kMaxPairs][4];  // word offsets of SS, SV, VS, VV
+  float tg_f[kMaxL], th_f[kMaxL], tau[kMaxL];   // float numerics (per layer l-1)
+  const float* tau_dev;                        // if set, tau is read from here (device, [L])
+  int64_t tg_i[kMaxL], th_i[kMaxL];            // fixed numerics (accumulator units)
+  float near_tie;
+  uint32_t n_words;
+};
+
+struct DevProp {
+  int kind, target;
+  float V_f;
+  int64_t V_i;
+};
+
+struct DevPert {
+  int kind, tuple, n_pixels, n_levels;
+  const int32_t* pixels;      // device [n_pixels]
+  uint64_t begin, end;        // index range
+  uint64_t seed;
+  float step_f, origin_f;     // PHILOX (BF16 values)
+  int step_i, origin_i;       // PHILOX (INT8)
+  uint64_t q2;                // TUPLE: q^2
+};
+
+struct DevResult {
+  uint64_t *checked, *violated, *flagged, *first_cex, *first_cex_unflagged;
+  uint32_t *cov_all, *cov_certain;
+};
+
+// Per-base workspace produced by the base prologue (K0).
+struct BaseWS {
+  void* trace;                // [n_base x T] float | int32 potentials of the base image
+  int32_t* cls;               // [n_base] base class
+  void* delta;                // [n_base x S x q x n_1] layer-1 delta tables (subset/tuple spaces)
+  int S;                      // slots per base: n_0 (TUPLE) or K (SUBSET)
+};
+
+// Launchers (kernels in k_small.cu / k_large.cu / k_util.cu)
+cudaError_t launch_base_prologue(const DevNet& net, const void* bases, int n_base, const DevPert& pert,
+                                 const void* levels_dev, BaseWS ws, cudaStream_t st);
+cudaError_t launch_small(const DevNet& net, const void* bases, int n_base, const DevPert& pert,
+                         const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
+                         const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
+                         int num_sms, cudaStream_t st, bool* supported);
+cudaError_t launch_init_result(const DevResult& r, int n_base, uint32_t n_words, cudaStream_t st);
+constexpr int kMaxParts = 64;
+struct MergeParts { DevResult p[kMaxParts]; };
+cudaError_t launch_merge(const MergeParts& parts, int n_parts, int n_base, size_t n_words,
+                         const DevResult& out, cudaStream_t st);
+cudaError_t launch_neuron_cov(const DevNet& net, const DevCov& cov, const uint32_t* words,
+                              uint8_t* covered, uint32_t* counts, cudaStream_t st);
+cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* tau_out, cudaStream_t st);
+
+}  // namespace mlpv
