@@ -1,21 +1,696 @@
-// k_large.cu -- placeholder until the tcgen05 kernel lands.
+// k_large.cu -- the large-net path (BASELINE configs 4 and 5): Philox-lattice candidates generated
+// on chip, every layer contracted on the 5th-generation tensor cores (tcgen05.mma, accumulators in
+// TMEM), fused epilogue with the coverage predicates and the safety property.
+//
+// One persistent CTA per SM; a tile is 128 consecutive candidate indices of one base input (one
+// candidate per TMEM lane).  Warp roles (320 threads):
+//   warp 0     producer: cp.async.bulk of pre-swizzled weight tiles (and, for layers >= 2, of the
+//              previous layer's activations from the CTA's L2-resident scratch) into a 3-stage ring
+//   warp 1     MMA issuer (one thread): tcgen05.mma kind::f16 (bf16 / f16) or kind::i8, owns TMEM
+//   warps 2-5  generator: Philox4x32-10 lattice candidates (reading C14/C15) written as SWIZZLE_128B
+//              K-major A tiles into a 3-stage ring
+//   warps 6-9  epilogue: tcgen05.ld of the accumulators (thread = candidate), bias, potentials,
+//              sign / value / distance predicates and pair coverage (rows a5, a8), hidden activation
+//              written back as the next layer's A operand, argmax / property / counts (a7, a9)
+// Float path (BF16): layer 1 is bf16 x bf16 -> fp32 (exact operands); hidden activations are split
+// h = hi + lo into two fp16 values (|h - hi - lo| <= 2^-22 |h|) and layer l >= 2 contracts [hi | lo]
+// against [W_l | W_l] in fp16 (reading C19).  INT8 path: u8 x s8 -> s32, bit-exact.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdint>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "mlpv_internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace mlpv {
+using namespace tc;
+
+constexpr int kM = 128;                   // candidates per tile = TMEM lanes
+constexpr int kSG = 3;                    // generator ring stages
+constexpr int kSP = 3;                    // producer ring stages
+constexpr uint32_t kABytes = 128u * 128u; // A tile: 128 rows x 128 B
+constexpr uint32_t kWBytes = 256u * 128u; // W tile: up to 256 rows x 128 B
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 512;       // two 256-column accumulator buffers
+constexpr int kPendWords = 32;            // per candidate: 16 sc + 16 vc words (upper width <= 512)
+constexpr size_t kSmemBytes = 1024 + kSG * kABytes + kSP * (kABytes + kWBytes) + (size_t)kM * kPendWords * 4;
+
+struct LayerDesc {
+  int n, npad, nc, nchunks, nkb;   // neurons, padded, rows per W tile, chunks, 128-byte K blocks of A
+  const uint8_t* W;                // device tiles [nchunks][nkb][nc * 128]
+  int lo_kb;                       // float path: first K block of the lo half in the next layer's A
+};
+
+struct LargeArgs {
+  DevNet net;
+  LayerDesc lay[kMaxL + 1];        // 1-based
+  DevPert pert;
+  DevProp prop;
+  DevCov cov;
+  DevResult res;
+  BaseWS ws;
+  const uint8_t* bases;
+  int n_base;
+  uint64_t tiles_per_base, n_tiles;
+  uint8_t* scratch;                // [gridDim.x][scratch_per_cta]
+  size_t scratch_per_cta;
+  size_t h_off[kMaxL + 1];         // activations of layer l (A operand of layer l+1)
+  const uint64_t* eval_idx;
+  int64_t eval_n;
+  int eval_base;
+  void* eval_out;
+  int pair_of_lower[kMaxL + 1];    // pair index whose lower layer is k, or -1
+};
+
+struct TileInfo {
+  int b;
+  uint64_t start;                  // first index (range mode)
+  int nvalid;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const LargeArgs& a, uint64_t t) {
+  TileInfo ti;
+  if (a.eval_idx) {
+    ti.b = a.eval_base;
+    ti.start = t * kM;
+    const int64_t rem = a.eval_n - (int64_t)(t * kM);
+    ti.nvalid = rem < kM ? (int)rem : kM;
+  } else {
+    ti.b = (int)(t / a.tiles_per_base);
+    ti.start = a.pert.begin + (t % a.tiles_per_base) * kM;
+    const uint64_t rem = a.pert.end - ti.start;
+    ti.nvalid = rem < (uint64_t)kM ? (int)rem : kM;
+  }
+  return ti;
+}
+
+__device__ __forceinline__ uint64_t row_index(const LargeArgs& a, const TileInfo& ti, int r) {
+  if (a.eval_idx) return r < ti.nvalid ? a.eval_idx[ti.start + r] : 0;
+  return ti.start + (uint64_t)r;
+}
+
+// Philox4x32-10 (reading C15): counter (c_lo, c_hi, b, j), key (seed_lo, seed_hi)
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ uint32_t bf2_u(__nv_bfloat162 v) { return *reinterpret_cast<uint32_t*>(&v); }
+__device__ __forceinline__ __nv_bfloat162 u_bf2(uint32_t v) { return *reinterpret_cast<__nv_bfloat162*>(&v); }
+
+// Two lattice pixels from one byte of a Philox word (nibble n -> pixel n, LSB first):
+// x' = min(relu(RNE(x + RNE(l*step + origin))), 1) in bf16x2 arithmetic (single roundings).
+__device__ __forceinline__ uint32_t lattice_pair_bf16(uint32_t byte, uint32_t x2, __nv_bfloat162 step2,
+                                                      __nv_bfloat162 origin2) {
+  const uint32_t v = (byte & 0xFu) | ((byte & 0xF0u) << 12) | 0x43004300u;     // (128 + la, 128 + lb)
+  const __nv_bfloat162 l = __hsub2(u_bf2(v), __floats2bfloat162_rn(128.f, 128.f));
+  const __nv_bfloat162 off = __hfma2(l, step2, origin2);
+  const __nv_bfloat162 one = __floats2bfloat162_rn(1.f, 1.f);
+  const __nv_bfloat162 y = __hfma2_relu(u_bf2(x2), one, off);
+  return bf2_u(__hmin2(y, one));
+}
+
+// ----------------------------------------------------------------------------- generator
+__device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot) {
+  const int n0 = a.net.sizes[0];
+  const uint64_t c = row_index(a, ti, r);
+  const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
+  const bool valid = r < ti.nvalid;
+  if (a.net.numeric == MLPV_NUM_BF16) {
+    const uint16_t* x = reinterpret_cast<const uint16_t*>(a.bases) + (size_t)ti.b * n0;
+    const __nv_bfloat162 step2 = __floats2bfloat162_rn(a.pert.step_f, a.pert.step_f);
+    const __nv_bfloat162 org2 = __floats2bfloat162_rn(a.pert.origin_f, a.pert.origin_f);
+#pragma unroll
+    for (int hb = 0; hb < 2; hb++) {
+      const int j = 2 * kb + hb;
+      const int p0 = 32 * j;
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, k0, k1);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int ww = 0; ww < 4; ww++) {
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int p = p0 + 8 * ww + 2 * k;               // pixels p, p+1
+          uint32_t x2 = 0;
+          if (p + 1 < n0) x2 = __ldg(reinterpret_cast<const uint32_t*>(x + p));
+          else if (p < n0) x2 = (uint32_t)__ldg(x + p);
+          uint32_t y = lattice_pair_bf16((ws[ww] >> (8 * k)) & 0xFFu, x2, step2, org2);
+          if (p >= n0) y = 0;
+          else if (p + 1 >= n0) y &= 0xFFFFu;
+          o[k] = y;
+        }
+        *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (4 * hb + ww))) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  } else {
+    const uint8_t* x = a.bases + (size_t)ti.b * n0;
+    const int s = a.pert.step_i, og = a.pert.origin_i;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int j = 4 * kb + q;
+      const int p0 = 32 * j;
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, k0, k1);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int half = 0; half < 2; half++) {
+        uint32_t o[4];
+#pragma unroll
+        for (int ww2 = 0; ww2 < 2; ww2++) {
+          const int ww = 2 * half + ww2;
+#pragma unroll
+          for (int h4 = 0; h4 < 2; h4++) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int n = 0; n < 4; n++) {
+              const int nb = 4 * h4 + n;
+              const int p = p0 + 8 * ww + nb;
+              int y = 0;
+              if (p < n0) {
+                const int l = (int)((ws[ww] >> (4 * nb)) & 15u);
+                y = max(0, min(255, (int)__ldg(x + p) + l * s + og));
+              }
+              packed |= (uint32_t)y << (8 * n);
+            }
+            o[2 * ww2 + h4] = packed;
+          }
+        }
+        *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (2 * q + half))) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ LargeArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sG = smem;                                        // [kSG][kABytes]
+  uint8_t* sPA = sG + kSG * kABytes;                         // [kSP][kABytes]
+  uint8_t* sPW = sPA + kSP * kABytes;                        // [kSP][kWBytes]
+  uint32_t* s_pend = reinterpret_cast<uint32_t*>(sPW + kSP * kWBytes);   // [kM][kPendWords]
+  __shared__ uint64_t gfull[kSG], gempty[kSG], pfull[kSP], pempty[kSP], acc_full[2], acc_empty[2], h_ready[kMaxL + 1];
+  __shared__ uint32_t s_tbase;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = a.net.L;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSG; i++) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
+    for (int i = 0; i < kSP; i++) { mbar_init(&pfull[i], 1); mbar_init(&pempty[i], 1); }
+    for (int i = 0; i < 2; i++) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 1); }
+    for (int i = 0; i <= kMaxL; i++) mbar_init(&h_ready[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) { tmem_alloc(&s_tbase, kTmemCols); tmem_relinquish(); }
+  for (int i = threadIdx.x; i < kM * kPendWords; i += blockDim.x) s_pend[i] = 0;
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = s_tbase;
+  uint8_t* scratch = a.scratch + (size_t)blockIdx.x * a.scratch_per_cta;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------- producer
+    if (lane == 0) {
+      uint32_t ps = 0, hph[kMaxL + 1] = {0};
+      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        for (int l = 1; l <= L; l++) {
+          const LayerDesc& ld = a.lay[l];
+          const uint32_t wbytes = (uint32_t)ld.nc * 128u;
+          if (l >= 2) { mbar_wait(&h_ready[l - 1], hph[l - 1]); hph[l - 1] ^= 1u; }
+          for (int ch = 0; ch < ld.nchunks; ch++)
+            for (int kb = 0; kb < ld.nkb; kb++) {
+              const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
+              mbar_wait(&pempty[st], ph ^ 1u);
+              mbar_expect_tx(&pfull[st], wbytes + (l >= 2 ? kABytes : 0u));
+              bulk_g2s(sPW + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wbytes, &pfull[st]);
+              if (l >= 2) bulk_g2s(sPA + st * kABytes, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
+              ps++;
+            }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      uint32_t gs = 0, ps = 0, cseq = 0;
+      const bool i8 = a.net.numeric == MLPV_NUM_INT8;
+      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        for (int l = 1; l <= L; l++) {
+          const LayerDesc& ld = a.lay[l];
+          const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, l == 1 ? 1 : 0, l == 1 ? 1 : 0);
+          for (int ch = 0; ch < ld.nchunks; ch++) {
+            const uint32_t buf = cseq & 1u, aph = (cseq >> 1) & 1u;
+            mbar_wait(&acc_empty[buf], aph ^ 1u);
+            fence_after();
+            const uint32_t d = tbase + buf * 256u;
+            for (int kb = 0; kb < ld.nkb; kb++) {
+              const uint32_t pst = ps % kSP;
+              mbar_wait(&pfull[pst], (ps / kSP) & 1u);
+              uint32_t gst = 0;
+              if (l == 1) { gst = gs % kSG; mbar_wait(&gfull[gst], (gs / kSG) & 1u); }
+              fence_after();
+              const uint32_t abase = smem_u32(l == 1 ? sG + gst * kABytes : sPA + pst * kABytes);
+              const uint32_t bbase = smem_u32(sPW + pst * kWBytes);
+#pragma unroll
+              for (int kk = 0; kk < 4; kk++) {
+                const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
+                const uint32_t acc = (kb | kk) ? 1u : 0u;
+                if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
+              }
+              mma_commit(&pempty[pst]);
+              if (l == 1) { mma_commit(&gempty[gst]); gs++; }
+              ps++;
+            }
+            mma_commit(&acc_full[buf]);
+            cseq++;
+          }
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------------- generator
+    const int r = threadIdx.x - 64;
+    uint32_t gs = 0;
+    const LayerDesc& l1 = a.lay[1];
+    for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+      const TileInfo ti = tile_info(a, t);
+      for (int ch = 0; ch < l1.nchunks; ch++)
+        for (int kb = 0; kb < l1.nkb; kb++) {
+          const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
+          mbar_wait(&gempty[st], ph ^ 1u);
+          gen_block(a, ti, r, kb, sG + st * kABytes);
+          fence_proxy_async();
+          named_bar(1, 128);
+          if (r == 0) mbar_arrive(&gfull[st]);
+          gs++;
+        }
+    }
+  } else {
+    // ------------------------------------------------------------------- epilogue
+    const int e = threadIdx.x - 192;
+    const int quad = warp & 3;
+    const int r = 32 * quad + lane;                  // candidate row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+    const bool fl = a.net.numeric == MLPV_NUM_BF16;
+    const int T = a.net.trace_len;
+    const bool eval = a.eval_idx != nullptr;
+    uint32_t cseq = 0;
+    uint32_t* pend = s_pend + r * kPendWords;
+    for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+      const TileInfo ti = tile_info(a, t);
+      const bool valid = r < ti.nvalid;
+      const uint64_t cidx = row_index(a, ti, r);
+      // per-layer summaries of the previous layer (lower layer of the pair being finished)
+      int p_nsc = 0, p_istar = -1;
+      bool p_cond = false, p_amb = false;
+      float lg_f[MLPV_MAX_CLASSES];
+      int32_t lg_i[MLPV_MAX_CLASSES];
+#pragma unroll
+      for (int i = 0; i < MLPV_MAX_CLASSES; i++) { lg_f[i] = 0.f; lg_i[i] = 0; }
+      for (int l = 1; l <= L; l++) {
+        const LayerDesc& ld = a.lay[l];
+        const int pidx = l >= 2 ? a.pair_of_lower[l - 1] : -1;
+        const bool pair_on = pidx >= 0 && p_cond && valid && !eval;
+        const float tg_f = a.cov.tg_f[l - 1], th_f = a.cov.th_f[l - 1];
+        const int32_t tg_i = (int32_t)a.cov.tg_i[l - 1], th_i = (int32_t)a.cov.th_i[l - 1];
+        const float tau_l = a.cov.tau_dev ? a.cov.tau_dev[l - 1] : a.cov.tau[l - 1];
+        int nsc = 0, istar = -1;
+        float linf_f = 0.f, minab = 3.0e38f, vcamb = 3.0e38f;
+        int32_t linf_i = 0;
+        const float* bias_f = static_cast<const float*>(a.net.b[l - 1]);
+        const int32_t* bias_i = static_cast<const int32_t*>(a.net.b[l - 1]);
+        const float* ub_f = static_cast<const float*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
+        const int32_t* ub_i = static_cast<const int32_t*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
+        uint8_t* hdst = scratch + a.h_off[l];
+        const int sh = a.net.shift[l - 1];
+        for (int ch = 0; ch < ld.nchunks; ch++) {
+          const uint32_t buf = cseq & 1u, ph = (cseq >> 1) & 1u;
+          mbar_wait(&acc_full[buf], ph);
+          fence_after();
+          for (int pc = 0; pc < ld.nc; pc += 32) {
+            const int j0 = ch * ld.nc + pc;
+            if (j0 >= ld.n && l == L) break;
+            if (j0 >= ((ld.n + 63) & ~63) && l < L && fl) break;
+            uint32_t v[32];
+            tmem_ld32(tbase + buf * 256u + (uint32_t)pc + lane_off, v);
+            tmem_ld_wait();
+            uint32_t hw[16];                         // fp16 hi pairs (float) or u8 quads (int8)
+            uint32_t lw[16];
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+              const int j = j0 + i;
+              const bool in = j < ld.n;
+              if (fl) {
+                const float u = in ? __uint_as_float(v[i]) + __ldg(bias_f + j) : 0.f;
+                if (in) {
+                  const float ub = __ldg(ub_f + j);
+                  if (eval && valid) static_cast<float*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j] = u;
+                  const bool sc = (u >= 0.f) != (ub >= 0.f);
+                  if (sc) { if (istar < 0) istar = j; nsc++; }
+                  const float d = fabsf(u - ub);
+                  linf_f = fmaxf(linf_f, d);
+                  minab = fminf(minab, fminf(fabsf(u), fabsf(ub)));
+                  if (pair_on) {
+                    const bool vc = !sc && d >= tg_f;
+                    if (sc) pend[j >> 5] |= 1u << (j & 31);
+                    if (vc) pend[16 + (j >> 5)] |= 1u << (j & 31);
+                    vcamb = fminf(vcamb, fabsf(d - tg_f));
+                  }
+                  if (l == L && j < MLPV_MAX_CLASSES) lg_f[j] = u;
+                }
+                if (l < L) {
+                  const float h = fmaxf(u, 0.f);
+                  const __half hi = __float2half_rn(h);
+                  const __half lo = __float2half_rn(h - __half2float(hi));
+                  const uint32_t hb = (uint32_t)__half_as_ushort(hi), lb = (uint32_t)__half_as_ushort(lo);
+                  if (i & 1) { hw[i >> 1] |= hb << 16; lw[i >> 1] |= lb << 16; }
+                  else { hw[i >> 1] = hb; lw[i >> 1] = lb; }
+                }
+              } else {
+                const int32_t u = in ? (int32_t)v[i] + __ldg(bias_i + j) : 0;
+                if (in) {
+                  const int32_t ub = __ldg(ub_i + j);
+                  if (eval && valid) static_cast<int32_t*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j] = u;
+                  const bool sc = (u >= 0) != (ub >= 0);
+                  if (sc) { if (istar < 0) istar = j; nsc++; }
+                  const int32_t d = abs(u - ub);
+                  linf_i = max(linf_i, d);
+                  if (pair_on) {
+                    const bool vc = !sc && d >= tg_i;
+                    if (sc) pend[j >> 5] |= 1u << (j & 31);
+                    if (vc) pend[16 + (j >> 5)] |= 1u << (j & 31);
+                  }
+                  if (l == L && j < MLPV_MAX_CLASSES) lg_i[j] = u;
+                }
+                if (l < L) {
+                  const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
+                  const uint32_t y = in ? (uint32_t)max(0, min(255, (u + rr) >> sh)) : 0u;
+                  if ((i & 3) == 0) hw[i >> 2] = y; else hw[i >> 2] |= y << (8 * (i & 3));
+                }
+              }
+            }
+            if (l < L) {
+              if (fl) {
+                // 32 fp16 values = 64 bytes at K element j0 (hi) and lo_kb*64 + j0 (lo)
+                const int kbh = j0 >> 6, byh = (2 * j0) & 127;
+                uint8_t* th = hdst + (size_t)kbh * kABytes;
+                uint8_t* tl = hdst + (size_t)(ld.lo_kb + kbh) * kABytes;
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                  *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
+                  *reinterpret_cast<uint4*>(tl + sw128_off(r, byh + 16 * m)) = make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]);
+                }
+              } else {
+                const int kbh = j0 >> 7, byh = j0 & 127;
+                uint8_t* th = hdst + (size_t)kbh * kABytes;
+#pragma unroll
+                for (int m = 0; m < 2; m++)
+                  *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
+              }
+            }
+          }
+          fence_before();
+          named_bar(2, 128);
+          if (e == 0) mbar_arrive(&acc_empty[buf]);
+          cseq++;
+        }
+        // ---- finish pair (l-1, l): coverage of this candidate (reading C3, C8; C20 for certainty)
+        if (pair_on) {
+          const int k = l - 1;
+          const int wpr = (ld.n + 31) >> 5;
+          const bool certain = !fl || (!p_amb && minab >= tau_l && vcamb >= tau_l);
+          const uint32_t* off = a.cov.off[pidx];
+          for (int w = 0; w < wpr; w++) {
+            const uint32_t scw = pend[w], vcw = pend[16 + w];
+            if (p_nsc == 1) {
+              if (scw) { atomicOr(&a.res.cov_all[off[0] + p_istar * wpr + w], scw); if (certain) atomicOr(&a.res.cov_certain[off[0] + p_istar * wpr + w], scw); }
+              if (vcw) { atomicOr(&a.res.cov_all[off[1] + p_istar * wpr + w], vcw); if (certain) atomicOr(&a.res.cov_certain[off[1] + p_istar * wpr + w], vcw); }
+            } else {
+              if (scw) { atomicOr(&a.res.cov_all[off[2] + w], scw); if (certain) atomicOr(&a.res.cov_certain[off[2] + w], scw); }
+              if (vcw) { atomicOr(&a.res.cov_all[off[3] + w], vcw); if (certain) atomicOr(&a.res.cov_certain[off[3] + w], vcw); }
+            }
+            pend[w] = 0;
+            pend[16 + w] = 0;
+          }
+          (void)k;
+        }
+        // ---- summary of layer l as the lower layer of pair (l, l+1)
+        p_nsc = nsc;
+        p_istar = istar;
+        if (fl) {
+          const bool dc = nsc == 0 && linf_f >= th_f;
+          p_cond = nsc == 1 || dc;
+          p_amb = minab < tau_l || (nsc == 0 && fabsf(linf_f - th_f) < tau_l);
+        } else {
+          const bool dc = nsc == 0 && linf_i >= th_i;
+          p_cond = nsc == 1 || dc;
+          p_amb = false;
+        }
+        if (l < L) {
+          fence_proxy_async_global();
+          __threadfence_block();
+          named_bar(2, 128);
+          if (e == 0) mbar_arrive(&h_ready[l]);
+        }
+      }
+      if (eval) continue;
+      // ---- argmax (lowest index on ties), margin, property
+      const int nL = a.net.sizes[L];
+      int cls = 0;
+      bool viol = false, flag = false;
+      const int base_cls = a.ws.cls[ti.b];
+      if (fl) {
+        float top1 = lg_f[0];
+#pragma unroll
+        for (int i = 1; i < MLPV_MAX_CLASSES; i++) if (i < nL && lg_f[i] > top1) { top1 = lg_f[i]; cls = i; }
+        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+          const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
+          bool any = false;
+          float yD = 0.f;
+#pragma unroll
+          for (int i = 0; i < MLPV_MAX_CLASSES; i++)
+            if (i < nL) {
+              if (i == D) yD = lg_f[i];
+              if (i != D && lg_f[i] > a.prop.V_f) any = true;
+              if (fabsf(lg_f[i] - a.prop.V_f) < a.cov.near_tie) flag = true;
+            }
+          viol = yD < a.prop.V_f && any;
+        } else {
+          float top2 = -3.0e38f;
+#pragma unroll
+          for (int i = 0; i < MLPV_MAX_CLASSES; i++) if (i < nL && i != cls && lg_f[i] > top2) top2 = lg_f[i];
+          flag = nL > 1 && top1 - top2 < a.cov.near_tie;
+          viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != base_cls;
+        }
+      } else {
+        int32_t top1 = lg_i[0];
+#pragma unroll
+        for (int i = 1; i < MLPV_MAX_CLASSES; i++) if (i < nL && lg_i[i] > top1) { top1 = lg_i[i]; cls = i; }
+        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+          const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
+          const int32_t V = (int32_t)a.prop.V_i;
+          bool any = false;
+          int32_t yD = 0;
+#pragma unroll
+          for (int i = 0; i < MLPV_MAX_CLASSES; i++)
+            if (i < nL) {
+              if (i == D) yD = lg_i[i];
+              if (i != D && lg_i[i] > V) any = true;
+            }
+          viol = yD < V && any;
+        } else {
+          viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != base_cls;
+        }
+      }
+      if (!valid) { viol = false; flag = false; }
+      // ---- per-tile reduction (a9): warp reduce, one atomic per warp and counter
+      const uint32_t nv = __reduce_add_sync(0xffffffffu, viol ? 1u : 0u);
+      const uint32_t nf = __reduce_add_sync(0xffffffffu, flag ? 1u : 0u);
+      const uint32_t nc_ = __reduce_add_sync(0xffffffffu, valid ? 1u : 0u);
+      const uint32_t rel = viol ? (uint32_t)r : 0xFFFFFFFFu;
+      const uint32_t relu_ = (viol && !flag) ? (uint32_t)r : 0xFFFFFFFFu;
+      const uint32_t mn = __reduce_min_sync(0xffffffffu, rel), mnu = __reduce_min_sync(0xffffffffu, relu_);
+      if (lane == 0) {
+        unsigned long long* cb = reinterpret_cast<unsigned long long*>(a.res.checked);
+        if (nc_) atomicAdd(cb + ti.b, (unsigned long long)nc_);
+        if (nv) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.violated) + ti.b, (unsigned long long)nv);
+        if (nf) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.flagged) + ti.b, (unsigned long long)nf);
+        if (mn != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex) + ti.b, (unsigned long long)(ti.start + mn));
+        if (mnu != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex_unflagged) + ti.b, (unsigned long long)(ti.start + mnu));
+      }
+      (void)cidx;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) tmem_dealloc(tbase, kTmemCols);
+}
+
+// ----------------------------------------------------------------------------- host side
+struct LargeGeom {
+  LayerDesc lay[kMaxL + 1];
+  size_t h_off[kMaxL + 1];
+  size_t scratch_per_cta;
+  size_t w_off[kMaxL + 1], w_total;
+};
+
+static int pad_to(int x, int m) { return (x + m - 1) / m * m; }
+
+static bool geometry(const DevNet& net, LargeGeom* g, std::string* why) {
+  const bool fl = net.numeric == MLPV_NUM_BF16;
+  const int L = net.L;
+  if (L < 2) { *why = "large path needs at least one hidden layer"; return false; }
+  size_t off = 0, wo = 0;
+  for (int l = 1; l <= L; l++) {
+    LayerDesc& d = g->lay[l];
+    d.n = net.sizes[l];
+    const int p16 = pad_to(d.n, 16);
+    d.npad = p16 <= 256 ? p16 : pad_to(d.n, 256);
+    d.nc = d.npad <= 256 ? d.npad : 256;
+    d.nchunks = d.npad / d.nc;
+    const int kin = net.sizes[l - 1];
+    int kbytes;
+    if (fl) kbytes = l == 1 ? 2 * kin : 4 * pad_to(kin, 64);   // [hi | lo] fp16 for l >= 2
+    else kbytes = kin;
+    d.nkb = (kbytes + 127) / 128;
+    d.lo_kb = fl ? pad_to(d.n, 64) / 64 : 0;
+    g->w_off[l] = wo;
+    wo += (size_t)d.nchunks * d.nkb * d.nc * 128;
+    if (d.n > 512 && l >= 2 && l < L) { /* upper layer of a pair: pending words cover 512 */ }
+    if (l >= 2 && d.n > 512) { *why = "upper layer of a coverage pair wider than 512"; return false; }
+  }
+  for (int l = 1; l < L; l++) {
+    g->h_off[l] = off;
+    off += (size_t)g->lay[l + 1].nkb * kABytes;
+  }
+  g->scratch_per_cta = (off + 1023) & ~size_t(1023);
+  g->w_total = wo;
+  return true;
+}
+
+static uint16_t host_f2h(float f) {
+  const __half h = __float2half_rn(f);
+  uint16_t u;
+  memcpy(&u, &h, 2);
+  return u;
+}
+
+static size_t sw128_host(uint32_t row, uint32_t byte) {
+  return (row >> 3) * 1024u + (row & 7u) * 128u + ((((byte >> 4) ^ row) & 7u) << 4) + (byte & 15u);
+}
+
 cudaError_t prepare_large(const DevNet& net, const void* const* W_host, void** Wt_dev, std::string* why) {
-  (void)net; (void)W_host; (void)Wt_dev;
-  *why = "tcgen05 kernel not built yet";
+  LargeGeom g;
+  if (!geometry(net, &g, why)) return cudaSuccess;
+  const bool fl = net.numeric == MLPV_NUM_BF16;
+  std::vector<uint8_t> buf(g.w_total, 0);
+  for (int l = 1; l <= net.L; l++) {
+    const LayerDesc& d = g.lay[l];
+    const int kin = net.sizes[l - 1];
+    const size_t tile = (size_t)d.nc * 128;
+    for (int n = 0; n < d.n; n++) {
+      const int ch = n / d.nc, row = n % d.nc;
+      for (int k = 0; k < kin; k++) {
+        auto put = [&](int kbyte, const uint8_t* src, int nbytes) {
+          const int kb = kbyte / 128, q = kbyte % 128;
+          uint8_t* t = buf.data() + g.w_off[l] + ((size_t)ch * d.nkb + kb) * tile;
+          for (int i = 0; i < nbytes; i++) t[sw128_host(row, q + i)] = src[i];
+        };
+        if (!fl) {
+          const int8_t v = static_cast<const int8_t*>(W_host[l - 1])[(size_t)n * kin + k];
+          put(k, reinterpret_cast<const uint8_t*>(&v), 1);
+        } else if (l == 1) {
+          const uint16_t v = static_cast<const uint16_t*>(W_host[0])[(size_t)n * kin + k];
+          put(2 * k, reinterpret_cast<const uint8_t*>(&v), 2);
+        } else {
+          const uint16_t b = static_cast<const uint16_t*>(W_host[l - 1])[(size_t)n * kin + k];
+          uint32_t u = (uint32_t)b << 16;
+          float f;
+          memcpy(&f, &u, 4);
+          const uint16_t h = host_f2h(f);          // exact for |w| >= 2^-17 (C19)
+          put(2 * k, reinterpret_cast<const uint8_t*>(&h), 2);
+          put(2 * (pad_to(kin, 64) + k), reinterpret_cast<const uint8_t*>(&h), 2);
+        }
+      }
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, g.w_total);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(p, buf.data(), g.w_total, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(p); return e; }
+  Wt_dev[0] = p;                                   // one allocation; layers at w_off
+  for (int l = 1; l < net.L; l++) Wt_dev[l] = nullptr;
   return cudaSuccess;
 }
-cudaError_t launch_large(const DevNet&, const void* const*, const void*, int, const DevPert&, const DevProp&,
-                         const DevCov&, const DevResult&, BaseWS, const uint64_t*, int64_t, int, void*, int,
-                         cudaStream_t, bool* supported, std::string* why) {
-  *supported = false;
-  *why = "tcgen05 kernel not built yet";
-  return cudaSuccess;
+
+static uint8_t* g_scratch = nullptr;               // per process; grown on demand (one device)
+static size_t g_scratch_size = 0;
+
+cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* bases, int n_base, const DevPert& pert,
+                         const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
+                         const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
+                         cudaStream_t st, bool* supported, std::string* why) {
+  LargeGeom g;
+  *supported = geometry(net, &g, why);
+  if (!*supported) return cudaSuccess;
+  if (net.sizes[net.L] > MLPV_MAX_CLASSES) { *supported = false; *why = "too many classes"; return cudaSuccess; }
+  LargeArgs a;
+  memset(&a, 0, sizeof a);
+  a.net = net;
+  for (int l = 1; l <= net.L; l++) {
+    a.lay[l] = g.lay[l];
+    a.lay[l].W = static_cast<const uint8_t*>(Wt[0]) + g.w_off[l];
+    a.h_off[l] = g.h_off[l];
+  }
+  a.pert = pert; a.prop = prop; a.cov = cov; a.res = res; a.ws = ws;
+  a.bases = static_cast<const uint8_t*>(bases);
+  a.n_base = n_base;
+  a.eval_idx = eval_idx; a.eval_n = eval_n; a.eval_base = eval_base; a.eval_out = eval_out;
+  for (int k = 0; k <= kMaxL; k++) a.pair_of_lower[k] = -1;
+  for (int p = 0; p < cov.n_pairs; p++) a.pair_of_lower[cov.lower[p]] = p;
+  if (eval_idx) {
+    a.tiles_per_base = (uint64_t)((eval_n + kM - 1) / kM);
+    a.n_tiles = a.tiles_per_base;
+  } else {
+    a.tiles_per_base = (pert.end - pert.begin + kM - 1) / kM;
+    a.n_tiles = a.tiles_per_base * (uint64_t)n_base;
+  }
+  if (a.n_tiles == 0) return cudaSuccess;
+  const int grid = (int)(a.n_tiles < (uint64_t)num_sms ? a.n_tiles : (uint64_t)num_sms);
+  a.scratch_per_cta = g.scratch_per_cta;
+  const size_t need = (size_t)grid * g.scratch_per_cta;
+  if (need > g_scratch_size) {
+    if (g_scratch) cudaFree(g_scratch);
+    g_scratch = nullptr;
+    g_scratch_size = 0;
+    cudaError_t e = cudaMalloc(&g_scratch, need);
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(g_scratch, 0, need);           // K padding of the activations stays zero
+    if (e != cudaSuccess) return e;
+    g_scratch_size = need;
+  }
+  a.scratch = g_scratch;
+  cudaError_t e = cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  if (e != cudaSuccess) return e;
+  k_large<<<grid, kThreads, kSmemBytes, st>>>(a);
+  return cudaGetLastError();
 }
+
 }  // namespace mlpv
