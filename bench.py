@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the data-parallel MLP safety check (BASELINE.json metric: perturbations verified/s,
+whole box, and % of roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl mlpv|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one mlpv_check (every row of SURVEY.md §8(a): decode / generate, forward, argmax,
+property, coverage, reductions) over all base inputs of the config and a fresh slice of S sample
+indices per base per GPU, followed at N > 1 by the all-gather + merge of the results.  Each rank
+checks its own slice (weak scaling).  Timing: W untimed warm-up steps; then K steps, each
+bracketed by barrier + synchronize and timed with CUDA events on the launching stream, with an L2
+flush (256 MiB write) between steps; the max over ranks is reported.  The oracle (test
+infrastructure) is run only in the cpu_baseline leg and in --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "perturbations verified/sec (whole box) at 1/2/4/8 B200; % of roofline"
+UNIT = "perturbations/s"
+DEFAULT_SAMPLES = {"cfg1": None, "cfg2": None, "cfg3": 1 << 20, "cfg4": 1 << 16, "cfg5_bf16": 1 << 10,
+                   "cfg5_int8": 1 << 11}
+DTYPE = {"cfg1": "fp32", "cfg2": "q4.12", "cfg3": "int8", "cfg4": "bf16", "cfg5_bf16": "bf16", "cfg5_int8": "int8"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="cfg4")
+    p.add_argument("--samples", type=int, default=0, help="samples per base per GPU per step (Philox spaces)")
+    p.add_argument("--impl", default="mlpv", choices=["mlpv", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def alg_ops_per_candidate(cfg):
+    """Algorithmic operations per candidate: dense MACs x 2 for the Philox
+    (dense) spaces; the incremental layer-1 update (|S| x n_1) + dense later layers for subset spaces."""
+    s = cfg.net.sizes
+    dense_rest = sum(s[l - 1] * s[l] for l in range(2, len(s)))
+    if cfg.pert.kind == 3:
+        return 2 * (s[0] * s[1] + dense_rest)
+    changed = cfg.pert.tuple if cfg.pert.kind == 0 else len(cfg.pert.pixels)
+    return 2 * (changed * s[1] + dense_rest)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: str):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", self.idx], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def to_device(bases, device):
+    import numpy as np
+    import torch
+    a = bases.view(np.int16) if bases.dtype == np.uint16 else bases
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+
+
+def samples_for(cfg, args):
+    if cfg.pert.kind != 3:
+        return None
+    return args.samples or DEFAULT_SAMPLES[cfg.name]
+
+
+def step_range(cfg, args, k, rank, world):
+    """Index range of step k on `rank`: a fresh slice of S samples per base (Philox spaces), or
+    the rank's shard of the whole space (enumerated spaces)."""
+    S = samples_for(cfg, args)
+    space = cfg.space
+    if S is None:
+        from paper_1907_12933_b200.dist import shard
+        return shard(0, space, rank, world)
+    slot = (k * world + rank) % max(1, space // S)
+    return slot * S, slot * S + S
+
+
+def cpu_baseline(cfg, budget_s=12.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the same workload."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    nb = min(16, cfg.n_base)
+    probe = cfg.subset(n_base=nb, begin=0, end=min(cfg.space, 8))
+    t0 = time.perf_counter()
+    O.check(probe, nthreads=cores)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    rate = nb * (probe.pert.index_end - probe.pert.index_begin) / dt
+    m = int(max(8, min(cfg.space, budget_s * rate / nb)))
+    s = cfg.subset(n_base=nb, begin=0, end=m)
+    t0 = time.perf_counter()
+    O.check(s, nthreads=cores)
+    dt = time.perf_counter() - t0
+    n = nb * m
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{cfg.name}: bases 0-{nb - 1} x indices [0, {m}) = {n} candidates in {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import mlpv_inputs as M
+    from oracle import oracle as O
+    cfg = M.make_config(args.config)
+    cores = os.cpu_count() or 1
+    nb = min(16, cfg.n_base)
+    # size each step to ~10 s of oracle work so the whole run stays within a few minutes
+    cal = cpu_baseline(cfg, budget_s=3.0)
+    per_step = int(max(8, min(cfg.space, 10.0 * cal["value"] / nb)))
+    times = []
+    for k in range(args.warmup + args.steps):
+        s = cfg.subset(n_base=nb, begin=k * per_step % max(1, cfg.space - per_step), end=None)
+        s = cfg.subset(n_base=nb, begin=s.pert.index_begin, end=s.pert.index_begin + per_step)
+        t0 = time.perf_counter()
+        O.check(s, nthreads=cores)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    T = sum(times)
+    n = args.steps * nb * per_step
+    v = n / T
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE[cfg.name], "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cfg.name, "description": cfg.description,
+                       "sample_per_step": f"bases 0-{nb - 1} x {per_step} indices"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} steps of {nb} bases x {per_step} indices"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import mlpv_inputs as M
+    import paper_1907_12933_b200 as P
+    from paper_1907_12933_b200 import dist as PD
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P.lib()                                      # fails loudly if libmlpv.so is missing
+
+    cfg = M.make_config(args.config)
+    chk = P.Checker(cfg.net, device=local)
+    bases = to_device(cfg.bases, dev)
+    nw, _ = chk.coverage_layout(cfg.cov)
+    res = P.alloc_result(cfg.n_base, nw, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(k):
+        b, e = step_range(cfg, args, k, rank, world)
+        r = chk.check(bases, cfg.pert.with_range(b, e), cfg.prop, cfg.cov, out=res)
+        if world > 1:
+            r = PD.reduce_results(r, cfg.n_base, nw)
+        return r, e - b
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for k in range(args.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    kev0, kev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    chk.profile(kev0, kev1)
+    launches0 = chk.profile(kev0, kev1)
+    gpu_idx = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local)
+    clocks = ClockSampler(gpu_idx)
+    clocks.start()
+    step_ms, kern_ms, n_cand = [], [], 0
+    for k in range(args.warmup, args.warmup + args.steps):
+        flush.fill_(k & 0xFF)                   # L2 flush between timed steps (outside the events)
+        torch.cuda.synchronize()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        _, per_base = one_step(k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        step_ms.append(ev0.elapsed_time(ev1))
+        kern_ms.append(kev0.elapsed_time(kev1))
+        n_cand += per_base * cfg.n_base
+    clk = clocks.stop()
+    launches = chk.profile(None, None) - launches0 + (args.steps if world > 1 else 0)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    total_cand = n_cand * world
+    value = total_cand / (total_ms / 1e3)
+
+    # ---- end to end through the public API: pinned host inputs -> device, check, results -> host
+    e2e = None
+    if not args.no_e2e:
+        arr = cfg.bases.view(np.int16) if cfg.bases.dtype == np.uint16 else cfg.bases
+        host_in = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+        dev_in = torch.empty_like(host_in, device=dev)
+        keys = ("checked", "violated", "flagged", "first_cex", "first_cex_unflagged", "cov_all", "cov_certain")
+        host_out = {k: torch.empty_like(res[k], device="cpu").pin_memory() for k in keys}
+        h2d = host_in.numel() * host_in.element_size()
+        d2h = sum(v.numel() * v.element_size() for v in host_out.values())
+        e2e_ms, e2e_cand = 0.0, 0
+        for k in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dev_in.copy_(host_in, non_blocking=True)
+            b, e = step_range(cfg, args, k, rank, world)
+            r = chk.check(dev_in, cfg.pert.with_range(b, e), cfg.prop, cfg.cov, out=res)
+            if world > 1:
+                r = PD.reduce_results(r, cfg.n_base, nw)
+            for kk in keys:
+                host_out[kk].copy_(r[kk], non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            e2e_ms += e0.elapsed_time(e1)
+            e2e_cand += (e - b) * cfg.n_base
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": e2e_cand * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    # ---- roofline of the dominant kernel (the enumeration kernel)
+    pk, src = peaks()
+    ops = alg_ops_per_candidate(cfg)
+    kern_avg_s = (sum(kern_ms) / len(kern_ms)) / 1e3
+    per_launch = n_cand / args.steps
+    if cfg.pert.kind == 3:
+        bound, unit = "tensor", "TFLOP/s"
+        peak = float(pk["bf16_tflops"]) * (2.0 if cfg.net.numeric == M.NUM_INT8 else 1.0)
+        peak_note = f"{src} bf16 burst" + (" x2 (int8 nominal ratio)" if cfg.net.numeric == M.NUM_INT8 else "")
+        achieved = ops * per_launch / kern_avg_s / 1e12
+    else:
+        bound, unit = "alu", "Gop/s"
+        peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+        peak_note = "148 SM x 128 lanes x sm_max_mhz (one op per lane per clock)"
+        achieved = ops * per_launch / kern_avg_s / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get(cfg.name)
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_large" if cfg.pert.kind == 3 else "k_small",
+                "kernel_ms": 1e3 * kern_avg_s, "peak_source": peak_note,
+                "alg_ops_per_candidate": ops, "candidates_per_launch": per_launch}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg)
+        S = samples_for(cfg, args)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": DTYPE[cfg.name], "data": "synthetic",
+                "config": {"workload": cfg.name, "description": cfg.description, "bases": cfg.n_base,
+                           "samples_per_base_per_gpu_per_step": S,
+                           "candidates_per_step": total_cand // args.steps,
+                           "l2": "flushed between timed steps (256 MiB write)",
+                           "parallelism": f"dp{world} (index-space shards, one all-gather per step)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

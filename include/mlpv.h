@@ -220,6 +220,12 @@ mlpv_status mlpv_merge(const mlpv_result *parts, int32_t n_parts, int32_t n_base
 mlpv_status mlpv_neuron_coverage(mlpv_t h, const mlpv_coverage_spec *cov, const uint32_t *words,
                                  uint8_t *covered, uint32_t *counts, void *stream);
 
+/* Measurement hook (bench.py): when ev_begin / ev_end (cudaEvent_t, or NULL to disable) are set,
+ * subsequent mlpv_check calls record them on their stream immediately before and after the
+ * enumeration kernel (k_small / k_large), so a caller can time that kernel alone.  *launches (may be
+ * NULL) receives the number of kernels this handle has launched so far. */
+mlpv_status mlpv_profile(mlpv_t h, void *ev_begin, void *ev_end, uint64_t *launches);
+
 /* Library version string. */
 const char *mlpv_version(void);
 

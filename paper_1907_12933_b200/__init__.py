@@ -22,7 +22,8 @@ LIB_PATH = os.path.join(HERE, "libmlpv.so")
 NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8 = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_UNSUPPORTED", 4: "E_OVERFLOW", 5: "E_OOM", 6: "E_CUDA"}
 EXPORTS = ["mlpv_create", "mlpv_destroy", "mlpv_last_error", "mlpv_coverage_layout", "mlpv_space_size",
-           "mlpv_check", "mlpv_eval", "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_version"]
+           "mlpv_check", "mlpv_eval", "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_profile",
+           "mlpv_version"]
 
 
 class MlpvError(RuntimeError):
@@ -87,9 +88,10 @@ def lib() -> C.CDLL:
         L.mlpv_decode.argtypes = [C.c_int, C.POINTER(_Pert), C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p]
         L.mlpv_merge.argtypes = [C.POINTER(_Res), C.c_int32, C.c_int32, C.c_size_t, C.POINTER(_Res), C.c_void_p]
         L.mlpv_neuron_coverage.argtypes = [C.c_void_p, C.POINTER(_Cov), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.mlpv_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
         L.mlpv_version.restype = C.c_char_p
         for f in ("mlpv_create", "mlpv_coverage_layout", "mlpv_space_size", "mlpv_check", "mlpv_eval",
-                  "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage"):
+                  "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_profile"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -266,6 +268,15 @@ class Checker:
                             C.c_void_p(indices.data_ptr()), n, C.c_void_p(out.data_ptr()), _stream_ptr(stream)),
             self._h)
         return out[:n]
+
+    def profile(self, ev_begin=None, ev_end=None) -> int:
+        """Record torch.cuda.Event pair around the enumeration kernel of later checks (None
+        disables); returns the number of kernels this handle has launched."""
+        n = C.c_uint64()
+        b = C.c_void_p(ev_begin.cuda_event) if ev_begin is not None else None
+        e = C.c_void_p(ev_end.cuda_event) if ev_end is not None else None
+        _ck(lib().mlpv_profile(self._h, b, e, C.byref(n)), self._h)
+        return int(n.value)
 
     def neuron_coverage(self, cov, words, stream=None):
         import torch

@@ -37,6 +37,8 @@ struct mlpv_ctx {
   mlpv_status sticky = MLPV_OK;
   std::string err;
   std::vector<double> acc_scale;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;   // mlpv_profile
+  uint64_t launches = 0;
 };
 
 static thread_local std::string g_err;
@@ -415,11 +417,13 @@ static mlpv_status prepare(mlpv_ctx* h, const void* bases, int n_base, const mlp
   DevPert dp2 = dp;
   dp2.pixels = plan->pixels_dev;
   CUDA_TRY(h, launch_base_prologue(n, bases, n_base, dp2, plan->levels_dev, plan->ws, st), "base prologue");
+  h->launches++;
   if (need_tau) {
     bool any = false;
     for (int l = 0; l < n.L; l++) any |= dc->tau[l] < 0;
     if (any) {
       CUDA_TRY(h, launch_tau(n, plan->ws.trace, n_base, plan->tau_dev, st), "tau");
+      h->launches++;
     }
   }
   return MLPV_OK;
@@ -431,6 +435,7 @@ static mlpv_status run_kernel(mlpv_ctx* h, const void* bases, int n_base, const 
   dp.pixels = plan.pixels_dev;
   bool supported = false;
   cudaError_t e;
+  if (h->ev_begin) CUDA_TRY(h, cudaEventRecord(h->ev_begin, st), "profile event");
   if (pert->kind == MLPV_PERT_PHILOX_LATTICE) {
     if (!h->large_ready) return fail(h, MLPV_E_UNSUPPORTED, "large-net path unavailable for this net: %s", h->large_why.c_str());
     std::string why;
@@ -444,6 +449,16 @@ static mlpv_status run_kernel(mlpv_ctx* h, const void* bases, int n_base, const 
                                 h->net.L, h->net.sizes[1], h->net.L > 1 ? h->net.sizes[2] : 0, h->net.L > 2 ? h->net.sizes[3] : 0);
   }
   if (e != cudaSuccess) return cuda_fail(h, e, "enumeration kernel");
+  h->launches++;
+  if (h->ev_end) CUDA_TRY(h, cudaEventRecord(h->ev_end, st), "profile event");
+  return MLPV_OK;
+}
+
+extern "C" mlpv_status mlpv_profile(mlpv_t h, void* ev_begin, void* ev_end, uint64_t* launches) {
+  if (!h) return fail(nullptr, MLPV_E_INVALID, "handle is NULL");
+  h->ev_begin = static_cast<cudaEvent_t>(ev_begin);
+  h->ev_end = static_cast<cudaEvent_t>(ev_end);
+  if (launches) *launches = h->launches;
   return MLPV_OK;
 }
 
@@ -487,6 +502,7 @@ extern "C" mlpv_status mlpv_check(mlpv_t h, const void* base_inputs, int32_t n_b
   CUDA_TRY(h, cudaSetDevice(h->device), "cudaSetDevice");
   DevResult dr{res->checked, res->violated, res->flagged, res->first_cex, res->first_cex_unflagged, res->cov_all, res->cov_certain};
   CUDA_TRY(h, launch_init_result(dr, n_base, dc.n_words, st), "init results");
+  h->launches++;
   Plan plan;
   const bool fl = !is_fixed(h->net.numeric);
   if ((s = prepare(h, base_inputs, n_base, pert, dp, &dc, &plan, st, fl)) != MLPV_OK) return s;
