@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmlpv.so")
-SOURCES = ["mlpv.cu", "k_small.cu", "k_large.cu", "k_util.cu"]
+SOURCES = ["mlpv.cu", "k_small.cu", "k_large.cu", "k_fused3.cu", "k_util.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
@@ -25,7 +25,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    extra = []
+    if os.environ.get("MLPV_WAIT_TIMEOUT"):            # debug: trap instead of hanging on a lost arrive
+        extra.append(f"-DMLPV_WAIT_TIMEOUT={int(os.environ['MLPV_WAIT_TIMEOUT'])}")
+    cmd = [NVCC, *FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

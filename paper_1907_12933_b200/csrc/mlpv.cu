@@ -21,7 +21,8 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* b
                          const DevPert& pert, const DevProp& prop, const DevCov& cov, const DevResult& res,
                          BaseWS ws, const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
                          int num_sms, cudaStream_t st, bool* supported, std::string* why);
-cudaError_t prepare_large(const DevNet& net, const void* const* W_host, void** Wt_dev, std::string* why);
+cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const void* const* b_host, void** Wt_dev,
+                          std::string* why);
 }  // namespace mlpv
 
 struct mlpv_ctx {
@@ -191,7 +192,7 @@ extern "C" mlpv_status mlpv_create(const mlpv_net* net, const mlpv_quant* quant,
     h->acc_scale[l] = quant->acc_scale ? quant->acc_scale[l] : (num == MLPV_NUM_Q4_12 ? 1.0 / 16777216.0 : 1.0);
   // tensor-core layouts for the large-net path (PHILOX spaces, BF16 / INT8)
   if (num == MLPV_NUM_BF16 || num == MLPV_NUM_INT8) {
-    cudaError_t pe = prepare_large(d, net->W, h->Wt, &h->large_why);
+    cudaError_t pe = prepare_large(d, net->W, net->b, h->Wt, &h->large_why);
     if (pe != cudaSuccess) { mlpv_destroy(h); return fail(nullptr, MLPV_E_CUDA, "prepare_large: %s", cudaGetErrorString(pe)); }
     h->large_ready = h->large_why.empty();
     for (int l = 0; l < L; l++) if (h->Wt[l]) h->allocs.push_back(h->Wt[l]);

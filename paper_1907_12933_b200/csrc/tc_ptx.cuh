@@ -4,6 +4,7 @@
 // descriptors (bit layouts as in cute/arch/mma_sm100_desc.hpp).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace mlpv {
 namespace tc {
@@ -22,12 +23,14 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread sleeps (up to the hint, in ns) until the
+// phase completes instead of spinning and stealing issue slots from the working warps.
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
-      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(20000u)
       : "memory");
   return ok != 0;
 }
@@ -36,7 +39,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #ifdef MLPV_WAIT_TIMEOUT
   const long long t0 = clock64();
   while (!mbar_try(bar, phase)) {
-    if (clock64() - t0 > (long long)MLPV_WAIT_TIMEOUT) __trap();
+    if (clock64() - t0 > (long long)MLPV_WAIT_TIMEOUT) {
+      printf("mlpv wait timeout: block %d thread %d bar smem 0x%x phase %u\n", blockIdx.x, threadIdx.x,
+             smem_u32(bar), phase);
+      __trap();
+    }
   }
 #else
   while (!mbar_try(bar, phase)) {
@@ -187,6 +194,90 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 }
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+}  // namespace tc
+}  // namespace mlpv
+
+namespace mlpv {
+namespace tc {
+// ----------------------------------------------------------------------------- clusters / CTA pairs
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address of `p` -> shared::cluster address of the same offset in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// arrive on the mbarrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa(smem_u32(bar), rank))
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(20000u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+#ifdef MLPV_WAIT_TIMEOUT
+  const long long t0 = clock64();
+  while (!mbar_try_cluster(bar, phase)) {
+    if (clock64() - t0 > (long long)MLPV_WAIT_TIMEOUT) {
+      printf("mlpv cluster wait timeout: block %d thread %d bar smem 0x%x phase %u\n", blockIdx.x, threadIdx.x,
+             smem_u32(bar), phase);
+      __trap();
+    }
+  }
+#else
+  while (!mbar_try_cluster(bar, phase)) {
+  }
+#endif
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish2() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// 2-CTA MMA (issued by the leader CTA only): M = 256 rows, rows 0-127 / 128-255 in CTA 0 / 1, each
+// CTA holding its own A rows and half of B (N/2 rows) at the same shared-memory offsets.
+__device__ __forceinline__ void mma2_f16_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_f16_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// commit the leader's previously issued MMAs to the mbarrier at `bar`'s offset in every CTA of mask
+__device__ __forceinline__ void mma2_commit(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 }  // namespace tc
 }  // namespace mlpv

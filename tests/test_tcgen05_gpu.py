@@ -66,3 +66,28 @@ def test_fp32_accumulation_error(probe):
     print(f"tcgen05 bf16 K={K}: max abs err {float(abs_err.max()):.3e}, rms {float(abs_err.pow(2).mean().sqrt()):.3e}, "
           f"|ref| rms {float(ref.pow(2).mean().sqrt()):.3e}")
     assert float(abs_err.max()) < 1e-5
+
+
+@pytest.fixture(scope="module")
+def probe2(tmp_path_factory):
+    so = str(tmp_path_factory.mktemp("tc2") / "probe2.so")
+    subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-shared",
+                           "-Xcompiler", "-fPIC", "-std=c++17", "-DMLPV_WAIT_TIMEOUT=4000000000", "-o", so,
+                           os.path.join(HERE, "cuda", "tc_probe2.cu")])
+    return C.CDLL(so)
+
+
+@pytest.mark.parametrize("mode,N,K", [(0, 256, 128), (0, 32, 64), (1, 256, 256), (1, 64, 128)])
+def test_cta_pair_mma(probe2, mode, N, K):
+    """cta_group::2: M = 256 split over a CTA pair, B split by N, commit multicast to both CTAs."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(11 + mode + N + K)
+    A = torch.randn((256, K), generator=g).to(torch.bfloat16).cuda()
+    B = (torch.randn((N, K), generator=g) * 0.1).to(torch.bfloat16).cuda()
+    D = torch.zeros((256, N), dtype=torch.int32, device="cuda")
+    rc = probe2.tc_probe2(mode, C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), C.c_void_p(D.data_ptr()), N, K)
+    assert rc == 0, rc
+    D = D.view(torch.float32).double().cpu()
+    ref = A.double().cpu() @ B.double().cpu().T
+    scale = A.double().abs().cpu() @ B.double().abs().cpu().T
+    assert float(((D - ref).abs() / scale.clamp_min(1e-30)).max()) < 2e-6
