@@ -17,7 +17,7 @@ from typing import Dict, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmlpv.so")
+LIB_PATH = os.environ.get("MLPV_LIB") or os.path.join(HERE, "libmlpv.so")   # MLPV_LIB: debug builds only
 
 NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8 = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_UNSUPPORTED", 4: "E_OVERFLOW", 5: "E_OOM", 6: "E_CUDA"}

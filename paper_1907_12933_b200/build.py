@@ -12,29 +12,31 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(os.path.dirname(HERE), "include", "mlpv.h"))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    extra = []
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True builds the debug variant libmlpv_trace.so (k_fused3 timeline stamps, -DMLPV_TRACE)."""
+    lib = LIB.replace(".so", "_trace.so") if trace else LIB
+    if not force and not _stale(lib):
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    extra = ["-DMLPV_TRACE"] if trace else []
     if os.environ.get("MLPV_WAIT_TIMEOUT"):            # debug: trap instead of hanging on a lost arrive
         extra.append(f"-DMLPV_WAIT_TIMEOUT={int(os.environ['MLPV_WAIT_TIMEOUT'])}")
     cmd = [NVCC, *FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

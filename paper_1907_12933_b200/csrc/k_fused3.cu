@@ -37,6 +37,13 @@ namespace mlpv {
 using namespace tc;
 
 namespace f3 {
+#ifdef MLPV_TRACE
+// debug timeline (tools/trace_fused3.py): clock64 stamps of the first 64 tiles of cluster 0
+__device__ unsigned long long g_trace[2][64][32];
+#define TR(tl, ev) do { if (cluster == 0 && (tl) < 64) g_trace[rank][(tl)][(ev)] = clock64(); } while (0)
+#else
+#define TR(tl, ev) do { } while (0)
+#endif
 constexpr int kThreads = 480;
 constexpr int kSG = 3;                       // generator ring stages
 constexpr int kSW = 4;                       // weight ring stages
@@ -237,10 +244,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       uint32_t ws = 0;
       const int nst = a.nkb1 + kNkb2;
       const uint8_t* src0 = a.wstream + (size_t)rank * nst * kTile;
-      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters)
+      uint32_t tl = 0;
+      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tl++)
         for (int s = 0; s < nst; s++) {
           const uint32_t st = ws % kSW, ph = (ws / kSW) & 1u;
           mbar_wait(&S.w_empty[st], ph ^ 1u);
+          if (s == 0) TR(tl, 31);
           mbar_expect_tx(&S.w_full[st], kTile);
           bulk_g2s(sW + st * kTile, src0 + (size_t)s * kTile, kTile, &S.w_full[st]);
           ws++;
@@ -265,10 +274,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const uint32_t id2 = idesc_f16(256, kN2, 0, 0);     // f16 x f16 -> f32
       for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tcount++) {
         // layer 1 into R1 (in-order after the previous tile's layer 2 read R1)
+        TR(tcount, 0);
         for (int kb = 0; kb < a.nkb1; kb++) {
           const uint32_t g = gs % kSG, w = ws % kSW;
           mbar_wait_cluster(&S.g_full[g], (gs / kSG) & 1u);
+          if (kb < 13) TR(tcount, 16 + kb);
           mbar_wait_cluster(&S.w_full[w], (ws / kSW) & 1u);
+          if (kb == 0) TR(tcount, 1);
+          if (kb == a.nkb1 - 1) TR(tcount, 2);
           fence_after();
           const uint32_t ab = smem_u32(sG + g * kTile), bb = smem_u32(sW + w * kTile);
 #pragma unroll
@@ -281,7 +294,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         mma2_commit(&S.acc1_full, 0x3);
         // layer 2: A = H1 (fp16 hi | lo) in R1, B = W2 half tiles, D = R2
         mbar_wait_cluster(&S.h1_ready, tcount & 1u);
+        TR(tcount, 3);
         mbar_wait_cluster(&S.acc2_free, (tcount & 1u) ^ 1u);
+        TR(tcount, 4);
         fence_after();
         for (int kb = 0; kb < kNkb2; kb++) {
           const uint32_t w = ws % kSW;
@@ -299,6 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           ws++;
         }
         mma2_commit(&S.acc2_full, 0x3);
+        TR(tcount, 5);
       }
     }
   } else if (warp == 2) {
@@ -306,10 +322,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       // ---------------------------------------------------------------- layer-3 issuer (leader)
       uint32_t use[4] = {0, 0, 0, 0};
       const uint32_t id3 = idesc_f16(256, kN3P, 0, 0);
-      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters) {
+      uint32_t tl = 0;
+      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tl++) {
         for (int p = 0; p < kChunks; p++) {
           const int slot = 2 * (p & 1) + ((p >> 1) & 1);
           mbar_wait_cluster(&S.h2c_full[slot], use[slot] & 1u);
+          if (p == 0) TR(tl, 14);
           use[slot]++;
           fence_after();
           const uint32_t ab = smem_u32(sH2 + slot * kTile), bb = smem_u32(sW3 + p * kW3Chunk);
@@ -319,6 +337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           mma2_commit(&S.h2c_empty[slot], 0x3);
         }
         mma2_commit(&S.acc3_full, 0x3);
+        TR(tl, 15);
       }
     }
   } else if (warp >= 3 && warp < 7) {
@@ -331,7 +350,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const uint32_t step2 = *reinterpret_cast<const uint32_t*>(&st2), org2 = *reinterpret_cast<const uint32_t*>(&or2);
     const int n0 = a.n0;
     const int full_kb = n0 / 64;                           // K blocks made only of lattice pixels
-    for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters) {
+    uint32_t tl = 0;
+    for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tl++) {
+      if (r == 0) TR(tl, 6);
       const TileInfo ti = tile_info(a, t);
       if (ti.b != S.base_g) {                              // stage the base image (bf16) once per base
         named_bar(1, 128);
@@ -390,6 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         if (r == 0) arrive_leader(&S.g_full[st], rank);
         gs++;
       }
+      if (r == 0) TR(tl, 7);
     }
   } else if (warp >= 7) {
     // ------------------------------------------------------------------ epilogue (both CTAs)
@@ -434,6 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
       // =========================== E1: layer-1 potentials -> predicates, H1 (fp16 hi|lo) in place
       mbar_wait(&S.acc1_full, tcount & 1u);
+      if (e == 0) TR(tcount, 8);
       fence_after();
       int nsc = 0, first = -1;
       uint32_t fw = 0;
@@ -473,6 +496,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       S.x_nsc[grp][r] = nsc; S.x_first[grp][r] = first; S.x_fw[grp][r] = fw;
       S.x_linf[grp][r] = linf; S.x_minab[grp][r] = minab;
       fence_before();
+      if (e == 0) TR(tcount, 9);
+      if (e == 128) TR(tcount, 29);
       named_bar(2, 256);
       if (e == 0) arrive_leader(&S.h1_ready, rank);
       // combine the two groups' summaries of layer 1
@@ -489,6 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const bool amb1 = minab1 < tau[0] || (nsc1 == 0 && fabsf(linf1 - th1) < tau[0]);
       // =========================== E2: layer-2 potentials -> predicates, H2 chunks for layer 3
       mbar_wait(&S.acc2_full, tcount & 1u);
+      if (e == 0) TR(tcount, 10);
       fence_after();
       const bool pair12 = a.pair12 >= 0 && cond1 && valid && !eval;
       const bool any12 = __any_sync(0xffffffffu, pair12);
@@ -563,7 +589,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       // combine summaries of layer 2 and finish pair (1, 2)
       S.x_nsc[grp][r] = nsc2; S.x_first[grp][r] = first2; S.x_fw[grp][r] = fw2;
       S.x_linf[grp][r] = linf2; S.x_minab[grp][r] = minab2; S.x_vcamb[grp][r] = vcamb2;
+      if (e == 128) TR(tcount, 30);
       named_bar(2, 256);
+      if (e == 0) TR(tcount, 11);
       const int nsc2t = nsc2 + S.x_nsc[o][r];
       int f2 = first2;
       uint32_t fw2t = fw2;
@@ -591,6 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       // =========================== E3: logits -> pair (2, 3), argmax, property, counts (group 0)
       if (grp == 0) {
         mbar_wait(&S.acc3_full, tcount & 1u);
+        if (e == 0) TR(tcount, 12);
         fence_after();
         uint32_t v[16];
         tmem_ld16(R2 + loff, v);
@@ -670,6 +699,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             if (mnu != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex_unflagged) + ti.b, (unsigned long long)(ti.start + mnu));
           }
         }
+        if (e == 0) TR(tcount, 13);
       }
     }
   }
@@ -681,6 +711,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 }
 
 }  // namespace f3
+
+#ifdef MLPV_TRACE
+extern "C" int mlpv_f3_trace_read(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, f3::g_trace, sizeof f3::g_trace);
+}
+#endif
 
 // ------------------------------------------------------------------------------------------- host
 bool fused3_applicable(const DevNet& net) {

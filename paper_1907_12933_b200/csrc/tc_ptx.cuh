@@ -215,15 +215,18 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-// arrive on the mbarrier at the same offset in CTA `rank` of the cluster
+// arrive on the mbarrier at the same offset in CTA `rank` of the cluster.  Default semantics
+// (release at CTA scope): the data this arrive publishes is either shared memory read by the pair's
+// tensor core (ordered by the caller's fence.proxy.async + named barrier) or TMEM (ordered by
+// tcgen05.fence::before_thread_sync).  `.release.cluster` would emit MEMBAR.ALL.GPU per arrive.
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa(smem_u32(bar), rank))
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(mapa(smem_u32(bar), rank))
                : "memory");
 }
 __device__ __forceinline__ bool mbar_try_cluster(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
-      "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(phase), "r"(20000u)
       : "memory");

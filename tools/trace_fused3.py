@@ -1,0 +1,53 @@
+"""Timeline of k_fused3 (debug build with -DMLPV_TRACE): per-tile clock64 stamps of cluster 0.
+
+    python tools/trace_fused3.py [n_samples_per_base]
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1907_12933_b200 import build as B  # noqa: E402
+
+os.environ["MLPV_LIB"] = B.build(trace=True)
+import torch  # noqa: E402
+
+import mlpv_inputs as M  # noqa: E402
+import paper_1907_12933_b200 as P  # noqa: E402
+
+P.LIB_PATH = os.environ["MLPV_LIB"]
+from tests.parity import to_device_bases  # noqa: E402
+
+EV = {0: "iss.top", 1: "iss.kb0", 2: "iss.kblast", 3: "iss.h1rdy", 4: "iss.acc2free", 5: "iss.L2done",
+      6: "gen.start", 7: "gen.end", 8: "epi.acc1", 9: "epi.E1done", 10: "epi.acc2", 11: "epi.E2done",
+      12: "epi.acc3", 13: "epi.E3done", 14: "l3.first", 15: "l3.last", 29: "epi1.E1done", 30: "epi1.E2pieces",
+      31: "prod.w0"}
+
+S = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+cfg = M.make_config("cfg4")
+cfg = cfg.subset(n_base=cfg.n_base, begin=0, end=S)
+chk = P.Checker(cfg.net)
+bases = to_device_bases(cfg)
+for _ in range(2):
+    chk.check(bases, cfg.pert, cfg.prop, cfg.cov)
+torch.cuda.synchronize()
+buf = np.zeros((2, 64, 32), np.uint64)
+assert P.lib().mlpv_f3_trace_read(buf.ctypes.data_as(C.c_void_p)) == 0
+t0 = int(buf[0, 8, 0])
+for rank in (0, 1):
+    print(f"== rank {rank}")
+    for tl in range(8, 14):
+        row = buf[rank, tl].astype(np.int64)
+        items = sorted(((int(row[e]) - t0, EV.get(e, f"g{e-16}")) for e in range(32) if row[e]), key=lambda x: x[0])
+        print(f"tile {tl}: " + "  ".join(f"{n}={v}" for v, n in items))
+r0 = buf[0].astype(np.int64)
+per = np.diff(r0[8:60, 0])
+print("issuer tile period (cycles): median", np.median(per), "min", per.min(), "max", per.max())
+for name, a, b in (("L1 gen-wait span kb0->kblast", 1, 2), ("h1 wait after kblast", 2, 3), ("acc2free after h1", 3, 4),
+                   ("E1 (acc1->E1done)", 8, 9), ("E2 (acc2->E2done)", 10, 11), ("E3 (acc3->E3done)", 12, 13),
+                   ("gen tile", 6, 7)):
+    d = r0[8:60, b] - r0[8:60, a]
+    print(f"{name:32s} median {np.median(d):8.0f}  min {d.min():8d}  max {d.max():8d}")
