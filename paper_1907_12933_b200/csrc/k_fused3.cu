@@ -1,26 +1,29 @@
 // k_fused3.cu -- the specialised large-net kernel for 3-layer bf16 nets with 256-wide hidden layers
-// (BASELINE config 4: 784-256-256-10).  Everything stays on chip:
+// (BASELINE config 4: 784-256-256-10), SURVEY.md §8(a) rows a1-a9 in one persistent launch.
 //
-//   * a CTA pair (cluster of 2, tcgen05.mma.cta_group::2, M = 256 candidates) shares each weight
-//     tile: every CTA loads only its half (128 of the 256 output neurons), halving L2->SM traffic
-//     and shared-memory bandwidth per MMA;
-//   * layer 1: A = Philox-lattice candidates written by 4 generator warps into a SWIZZLE_128B ring,
-//     B = W1 half tiles streamed by cp.async.bulk; the layer bias rides along as three extra K
-//     columns (bf16 hi/mid/lo of the fp32 bias) in the otherwise zero K padding (784 -> 832);
-//   * the layer-1 accumulator (TMEM columns 0-255) is turned in place by the epilogue into the
-//     fp16 hi/lo split of the hidden activations (reading C19), which is the A operand of layer 2
-//     straight from TMEM (tcgen05.mma ... [a_tmem]); layer 2 accumulates in columns 256-511;
-//   * layer 3 (N = 10, padded to 32): the epilogue stages 32-neuron chunks of [hi | lo] in shared
-//     memory and a second issuer thread runs the small MMAs into the drained columns 256-287;
-//   * 8 epilogue warps (two groups of four, one thread per candidate row) evaluate the predicates
-//     and coverage with the sign / L-inf / min|u| summaries of each
-//     32-neuron piece, and only rare candidates take the per-neuron coverage path.
+// A CTA pair (cluster of 2) owns a contiguous range of 256-candidate pair tiles; the leader
+// (cluster rank 0) issues every tcgen05.mma with cta_group::2 (M = 256: rows 0-127 of the tile in
+// CTA 0's TMEM lanes, rows 128-255 in CTA 1's), each CTA supplying half of every B operand.
 //
-// Warp roles (15 warps): 0 producer, 1 MMA issuer (leader) / relay (peer) and TMEM owner,
-// 2 layer-3 issuer (leader), 3-6 generator, 7-14 epilogue (two groups of four warps covering the
-// four TMEM lane quadrants each).  The leader (cluster rank 0) issues every MMA;
-// the peer signals its readiness by remote mbarrier arrives; MMA completion is committed with
-// multicast to both CTAs.
+//   layer 1  A = Philox-lattice candidates generated on chip into a SWIZZLE_128B ring; B = W1 half
+//            tiles streamed by cp.async.bulk; the layer-1 bias rides along as three extra K columns
+//            (bf16 hi / mid / lo of the fp32 bias), so TMEM cols [0,256) hold u1 (Eq. 1).
+//   E1       4 warps, thread = candidate row, all 256 neurons: pass A builds the sign-change words
+//            sc1 against the base potentials (one funnel shift per neuron); pass B turns u1 in
+//            place into the fp16 hi/lo split of h1 = ReLU(u1) (reading C19; each 16-column group
+//            becomes [hi | lo]) and hands it to the MMA 64 neurons at a time.  The L-inf / min|u| predicates are computed only by warps
+//            with a candidate whose sc1 count is <= 1 (the only ones a covering method can fire on).
+//   layer 2  A = H1 straight from TMEM, B = W2 (fp16, duplicated for the lo half); the bias is one
+//            more SS MMA (ones column x [b_hi | b_lo]); accumulator TMEM cols [256,512).
+//   E2       4 warps: pass A sign words sc2; pass B fp16 hi/lo of h2 into 32-neuron shared-memory
+//            chunks for layer 3, plus the pair-(1,2) coverage and pair-(2,3) predicates on the
+//            (warp-uniform) slow path.
+//   layer 3  N = 16 (n_3 <= 16), one MMA chain per chunk, accumulator in the drained cols [256,272).
+//   E3       E2's warps: logits, pair (2,3), argmax / margin / property, counts, first counterexample.
+//
+// Warp roles (20 warps): 0 weight producer, 1 MMA issuer (leader) / weight relay (peer) and TMEM
+// owner, 2 layer-3 issuer (leader), 3 idle, 4-11 generator (8 warps: row quadrant x half K block),
+// 12-15 E1, 16-19 E2/E3.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -44,23 +47,42 @@ __device__ unsigned long long g_trace[2][64][32];
 #else
 #define TR(tl, ev) do { } while (0)
 #endif
-constexpr int kThreads = 480;
-constexpr int kSG = 3;                       // generator ring stages
+
+constexpr int kThreads = 640;
+constexpr int kSG = 4;                       // generator ring stages
 constexpr int kSW = 4;                       // weight ring stages
+constexpr int kSH = 2;                       // layer-3 A chunk ring
 constexpr uint32_t kTile = 16384;            // 128 rows x 128 B
-constexpr int kN1 = 256, kN2 = 256, kN3P = 32;
+constexpr int kN1 = 256, kN2 = 256, kN3P = 16;
 constexpr int kNkb2 = kN1 / 64;              // W2 K blocks (64 fp16 per 128-B row)
 constexpr int kChunks = kN2 / 32;            // layer-3 chunks (32 neurons of layer 2)
-constexpr uint32_t kW3Chunk = 16u * 128u;    // per CTA: 16 rows x 128 B
+constexpr uint32_t kW3Chunk = 8u * 128u;     // per CTA: 8 rows x 128 B
 constexpr int kMaxN0 = 1024;
+constexpr int kWGen = 4, kWE1 = 12, kWE2 = 16;
+
+// device weight block of one handle: [rank][nst][16 KB] stream | [rank][8][1 KB] W3 | ones | [rank] bias2
+struct Layout {
+  size_t stream, w3, ones, bias2, total;
+  int nkb1, nk16, nst;
+};
+__host__ __device__ inline Layout layout_of(int n0) {
+  Layout L;
+  L.nk16 = (n0 + 3 + 15) / 16;               // K steps of layer 1 (pixels + 3 bias columns)
+  L.nkb1 = (L.nk16 + 3) / 4;
+  L.nst = L.nkb1 + kNkb2;
+  L.stream = 0;
+  L.w3 = L.stream + (size_t)2 * L.nst * kTile;
+  L.ones = L.w3 + (size_t)2 * kChunks * kW3Chunk;
+  L.bias2 = L.ones + kTile;
+  L.total = L.bias2 + 2 * (size_t)kTile;
+  return L;
+}
 
 struct Args {
-  int n0, n3, nkb1;
-  uint64_t n_pairs_tiles;                    // pair tiles (256 candidates each)
-  uint64_t tiles_per_base;
-  const uint8_t* wstream;                    // [rank][nkb1 + 4][16 KB] W1 (with bias columns) then W2 (fp16)
-  const uint8_t* w3;                         // [rank][kChunks][2 KB]
-  const float* b2;                           // [256]
+  int n0, n3, nkb1, nk16;
+  uint64_t n_pairs_tiles, tiles_per_base;
+  const uint8_t* wblk;                       // Layout above
+  Layout lay;
   const float* b3;                           // [n3]
   const uint16_t* bases;                     // [n_base][n0] bf16
   DevPert pert;
@@ -77,28 +99,35 @@ struct Args {
   float* eval_out;
 };
 
-struct alignas(16) Smem {                    // (dynamic part follows the 1 KiB-aligned tiles)
+struct alignas(16) Smem {
   uint64_t g_full[kSG], g_empty[kSG], w_full[kSW], w_empty[kSW];
-  uint64_t acc1_full, acc2_full, acc3_full, h1_ready, acc2_free;
-  uint64_t h2c_full[4], h2c_empty[4];
+  uint64_t acc1_full, acc2_full, acc3_full, acc2_free;
+  uint64_t h1_kb[kNkb2];
+  uint64_t h2_full[kSH], h2_empty[kSH];
+  uint64_t info_full[2];
   uint32_t tbase;
-  int base_g, base_e;                        // base input whose data is staged (generator / epilogue)
+  int base_g, base_e1, base_e2;
+  // E1 team: base data
   alignas(16) float ub1[kN1];
+  uint32_t nb1[8];
+  float minub1;
+  // E2 team: base data
   alignas(16) float ub2[kN2];
   alignas(16) float ub3[kN3P];
-  alignas(16) float b2[kN2];
   alignas(16) float b3[kN3P];
-  uint32_t nb1[8], nb2[8], nb3;
-  float minub[3];
-  // per-candidate summaries exchanged between the two epilogue groups
-  int x_nsc[2][128], x_first[2][128];
-  uint32_t x_fw[2][128];
-  float x_linf[2][128], x_minab[2][128], x_vcamb[2][128];
-  alignas(16) uint16_t xg[kMaxN0 + 128];     // base image (bf16) for the generator, zero padded
+  uint32_t nb2[8], nb3;
+  float minub2, minub3;
+  int bcls;
+  // E1 -> E2, per tile parity and row: bit 0 cond1, bit 1 (nsc1 == 1), bit 2 amb1, bits 8.. i*
+  int info[2][128];
+  uint32_t sc2[8][128];                      // E2: sign-change words of layer 2
+  uint32_t vc2[8][128];                      // E2 slow path: value-change words of layer 2
+  alignas(16) uint16_t xg[kMaxN0 + 64];     // base image (bf16) for the generator, zero padded
 };
 
-constexpr size_t kTilesBytes = (size_t)kSG * kTile + (size_t)kSW * kTile + (size_t)kChunks * kW3Chunk + 4 * (size_t)kTile;
+constexpr size_t kTilesBytes = (size_t)(kSG + kSW + kSH + 2) * kTile + (size_t)kChunks * kW3Chunk;
 constexpr size_t kSmemBytes = 1024 + kTilesBytes + sizeof(Smem);
+static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
 struct TileInfo {
   int b;
@@ -120,6 +149,13 @@ __device__ __forceinline__ TileInfo tile_info(const Args& a, uint64_t t) {
     ti.nvalid = rem < 256 ? (int)rem : 256;
   }
   return ti;
+}
+
+// contiguous range of pair tiles owned by cluster c (base inputs change rarely inside a range)
+__device__ __forceinline__ void cluster_range(uint64_t n, uint64_t c, uint64_t nc, uint64_t& t0, uint64_t& t1) {
+  const uint64_t q = n / nc, r = n % nc;
+  t0 = c * q + (c < r ? c : r);
+  t1 = t0 + q + (c < r ? 1 : 0);
 }
 
 __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
@@ -174,22 +210,23 @@ __device__ __forceinline__ uint4 lattice_word(uint32_t w, uint4 x2, uint32_t ste
   return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-__device__ __forceinline__ uint32_t f2h2_rz_relu(float lo, float hi) {
-  uint32_t d;
-  asm("cvt.rz.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
-  return d;
-}
-__device__ __forceinline__ uint32_t f2h2_rn_relu(float lo, float hi) {
-  uint32_t d;
-  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
-  return d;
-}
-// h = max(u, 0) = hi + lo + O(2^-21 h):  hi = RZ_f16(h), lo = RN_f16(h - hi)  (both relu'd)
+// h = max(u, 0) = hi + lo + O(2^-22 h): hi = RZ_f16(h), lo = RN_f16(h - hi) (relu'd), with the
+// exact difference u - hi taken by one mixed-precision FMA (u + hi * -1).
 __device__ __forceinline__ void split_pair(float u0, float u1, uint32_t& hi2, uint32_t& lo2) {
-  hi2 = f2h2_rz_relu(u0, u1);
-  const float h0 = __half2float(__ushort_as_half((unsigned short)(hi2 & 0xFFFFu)));
-  const float h1 = __half2float(__ushort_as_half((unsigned short)(hi2 >> 16)));
-  lo2 = f2h2_rn_relu(u0 - h0, u1 - h1);
+  asm("cvt.rz.relu.f16x2.f32 %0, %1, %2;" : "=r"(hi2) : "f"(u1), "f"(u0));
+  float d0, d1;
+  asm("{.reg .b16 l, h, m; mov.b16 m, 0xBC00; mov.b32 {l, h}, %2;\n\t"
+      "fma.rn.f32.f16 %0, l, m, %3; fma.rn.f32.f16 %1, h, m, %4;}"
+      : "=f"(d0), "=f"(d1) : "r"(hi2), "f"(u0), "f"(u1));
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(lo2) : "f"(d1), "f"(d0));
+}
+
+// sign bits of 16 potentials shifted into m from the top (bit i of the final word = neuron i when
+// the upper half is folded first): one funnel shift per neuron
+__device__ __forceinline__ uint32_t sign_fold(const uint32_t (&v)[16], uint32_t m) {
+#pragma unroll
+  for (int i = 15; i >= 0; i--) m = __funnelshift_l(v[i], m, 1);
+  return m;
 }
 
 __device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t rank) {
@@ -203,33 +240,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sG = base;                                    // [kSG][16 KB] generated A tiles
   uint8_t* sW = sG + kSG * kTile;                        // [kSW][16 KB] W1 / W2 half tiles
-  uint8_t* sW3 = sW + kSW * kTile;                       // [kChunks][2 KB] W3 half (resident)
-  uint8_t* sH2 = sW3 + kChunks * kW3Chunk;               // [4][16 KB] layer-3 A chunks
-  Smem& S = *reinterpret_cast<Smem*>(sH2 + 4 * kTile);
+  uint8_t* sH2 = sW + kSW * kTile;                       // [kSH][16 KB] layer-3 A chunks
+  uint8_t* sOnes = sH2 + kSH * kTile;                    // [16 KB] ones column (bias MMA A)
+  uint8_t* sB2 = sOnes + kTile;                          // [16 KB] [b2_hi | b2_lo] half (bias MMA B)
+  uint8_t* sW3 = sB2 + kTile;                            // [kChunks][1 KB] W3 half (resident)
+  Smem& S = *reinterpret_cast<Smem*>(sW3 + kChunks * kW3Chunk);
 
   const uint32_t rank = cluster_ctarank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  uint64_t t_begin, t_end;
+  cluster_range(a.n_pairs_tiles, cluster, nclusters, t_begin, t_end);
 
   if (threadIdx.x == 0) {
     const uint32_t two = rank == 0 ? 2u : 1u;
-    for (int i = 0; i < kSG; i++) { mbar_init(&S.g_full[i], two); mbar_init(&S.g_empty[i], 1); }
+    for (int i = 0; i < kSG; i++) { mbar_init(&S.g_full[i], 16); mbar_init(&S.g_empty[i], 1); }
     for (int i = 0; i < kSW; i++) { mbar_init(&S.w_full[i], two); mbar_init(&S.w_empty[i], 1); }
     mbar_init(&S.acc1_full, 1); mbar_init(&S.acc2_full, 1); mbar_init(&S.acc3_full, 1);
-    mbar_init(&S.h1_ready, two); mbar_init(&S.acc2_free, two);
-    for (int i = 0; i < 4; i++) { mbar_init(&S.h2c_full[i], two); mbar_init(&S.h2c_empty[i], 1); }
-    S.base_g = -1;
-    S.base_e = -1;
+    mbar_init(&S.acc2_free, 8);
+    for (int i = 0; i < kNkb2; i++) mbar_init(&S.h1_kb[i], 8);
+    for (int i = 0; i < kSH; i++) { mbar_init(&S.h2_full[i], 8); mbar_init(&S.h2_empty[i], 1); }
+    for (int i = 0; i < 2; i++) mbar_init(&S.info_full[i], 4);
+    S.base_g = S.base_e1 = S.base_e2 = -1;
     fence_mbar_init();
   }
   if (warp == 1) { tmem_alloc2(&S.tbase, 512); tmem_relinquish2(); }
-  // resident data: W3 half, biases (plain loads, once)
+  // resident operands: W3 half, ones column, bias-2 half (plain 16-byte copies, once)
   {
-    const uint4* src = reinterpret_cast<const uint4*>(a.w3 + (size_t)rank * kChunks * kW3Chunk);
-    uint4* dst = reinterpret_cast<uint4*>(sW3);
-    for (int i = threadIdx.x; i < (int)(kChunks * kW3Chunk / 16); i += kThreads) dst[i] = src[i];
-    for (int i = threadIdx.x; i < kN2; i += kThreads) S.b2[i] = a.b2[i];
-    for (int i = threadIdx.x; i < kN3P; i += kThreads) S.b3[i] = i < a.n3 ? a.b3[i] : 0.f;
+    const uint4* s3 = reinterpret_cast<const uint4*>(a.wblk + a.lay.w3 + (size_t)rank * kChunks * kW3Chunk);
+    uint4* d3 = reinterpret_cast<uint4*>(sW3);
+    for (int i = threadIdx.x; i < (int)(kChunks * kW3Chunk / 16); i += kThreads) d3[i] = s3[i];
+    const uint4* so = reinterpret_cast<const uint4*>(a.wblk + a.lay.ones);
+    const uint4* sb = reinterpret_cast<const uint4*>(a.wblk + a.lay.bias2 + (size_t)rank * kTile);
+    uint4* dO = reinterpret_cast<uint4*>(sOnes);
+    uint4* dB = reinterpret_cast<uint4*>(sB2);
+    for (int i = threadIdx.x; i < (int)(kTile / 16); i += kThreads) { dO[i] = so[i]; dB[i] = sb[i]; }
   }
   fence_proxy_async();
   fence_before();
@@ -237,19 +282,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   fence_after();
   const uint32_t tb = S.tbase;
   const uint32_t R1 = tb, R2 = tb + 256u;
+  const int nst = a.lay.nst;
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ producer (both CTAs)
+    // ------------------------------------------------------------------ weight producer (both CTAs)
     if (lane == 0) {
       uint32_t ws = 0;
-      const int nst = a.nkb1 + kNkb2;
-      const uint8_t* src0 = a.wstream + (size_t)rank * nst * kTile;
-      uint32_t tl = 0;
-      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tl++)
+      const uint8_t* src0 = a.wblk + a.lay.stream + (size_t)rank * nst * kTile;
+      for (uint64_t t = t_begin; t < t_end; t++)
         for (int s = 0; s < nst; s++) {
           const uint32_t st = ws % kSW, ph = (ws / kSW) & 1u;
           mbar_wait(&S.w_empty[st], ph ^ 1u);
-          if (s == 0) TR(tl, 31);
           mbar_expect_tx(&S.w_full[st], kTile);
           bulk_g2s(sW + st * kTile, src0 + (size_t)s * kTile, kTile, &S.w_full[st]);
           ws++;
@@ -257,10 +300,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 1) {
-      // ---------------------------------------------------------------- peer relay: W stages
+      // ---------------------------------------------------------------- peer: relay its weight stages
       uint32_t ws = 0;
-      const int nst = a.nkb1 + kNkb2;
-      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters)
+      for (uint64_t t = t_begin; t < t_end; t++)
         for (int s = 0; s < nst; s++) {
           const uint32_t st = ws % kSW, ph = (ws / kSW) & 1u;
           mbar_wait(&S.w_full[st], ph);
@@ -269,96 +311,97 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         }
     } else if (lane == 0 && rank == 0) {
       // ---------------------------------------------------------------- MMA issuer (leader)
-      uint32_t gs = 0, ws = 0, tcount = 0;
+      uint32_t gs = 0, ws = 0, tl = 0;
       const uint32_t id1 = idesc_f16(256, kN1, 1, 1);     // bf16 x bf16 -> f32
       const uint32_t id2 = idesc_f16(256, kN2, 0, 0);     // f16 x f16 -> f32
-      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tcount++) {
-        // layer 1 into R1 (in-order after the previous tile's layer 2 read R1)
-        TR(tcount, 0);
+      for (uint64_t t = t_begin; t < t_end; t++, tl++) {
+        TR(tl, 0);
+        // layer 1 into R1 (issued after the previous tile's layer 2, which read R1: in-order pipe)
         for (int kb = 0; kb < a.nkb1; kb++) {
           const uint32_t g = gs % kSG, w = ws % kSW;
-          mbar_wait_cluster(&S.g_full[g], (gs / kSG) & 1u);
-          if (kb < 13) TR(tcount, 16 + kb);
-          mbar_wait_cluster(&S.w_full[w], (ws / kSW) & 1u);
-          if (kb == 0) TR(tcount, 1);
-          if (kb == a.nkb1 - 1) TR(tcount, 2);
+          mbar_wait(&S.g_full[g], (gs / kSG) & 1u);
+          if (kb < 13) TR(tl, 16 + kb);
+          mbar_wait(&S.w_full[w], (ws / kSW) & 1u);
           fence_after();
           const uint32_t ab = smem_u32(sG + g * kTile), bb = smem_u32(sW + w * kTile);
+          const int nk = min(4, a.nk16 - 4 * kb);
 #pragma unroll
           for (int kk = 0; kk < 4; kk++)
-            mma2_f16_ss(R1, sdesc_sw128(ab + 32u * kk), sdesc_sw128(bb + 32u * kk), id1, (kb | kk) ? 1u : 0u);
+            if (kk < nk) mma2_f16_ss(R1, sdesc_sw128(ab + 32u * kk), sdesc_sw128(bb + 32u * kk), id1, (kb | kk) ? 1u : 0u);
           mma2_commit(&S.g_empty[g], 0x3);
           mma2_commit(&S.w_empty[w], 0x3);
           gs++; ws++;
         }
         mma2_commit(&S.acc1_full, 0x3);
-        // layer 2: A = H1 (fp16 hi | lo) in R1, B = W2 half tiles, D = R2
-        mbar_wait_cluster(&S.h1_ready, tcount & 1u);
-        TR(tcount, 3);
-        mbar_wait_cluster(&S.acc2_free, (tcount & 1u) ^ 1u);
-        TR(tcount, 4);
+        TR(tl, 2);
+        // layer 2: D = R2 <- bias (ones x [b_hi | b_lo]) + H1 (fp16 hi | lo, TMEM) x W2 half tiles
+        mbar_wait(&S.acc2_free, (tl & 1u) ^ 1u);
+        TR(tl, 4);
         fence_after();
+        mma2_f16_ss(R2, sdesc_sw128(smem_u32(sOnes)), sdesc_sw128(smem_u32(sB2)), id2, 0u);
         for (int kb = 0; kb < kNkb2; kb++) {
           const uint32_t w = ws % kSW;
-          mbar_wait_cluster(&S.w_full[w], (ws / kSW) & 1u);
+          mbar_wait(&S.h1_kb[kb], tl & 1u);
+          if (kb == 0) TR(tl, 3);
+          mbar_wait(&S.w_full[w], (ws / kSW) & 1u);
           fence_after();
           const uint32_t bb = smem_u32(sW + w * kTile);
 #pragma unroll
           for (int kk = 0; kk < 4; kk++) {
-            const uint32_t col = 32u * (2u * kb + (kk >> 1)) + 8u * (kk & 1);
+            const uint32_t col = 16u * (4u * kb + kk);      // neurons [col, col+16): hi | lo
             const uint64_t bd = sdesc_sw128(bb + 32u * kk);
-            mma2_f16_ts(R2, R1 + col, bd, id2, (kb | kk) ? 1u : 0u);
-            mma2_f16_ts(R2, R1 + col + 16u, bd, id2, 1u);
+            mma2_f16_ts(R2, R1 + col, bd, id2, 1u);
+            mma2_f16_ts(R2, R1 + col + 8u, bd, id2, 1u);
           }
           mma2_commit(&S.w_empty[w], 0x3);
           ws++;
         }
         mma2_commit(&S.acc2_full, 0x3);
-        TR(tcount, 5);
+        TR(tl, 5);
       }
     }
   } else if (warp == 2) {
     if (lane == 0 && rank == 0) {
       // ---------------------------------------------------------------- layer-3 issuer (leader)
-      uint32_t use[4] = {0, 0, 0, 0};
+      uint32_t hs = 0, tl = 0;
       const uint32_t id3 = idesc_f16(256, kN3P, 0, 0);
-      uint32_t tl = 0;
-      for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tl++) {
+      for (uint64_t t = t_begin; t < t_end; t++, tl++) {
         for (int p = 0; p < kChunks; p++) {
-          const int slot = 2 * (p & 1) + ((p >> 1) & 1);
-          mbar_wait_cluster(&S.h2c_full[slot], use[slot] & 1u);
+          const uint32_t slot = hs % kSH;
+          mbar_wait(&S.h2_full[slot], (hs / kSH) & 1u);
           if (p == 0) TR(tl, 14);
-          use[slot]++;
           fence_after();
           const uint32_t ab = smem_u32(sH2 + slot * kTile), bb = smem_u32(sW3 + p * kW3Chunk);
 #pragma unroll
           for (int kk = 0; kk < 4; kk++)
             mma2_f16_ss(R2, sdesc_sw128(ab + 32u * kk), sdesc_sw128(bb + 32u * kk), id3, (p | kk) ? 1u : 0u);
-          mma2_commit(&S.h2c_empty[slot], 0x3);
+          mma2_commit(&S.h2_empty[slot], 0x3);
+          hs++;
         }
         mma2_commit(&S.acc3_full, 0x3);
         TR(tl, 15);
       }
     }
-  } else if (warp >= 3 && warp < 7) {
+  } else if (warp >= kWGen && warp < kWE1) {
     // ------------------------------------------------------------------ generator (both CTAs)
-    const int r = threadIdx.x - 96;                        // row of this CTA's A tile
-    uint32_t gs = 0;
+    const int gw = warp - kWGen, h = gw >> 2;
+    const int r = 32 * (gw & 3) + lane;                    // row of this CTA's A tile
+    const int gt = threadIdx.x - 32 * kWGen;               // 0..255
+    uint32_t gs = 0, tl = 0;
     const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
     const __nv_bfloat162 st2 = __floats2bfloat162_rn(a.pert.step_f, a.pert.step_f);
     const __nv_bfloat162 or2 = __floats2bfloat162_rn(a.pert.origin_f, a.pert.origin_f);
     const uint32_t step2 = *reinterpret_cast<const uint32_t*>(&st2), org2 = *reinterpret_cast<const uint32_t*>(&or2);
     const int n0 = a.n0;
-    const int full_kb = n0 / 64;                           // K blocks made only of lattice pixels
-    uint32_t tl = 0;
-    for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tl++) {
-      if (r == 0) TR(tl, 6);
+    const int kneed = 16 * a.nk16;                         // K elements the MMA reads
+    for (uint64_t t = t_begin; t < t_end; t++, tl++) {
+      if (gt == 0) TR(tl, 6);
       const TileInfo ti = tile_info(a, t);
       if (ti.b != S.base_g) {                              // stage the base image (bf16) once per base
-        named_bar(1, 128);
-        for (int i = r; i < (a.nkb1 * 64); i += 128) S.xg[i] = i < n0 ? a.bases[(size_t)ti.b * n0 + i] : (uint16_t)0;
-        named_bar(1, 128);
-        if (r == 0) S.base_g = ti.b;
+        named_bar(1, 256);
+        for (int i = gt; i < a.nkb1 * 64; i += 256) S.xg[i] = i < n0 ? a.bases[(size_t)ti.b * n0 + i] : (uint16_t)0;
+        named_bar(1, 256);
+        if (gt == 0) S.base_g = ti.b;
       }
       const int grow = 128 * (int)rank + r;
       uint64_t c;
@@ -369,338 +412,364 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
         mbar_wait(&S.g_empty[st], ph ^ 1u);
         uint8_t* slot = sG + st * kTile;
-        const uint4* xv = reinterpret_cast<const uint4*>(S.xg + 64 * kb);
-        if (kb < full_kb) {
+        const int j = 2 * kb + h;                          // 32-pixel Philox block
+        const int e0 = 32 * j;                             // first K element of this half
+        if (e0 + 32 <= n0) {
+          const uint4 w = philox(c0, c1, cb, (uint32_t)j, k0, k1);
+          const uint4* xv = reinterpret_cast<const uint4*>(S.xg + e0);
+          const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-          for (int hb = 0; hb < 2; hb++) {
-            const uint4 w = philox(c0, c1, cb, (uint32_t)(2 * kb + hb), k0, k1);
-            const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
+          for (int ww = 0; ww < 4; ww++)
+            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (4 * h + ww))) = lattice_word(wsr[ww], xv[ww], step2, org2);
+        } else if (e0 < kneed) {
+          // tail: remaining pixels, then the bias columns (1.0) at K = n0 .. n0+2, then zeros
+          uint4 w = make_uint4(0, 0, 0, 0);
+          if (e0 < n0) w = philox(c0, c1, cb, (uint32_t)j, k0, k1);
+          const uint4* xv = reinterpret_cast<const uint4*>(S.xg + e0);
+          const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int ww = 0; ww < 4; ww++) {
-              const int ch = 4 * hb + ww;                  // 16-byte chunk = 8 pixels
-              *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = lattice_word(wsr[ww], xv[ch], step2, org2);
+          for (int ww = 0; ww < 4; ww++) {
+            const uint4 y = lattice_word(wsr[ww], xv[ww], step2, org2);
+            uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const int e = e0 + 8 * ww + 2 * k;          // K index of the low element
+              uint32_t lo = ys[k] & 0xFFFFu, hi = ys[k] >> 16;
+              if (e >= n0) lo = (e < n0 + 3) ? 0x3F80u : 0u;
+              if (e + 1 >= n0) hi = (e + 1 < n0 + 3) ? 0x3F80u : 0u;
+              ys[k] = lo | (hi << 16);
             }
-          }
-        } else {
-          // tail block: remaining pixels, then the bias columns (1.0) at K = n0 .. n0+2, then zeros
-#pragma unroll
-          for (int hb = 0; hb < 2; hb++) {
-            const int j = 2 * kb + hb;
-            uint4 w = make_uint4(0, 0, 0, 0);
-            if (32 * j < n0) w = philox(c0, c1, cb, (uint32_t)j, k0, k1);
-            const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int ww = 0; ww < 4; ww++) {
-              const int ch = 4 * hb + ww;
-              const uint4 y = lattice_word(wsr[ww], xv[ch], step2, org2);
-              uint32_t ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-              for (int k = 0; k < 4; k++) {
-                const int e = 64 * kb + 8 * ch + 2 * k;     // K index of the low element
-                uint32_t lo = ys[k] & 0xFFFFu, hi = ys[k] >> 16;
-                if (e >= n0) lo = (e < n0 + 3) ? 0x3F80u : 0u;
-                if (e + 1 >= n0) hi = (e + 1 < n0 + 3) ? 0x3F80u : 0u;
-                ys[k] = lo | (hi << 16);
-              }
-              *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = make_uint4(ys[0], ys[1], ys[2], ys[3]);
-            }
+            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (4 * h + ww))) = make_uint4(ys[0], ys[1], ys[2], ys[3]);
           }
         }
         fence_proxy_async();
-        named_bar(1, 128);
-        if (r == 0) arrive_leader(&S.g_full[st], rank);
+        __syncwarp();
+        if (lane == 0) arrive_leader(&S.g_full[st], rank);
         gs++;
       }
-      if (r == 0) TR(tl, 7);
+      if (gt == 0) TR(tl, 7);
     }
-  } else if (warp >= 7) {
-    // ------------------------------------------------------------------ epilogue (both CTAs)
-    const int e = threadIdx.x - 224;                       // 0..255
-    const int grp = e >> 7;                                // 0 or 1
-    const int quad = warp & 3;
-    const int r = 32 * quad + lane;                        // row = TMEM lane
-    const uint32_t loff = (uint32_t)(32 * quad) << 16;
-    uint32_t tcount = 0, h2use[2] = {0, 0};
-    const float tg2 = a.cov.tg_f[1], tg3 = a.cov.tg_f[2], th1 = a.cov.th_f[0], th2 = a.cov.th_f[1];
-    float tau[3];
-#pragma unroll
-    for (int l = 0; l < 3; l++) tau[l] = a.cov.tau_dev ? a.cov.tau_dev[l] : a.cov.tau[l];
+  } else if (warp >= kWE1 && warp < kWE2) {
+    // ------------------------------------------------------------------ E1: layer-1 epilogue
+    const int q = warp & 3, r = 32 * q + lane;             // row = TMEM lane
+    const int et = threadIdx.x - 32 * kWE1;                // 0..127
+    const uint32_t loff = (uint32_t)(32 * q) << 16;
+    const float th1 = a.cov.th_f[0];
+    const float tau0 = a.cov.tau_dev ? a.cov.tau_dev[0] : a.cov.tau[0];
     const bool eval = a.eval_idx != nullptr;
-    for (uint64_t t = cluster; t < a.n_pairs_tiles; t += nclusters, tcount++) {
+    const bool need12 = a.pair12 >= 0 && !eval;
+    uint32_t tl = 0;
+    for (uint64_t t = t_begin; t < t_end; t++, tl++) {
       const TileInfo ti = tile_info(a, t);
       const int grow = 128 * (int)rank + r;
       const bool valid = grow < ti.nvalid;
-      const uint64_t cidx = a.eval_idx ? (valid ? (uint64_t)(ti.start + grow) : 0) : ti.start + (uint64_t)grow;
-      if (ti.b != S.base_e) {                              // stage the base trace once per base
-        named_bar(2, 256);
+      const uint64_t cidx = eval ? (uint64_t)(ti.start + grow) : 0;
+      if (ti.b != S.base_e1) {
+        named_bar(2, 128);
         const float* tr = a.trace + (size_t)ti.b * a.T;
-        for (int i = e; i < kN1; i += 256) S.ub1[i] = tr[i];
-        for (int i = e; i < kN2; i += 256) S.ub2[i] = tr[kN1 + i];
-        for (int i = e; i < kN3P; i += 256) S.ub3[i] = i < a.n3 ? tr[kN1 + kN2 + i] : 0.f;
-        named_bar(2, 256);
-        if (e < 17) {
-          const float* u = e < 8 ? S.ub1 + 32 * e : (e < 16 ? S.ub2 + 32 * (e - 8) : S.ub3);
+        for (int i = et; i < kN1; i += 128) S.ub1[i] = tr[i];
+        named_bar(2, 128);
+        if (et < 8) {
           uint32_t m = 0;
-          for (int i = 0; i < 32; i++) m |= (__float_as_uint(u[i]) >> 31) << i;
-          if (e < 8) S.nb1[e] = m; else if (e < 16) S.nb2[e - 8] = m; else S.nb3 = m & ((a.n3 >= 32) ? ~0u : ((1u << a.n3) - 1u));
-        } else if (e < 20) {
-          const int l = e - 17;
-          const int n = l == 0 ? kN1 : (l == 1 ? kN2 : a.n3);
-          const float* u = l == 0 ? S.ub1 : (l == 1 ? S.ub2 : S.ub3);
+          for (int i = 0; i < 32; i++) m |= (__float_as_uint(S.ub1[32 * et + i]) >> 31) << i;
+          S.nb1[et] = m;
+        } else if (et == 8) {
           float m = 3.0e38f;
-          for (int i = 0; i < n; i++) m = fminf(m, fabsf(u[i]));
-          S.minub[l] = m;
+          for (int i = 0; i < kN1; i++) m = fminf(m, fabsf(S.ub1[i]));
+          S.minub1 = m;
         }
-        named_bar(2, 256);
-        if (e == 0) S.base_e = ti.b;
+        named_bar(2, 128);
+        if (et == 0) S.base_e1 = ti.b;
       }
-      // =========================== E1: layer-1 potentials -> predicates, H1 (fp16 hi|lo) in place
-      mbar_wait(&S.acc1_full, tcount & 1u);
-      if (e == 0) TR(tcount, 8);
+      mbar_wait(&S.acc1_full, tl & 1u);
+      if (et == 0) TR(tl, 8);
       fence_after();
-      int nsc = 0, first = -1;
-      uint32_t fw = 0;
+      // pass A: sign-change count and the first changed neuron i*
+      int nsc = 0, istar = -1;
+#pragma unroll 1
+      for (int p = 0; p < 8; p++) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int hf = 1; hf >= 0; hf--) {
+          uint32_t v[16];
+          tmem_ld16(R1 + loff + 32u * p + 16u * hf, v);
+          tmem_ld_wait();
+          m = sign_fold(v, m);
+          if (eval && valid) {
+#pragma unroll
+            for (int i = 0; i < 16; i++) a.eval_out[cidx * a.T + 32 * p + 16 * hf + i] = __uint_as_float(v[i]);
+          }
+        }
+        const uint32_t scw = m ^ S.nb1[p];
+        nsc += __popc(scw);
+        if (istar < 0 && scw) istar = 32 * p + __ffs(scw) - 1;
+      }
+      // pass B: predicates on the slow path, H1 = fp16 hi | lo in place, handed over per K block
+      const bool slow = __any_sync(0xffffffffu, need12 && valid && nsc <= 1);
       float linf = 0.f, minab = 3.0e38f;
 #pragma unroll 1
-      for (int pi = 0; pi < 4; pi++) {
-        const int p = 4 * grp + pi;
-        uint32_t v[32];
-        tmem_ld32(R1 + loff + 32u * p, v);
-        tmem_ld_wait();
-        uint32_t neg = 0;
+      for (int p = 0; p < 8; p++) {
 #pragma unroll
-        for (int i = 0; i < 32; i++) neg |= (v[i] >> 31) << i;
-        const uint32_t scw = neg ^ S.nb1[p];
-        nsc += __popc(scw);
-        if (first < 0 && scw) { first = p; fw = scw; }
-        const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 32 * p);
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const float4 b4 = ub[q];
-          const float u0 = __uint_as_float(v[4 * q]), u1 = __uint_as_float(v[4 * q + 1]);
-          const float u2 = __uint_as_float(v[4 * q + 2]), u3 = __uint_as_float(v[4 * q + 3]);
-          linf = fmaxf(linf, fmaxf(fmaxf(fabsf(u0 - b4.x), fabsf(u1 - b4.y)), fmaxf(fabsf(u2 - b4.z), fabsf(u3 - b4.w))));
-          minab = fminf(minab, fminf(fminf(fabsf(u0), fabsf(u1)), fminf(fabsf(u2), fabsf(u3))));
-        }
-        if (eval && valid) {
-#pragma unroll
-          for (int i = 0; i < 32; i++) a.eval_out[cidx * a.T + 32 * p + i] = __uint_as_float(v[i]);
-        }
-        uint32_t hi[16], lo[16];
-#pragma unroll
-        for (int k = 0; k < 16; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hi[k], lo[k]);
-        tmem_st16(R1 + loff + 32u * p, hi);
-        tmem_st16(R1 + loff + 32u * p + 16u, lo);
-      }
-      tmem_st_wait();
-      S.x_nsc[grp][r] = nsc; S.x_first[grp][r] = first; S.x_fw[grp][r] = fw;
-      S.x_linf[grp][r] = linf; S.x_minab[grp][r] = minab;
-      fence_before();
-      if (e == 0) TR(tcount, 9);
-      if (e == 128) TR(tcount, 29);
-      named_bar(2, 256);
-      if (e == 0) arrive_leader(&S.h1_ready, rank);
-      // combine the two groups' summaries of layer 1
-      const int o = grp ^ 1;
-      const int nsc1 = nsc + S.x_nsc[o][r];
-      int f1;
-      uint32_t fw1;
-      if (grp == 0) { f1 = first >= 0 ? first : S.x_first[1][r]; fw1 = first >= 0 ? fw : S.x_fw[1][r]; }
-      else { f1 = S.x_first[0][r] >= 0 ? S.x_first[0][r] : first; fw1 = S.x_first[0][r] >= 0 ? S.x_fw[0][r] : fw; }
-      const int istar1 = f1 >= 0 ? 32 * f1 + __ffs(fw1) - 1 : -1;
-      const float linf1 = fmaxf(linf, S.x_linf[o][r]);
-      const float minab1 = fminf(fminf(minab, S.x_minab[o][r]), S.minub[0]);
-      const bool cond1 = (nsc1 == 1) || (nsc1 == 0 && linf1 >= th1);
-      const bool amb1 = minab1 < tau[0] || (nsc1 == 0 && fabsf(linf1 - th1) < tau[0]);
-      // =========================== E2: layer-2 potentials -> predicates, H2 chunks for layer 3
-      mbar_wait(&S.acc2_full, tcount & 1u);
-      if (e == 0) TR(tcount, 10);
-      fence_after();
-      const bool pair12 = a.pair12 >= 0 && cond1 && valid && !eval;
-      const bool any12 = __any_sync(0xffffffffu, pair12);
-      int nsc2 = 0, first2 = -1;
-      uint32_t fw2 = 0;
-      float linf2 = 0.f, minab2 = 3.0e38f, vcamb2 = 3.0e38f;
-      uint32_t scs[4], vcs[4];
-#pragma unroll 1
-      for (int pi = 0; pi < 4; pi++) {
-        const int p = 2 * pi + grp;                        // group g takes pieces of parity g
-        uint32_t v[32];
-        tmem_ld32(R2 + loff + 32u * p, v);
-        tmem_ld_wait();
-        float u[32];
-        const float4* bb = reinterpret_cast<const float4*>(S.b2 + 32 * p);
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const float4 b4 = bb[q];
-          u[4 * q] = __uint_as_float(v[4 * q]) + b4.x;
-          u[4 * q + 1] = __uint_as_float(v[4 * q + 1]) + b4.y;
-          u[4 * q + 2] = __uint_as_float(v[4 * q + 2]) + b4.z;
-          u[4 * q + 3] = __uint_as_float(v[4 * q + 3]) + b4.w;
-        }
-        uint32_t neg = 0;
-#pragma unroll
-        for (int i = 0; i < 32; i++) neg |= (__float_as_uint(u[i]) >> 31) << i;
-        const uint32_t scw = neg ^ S.nb2[p];
-        nsc2 += __popc(scw);
-        if (first2 < 0 && scw) { first2 = p; fw2 = scw; }
-        const float4* ub = reinterpret_cast<const float4*>(S.ub2 + 32 * p);
-        uint32_t vcw = 0;
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const float4 b4 = ub[q];
-          const float d0 = fabsf(u[4 * q] - b4.x), d1 = fabsf(u[4 * q + 1] - b4.y);
-          const float d2 = fabsf(u[4 * q + 2] - b4.z), d3 = fabsf(u[4 * q + 3] - b4.w);
-          linf2 = fmaxf(linf2, fmaxf(fmaxf(d0, d1), fmaxf(d2, d3)));
-          minab2 = fminf(minab2, fminf(fminf(fabsf(u[4 * q]), fabsf(u[4 * q + 1])), fminf(fabsf(u[4 * q + 2]), fabsf(u[4 * q + 3]))));
-          if (any12) {
-            const float dd[4] = {d0, d1, d2, d3};
+        for (int hf = 0; hf < 2; hf++) {                   // 16 neurons at a time (register budget)
+          uint32_t v[16];
+          tmem_ld16(R1 + loff + 32u * p + 16u * hf, v);
+          tmem_ld_wait();
+          if (slow) {
+            const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 32 * p + 16 * hf);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-              if (dd[k] >= tg2) vcw |= 1u << (4 * q + k);
-              vcamb2 = fminf(vcamb2, fabsf(dd[k] - tg2));
+              const float4 b4 = ub[k];
+              const float u0 = __uint_as_float(v[4 * k]), u1 = __uint_as_float(v[4 * k + 1]);
+              const float u2 = __uint_as_float(v[4 * k + 2]), u3 = __uint_as_float(v[4 * k + 3]);
+              linf = fmaxf(linf, fmaxf(fmaxf(fabsf(u0 - b4.x), fabsf(u1 - b4.y)), fmaxf(fabsf(u2 - b4.z), fabsf(u3 - b4.w))));
+              minab = fminf(minab, fminf(fminf(fabsf(u0), fabsf(u1)), fminf(fabsf(u2), fabsf(u3))));
             }
           }
-        }
-        scs[pi] = scw;
-        vcs[pi] = vcw & ~scw;
-        if (eval && valid) {
+          uint32_t hi[8], lo[8];
 #pragma unroll
-          for (int i = 0; i < 32; i++) a.eval_out[cidx * a.T + kN1 + 32 * p + i] = u[i];
+          for (int k = 0; k < 8; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hi[k], lo[k]);
+          // in place: the 16 fp32 columns of these neurons become [hi (8 cols) | lo (8 cols)]
+          tmem_st8(R1 + loff + 32u * p + 16u * hf, hi);
+          tmem_st8(R1 + loff + 32u * p + 16u * hf + 8u, lo);
         }
-        // stage [hi 32 | lo 32] of this piece as layer-3 A chunk p
-        const int slot = 2 * grp + (pi & 1);
-        mbar_wait(&S.h2c_empty[slot], (h2use[pi & 1] & 1u) ^ 1u);
-        h2use[pi & 1]++;
-        uint8_t* dst = sH2 + slot * kTile;
-        uint32_t hi[16], lo[16];
-#pragma unroll
-        for (int k = 0; k < 16; k++) split_pair(u[2 * k], u[2 * k + 1], hi[k], lo[k]);
-#pragma unroll
-        for (int m = 0; m < 4; m++) {
-          *reinterpret_cast<uint4*>(dst + sw128_off(r, 16 * m)) = make_uint4(hi[4 * m], hi[4 * m + 1], hi[4 * m + 2], hi[4 * m + 3]);
-          *reinterpret_cast<uint4*>(dst + sw128_off(r, 64 + 16 * m)) = make_uint4(lo[4 * m], lo[4 * m + 1], lo[4 * m + 2], lo[4 * m + 3]);
+        if (p & 1) {
+          tmem_st_wait();
+          fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_leader(&S.h1_kb[p >> 1], rank);
         }
-        fence_proxy_async();
-        fence_before();
-        named_bar(3 + grp, 128);
-        if ((e & 127) == 0) arrive_leader(&S.h2c_full[slot], rank);
       }
-      // combine summaries of layer 2 and finish pair (1, 2)
-      S.x_nsc[grp][r] = nsc2; S.x_first[grp][r] = first2; S.x_fw[grp][r] = fw2;
-      S.x_linf[grp][r] = linf2; S.x_minab[grp][r] = minab2; S.x_vcamb[grp][r] = vcamb2;
-      if (e == 128) TR(tcount, 30);
-      named_bar(2, 256);
-      if (e == 0) TR(tcount, 11);
-      const int nsc2t = nsc2 + S.x_nsc[o][r];
-      int f2 = first2;
-      uint32_t fw2t = fw2;
-      if (S.x_first[o][r] >= 0 && (f2 < 0 || S.x_first[o][r] < f2)) { f2 = S.x_first[o][r]; fw2t = S.x_fw[o][r]; }
-      const int istar2 = f2 >= 0 ? 32 * f2 + __ffs(fw2t) - 1 : -1;
-      const float linf2t = fmaxf(linf2, S.x_linf[o][r]);
-      const float minab2t = fminf(fminf(minab2, S.x_minab[o][r]), S.minub[1]);
-      const float vcamb2t = fminf(vcamb2, S.x_vcamb[o][r]);
-      if (pair12) {
-        const bool certain = !amb1 && minab2t >= tau[1] && vcamb2t >= tau[1];
+      if (et == 0) TR(tl, 9);
+      // summary for E2 (pair (1, 2) is decided by layer 1 alone)
+      minab = fminf(minab, S.minub1);
+      const bool cond1 = need12 && valid && ((nsc == 1) || (nsc == 0 && linf >= th1));
+      const bool amb1 = minab < tau0 || (nsc == 0 && fabsf(linf - th1) < tau0);
+      S.info[tl & 1][r] = (cond1 ? 1 : 0) | (nsc == 1 ? 2 : 0) | (amb1 ? 4 : 0) | ((istar & 0xFFFF) << 8);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.info_full[tl & 1]);
+    }
+  } else if (warp >= kWE2) {
+    // ------------------------------------------------------------------ E2 / E3: layers 2 and 3
+    const int q = warp & 3, r = 32 * q + lane;
+    const int et = threadIdx.x - 32 * kWE2;                // 0..127
+    const uint32_t loff = (uint32_t)(32 * q) << 16;
+    const float tg2 = a.cov.tg_f[1], tg3 = a.cov.tg_f[2], th2 = a.cov.th_f[1];
+    const float tau1 = a.cov.tau_dev ? a.cov.tau_dev[1] : a.cov.tau[1];
+    const float tau2 = a.cov.tau_dev ? a.cov.tau_dev[2] : a.cov.tau[2];
+    const bool eval = a.eval_idx != nullptr;
+    const bool need23 = a.pair23 >= 0 && !eval;
+    uint32_t tl = 0, hs = 0;
+    for (uint64_t t = t_begin; t < t_end; t++, tl++) {
+      const TileInfo ti = tile_info(a, t);
+      const int grow = 128 * (int)rank + r;
+      const bool valid = grow < ti.nvalid;
+      const uint64_t cidx = eval ? (uint64_t)(ti.start + grow) : 0;
+      if (ti.b != S.base_e2) {
+        named_bar(3, 128);
+        const float* tr = a.trace + (size_t)ti.b * a.T;
+        for (int i = et; i < kN2; i += 128) S.ub2[i] = tr[kN1 + i];
+        if (et < kN3P) {
+          S.ub3[et] = et < a.n3 ? tr[kN1 + kN2 + et] : 0.f;
+          S.b3[et] = et < a.n3 ? a.b3[et] : 0.f;
+        }
+        named_bar(3, 128);
+        if (et < 8) {
+          uint32_t m = 0;
+          for (int i = 0; i < 32; i++) m |= (__float_as_uint(S.ub2[32 * et + i]) >> 31) << i;
+          S.nb2[et] = m;
+        } else if (et == 8) {
+          uint32_t m = 0;
+          for (int i = 0; i < a.n3; i++) m |= (__float_as_uint(S.ub3[i]) >> 31) << i;
+          S.nb3 = m;
+        } else if (et == 9) {
+          float m = 3.0e38f;
+          for (int i = 0; i < kN2; i++) m = fminf(m, fabsf(S.ub2[i]));
+          S.minub2 = m;
+        } else if (et == 10) {
+          float m = 3.0e38f;
+          for (int i = 0; i < a.n3; i++) m = fminf(m, fabsf(S.ub3[i]));
+          S.minub3 = m;
+          S.bcls = a.cls[ti.b];
+        }
+        named_bar(3, 128);
+        if (et == 0) S.base_e2 = ti.b;
+      }
+      mbar_wait(&S.acc2_full, tl & 1u);
+      if (et == 0) TR(tl, 10);
+      fence_after();
+      mbar_wait(&S.info_full[tl & 1], (tl >> 1) & 1u);
+      const int info = S.info[tl & 1][r];
+      const bool cond1 = info & 1, one1 = info & 2, amb1 = info & 4;
+      const int istar1 = info >> 8;
+      // pass A: sign-change words of layer 2 (kept in shared memory, row-private)
+      int nsc = 0, istar2 = -1;
+#pragma unroll 1
+      for (int p = 0; p < 8; p++) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int hf = 1; hf >= 0; hf--) {
+          uint32_t v[16];
+          tmem_ld16(R2 + loff + 32u * p + 16u * hf, v);
+          tmem_ld_wait();
+          m = sign_fold(v, m);
+          if (eval && valid) {
+#pragma unroll
+            for (int i = 0; i < 16; i++) a.eval_out[cidx * a.T + kN1 + 32 * p + 16 * hf + i] = __uint_as_float(v[i]);
+          }
+        }
+        const uint32_t scw = m ^ S.nb2[p];
+        S.sc2[p][r] = scw;
+        nsc += __popc(scw);
+        if (istar2 < 0 && scw) istar2 = 32 * p + __ffs(scw) - 1;
+      }
+      // pass B: H2 chunks for layer 3; slow path: value changes / L-inf / min|u| of layer 2
+      const bool slow = __any_sync(0xffffffffu, cond1 || (need23 && valid && nsc <= 1));
+      float linf = 0.f, minab = 3.0e38f, vcamb = 3.0e38f;
+#pragma unroll 1
+      for (int p = 0; p < 8; p++) {
+        const uint32_t slot = hs % kSH;
+        mbar_wait(&S.h2_empty[slot], ((hs / kSH) & 1u) ^ 1u);
+        uint8_t* dst = sH2 + slot * kTile;
+        uint32_t vw = 0;
+#pragma unroll
+        for (int hf = 0; hf < 2; hf++) {                   // 16 neurons at a time (register budget)
+          uint32_t v[16];
+          tmem_ld16(R2 + loff + 32u * p + 16u * hf, v);
+          tmem_ld_wait();
+          if (slow) {
+            const float4* ub = reinterpret_cast<const float4*>(S.ub2 + 32 * p + 16 * hf);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const float4 b4 = ub[k];
+              const float uu[4] = {__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]),
+                                   __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])};
+              const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+              for (int i = 0; i < 4; i++) {
+                const float d = fabsf(uu[i] - bb[i]);
+                linf = fmaxf(linf, d);
+                minab = fminf(minab, fabsf(uu[i]));
+                vcamb = fminf(vcamb, fabsf(d - tg2));
+                vw |= (d >= tg2 ? 1u : 0u) << (16 * hf + 4 * k + i);
+              }
+            }
+          }
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int k = 0; k < 8; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hi[k], lo[k]);
+#pragma unroll
+          for (int m = 0; m < 2; m++) {
+            *reinterpret_cast<uint4*>(dst + sw128_off(r, 32 * hf + 16 * m)) = make_uint4(hi[4 * m], hi[4 * m + 1], hi[4 * m + 2], hi[4 * m + 3]);
+            *reinterpret_cast<uint4*>(dst + sw128_off(r, 64 + 32 * hf + 16 * m)) = make_uint4(lo[4 * m], lo[4 * m + 1], lo[4 * m + 2], lo[4 * m + 3]);
+          }
+        }
+        if (slow) S.vc2[p][r] = vw & ~S.sc2[p][r];
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) arrive_leader(&S.h2_full[slot], rank);
+        hs++;
+      }
+      if (et == 0) TR(tl, 11);
+      minab = fminf(minab, S.minub2);
+      // pair (1, 2): SS / SV row i* (nsc1 == 1) or VS / VV column masks (nsc1 == 0), reading C8
+      if (cond1) {
+        const bool certain = !amb1 && minab >= tau1 && vcamb >= tau1;
         const uint32_t* off = a.cov.off[a.pair12];
 #pragma unroll
-        for (int pi = 0; pi < 4; pi++) {
-          const int p = 2 * pi + grp;
-          const uint32_t sw = scs[pi], vw = vcs[pi];
+        for (int p = 0; p < 8; p++) {
           uint32_t is, iv;
-          if (nsc1 == 1) { is = off[0] + istar1 * 8 + p; iv = off[1] + istar1 * 8 + p; }
+          if (one1) { is = off[0] + istar1 * 8 + p; iv = off[1] + istar1 * 8 + p; }
           else { is = off[2] + p; iv = off[3] + p; }
-          if (sw) { atomicOr(&a.res.cov_all[is], sw); if (certain) atomicOr(&a.res.cov_certain[is], sw); }
+          const uint32_t scw = S.sc2[p][r];
+          if (scw) { atomicOr(&a.res.cov_all[is], scw); if (certain) atomicOr(&a.res.cov_certain[is], scw); }
+          const uint32_t vcw = S.vc2[p][r];
+          if (vcw) { atomicOr(&a.res.cov_all[iv], vcw); if (certain) atomicOr(&a.res.cov_certain[iv], vcw); }
+        }
+      }
+      const bool cond2 = need23 && valid && ((nsc == 1) || (nsc == 0 && linf >= th2));
+      const bool amb2 = minab < tau1 || (nsc == 0 && fabsf(linf - th2) < tau1);
+      // ============================ E3: logits -> pair (2, 3), argmax, property, counts
+      mbar_wait(&S.acc3_full, tl & 1u);
+      if (et == 0) TR(tl, 12);
+      fence_after();
+      uint32_t v[16];
+      tmem_ld16(R2 + loff, v);
+      tmem_ld_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&S.acc2_free, rank);
+      const int n3 = a.n3;
+      float y[16];
+#pragma unroll
+      for (int i = 0; i < 16; i++) y[i] = __uint_as_float(v[i]) + S.b3[i];
+      if (eval) {
+        if (valid)
+          for (int i = 0; i < n3; i++) a.eval_out[cidx * a.T + kN1 + kN2 + i] = y[i];
+      } else {
+        const int bcls = S.bcls;
+        if (cond2) {
+          uint32_t neg = 0, vcw = 0;
+          float minab3 = S.minub3, vcamb3 = 3.0e38f;
+#pragma unroll
+          for (int i = 0; i < 16; i++)
+            if (i < n3) {
+              neg |= (__float_as_uint(y[i]) >> 31) << i;
+              const float d = fabsf(y[i] - S.ub3[i]);
+              if (d >= tg3) vcw |= 1u << i;
+              vcamb3 = fminf(vcamb3, fabsf(d - tg3));
+              minab3 = fminf(minab3, fabsf(y[i]));
+            }
+          const uint32_t scw = neg ^ S.nb3;
+          const uint32_t vw = vcw & ~scw;
+          const bool certain = !amb2 && minab3 >= tau2 && vcamb3 >= tau2;
+          const uint32_t* off = a.cov.off[a.pair23];
+          uint32_t is, iv;
+          if (nsc == 1) { is = off[0] + istar2; iv = off[1] + istar2; }
+          else { is = off[2]; iv = off[3]; }
+          if (scw) { atomicOr(&a.res.cov_all[is], scw); if (certain) atomicOr(&a.res.cov_certain[is], scw); }
           if (vw) { atomicOr(&a.res.cov_all[iv], vw); if (certain) atomicOr(&a.res.cov_certain[iv], vw); }
         }
-      }
-      const bool cond2 = (nsc2t == 1) || (nsc2t == 0 && linf2t >= th2);
-      const bool amb2 = minab2t < tau[1] || (nsc2t == 0 && fabsf(linf2t - th2) < tau[1]);
-      // =========================== E3: logits -> pair (2, 3), argmax, property, counts (group 0)
-      if (grp == 0) {
-        mbar_wait(&S.acc3_full, tcount & 1u);
-        if (e == 0) TR(tcount, 12);
-        fence_after();
-        uint32_t v[16];
-        tmem_ld16(R2 + loff, v);
-        tmem_ld_wait();
-        fence_before();
-        named_bar(3, 128);
-        if (e == 0) arrive_leader(&S.acc2_free, rank);
-        const int n3 = a.n3;
-        float y[16];
+        // argmax (lowest index on ties), margin, property
+        int cls = 0;
+        float top1 = y[0];
 #pragma unroll
-        for (int i = 0; i < 16; i++) y[i] = __uint_as_float(v[i]) + S.b3[i];
-        if (eval) {
-          if (valid)
-            for (int i = 0; i < n3; i++) a.eval_out[cidx * a.T + kN1 + kN2 + i] = y[i];
+        for (int i = 1; i < 16; i++) if (i < n3 && y[i] > top1) { top1 = y[i]; cls = i; }
+        bool viol = false, flag = false;
+        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+          const int D = a.prop.target >= 0 ? a.prop.target : bcls;
+          bool any = false;
+          float yD = 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; i++)
+            if (i < n3) {
+              if (i == D) yD = y[i];
+              if (i != D && y[i] > a.prop.V_f) any = true;
+              if (fabsf(y[i] - a.prop.V_f) < a.cov.near_tie) flag = true;
+            }
+          viol = yD < a.prop.V_f && any;
         } else {
-          const int bcls = a.cls[ti.b];
-          // pair (2, 3)
-          if (a.pair23 >= 0 && cond2 && valid) {
-            uint32_t neg = 0, vcw = 0;
-            float minab3 = S.minub[2], vcamb3 = 3.0e38f;
+          float top2 = -3.0e38f;
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-              if (i < n3) {
-                neg |= (__float_as_uint(y[i]) >> 31) << i;
-                const float d = fabsf(y[i] - S.ub3[i]);
-                if (d >= tg3) vcw |= 1u << i;
-                vcamb3 = fminf(vcamb3, fabsf(d - tg3));
-                minab3 = fminf(minab3, fabsf(y[i]));
-              }
-            const uint32_t scw = neg ^ S.nb3;
-            const uint32_t vw = vcw & ~scw;
-            const bool certain = !amb2 && minab3 >= tau[2] && vcamb3 >= tau[2];
-            const uint32_t* off = a.cov.off[a.pair23];
-            uint32_t is, iv;
-            if (nsc2t == 1) { is = off[0] + istar2; iv = off[1] + istar2; }
-            else { is = off[2]; iv = off[3]; }
-            if (scw) { atomicOr(&a.res.cov_all[is], scw); if (certain) atomicOr(&a.res.cov_certain[is], scw); }
-            if (vw) { atomicOr(&a.res.cov_all[iv], vw); if (certain) atomicOr(&a.res.cov_certain[iv], vw); }
-          }
-          // argmax (lowest index on ties), margin, property
-          int cls = 0;
-          float top1 = y[0];
-#pragma unroll
-          for (int i = 1; i < 16; i++) if (i < n3 && y[i] > top1) { top1 = y[i]; cls = i; }
-          bool viol = false, flag = false;
-          if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
-            const int D = a.prop.target >= 0 ? a.prop.target : bcls;
-            bool any = false;
-            float yD = 0.f;
-#pragma unroll
-            for (int i = 0; i < 16; i++)
-              if (i < n3) {
-                if (i == D) yD = y[i];
-                if (i != D && y[i] > a.prop.V_f) any = true;
-                if (fabsf(y[i] - a.prop.V_f) < a.cov.near_tie) flag = true;
-              }
-            viol = yD < a.prop.V_f && any;
-          } else {
-            float top2 = -3.0e38f;
-#pragma unroll
-            for (int i = 0; i < 16; i++) if (i < n3 && i != cls && y[i] > top2) top2 = y[i];
-            flag = n3 > 1 && top1 - top2 < a.cov.near_tie;
-            viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != bcls;
-          }
-          if (!valid) { viol = false; flag = false; }
-          const uint32_t nv = __reduce_add_sync(0xffffffffu, viol ? 1u : 0u);
-          const uint32_t nf = __reduce_add_sync(0xffffffffu, flag ? 1u : 0u);
-          const uint32_t nc = __reduce_add_sync(0xffffffffu, valid ? 1u : 0u);
-          const uint32_t rel = viol ? (uint32_t)grow : 0xFFFFFFFFu;
-          const uint32_t relu = (viol && !flag) ? (uint32_t)grow : 0xFFFFFFFFu;
-          const uint32_t mn = __reduce_min_sync(0xffffffffu, rel), mnu = __reduce_min_sync(0xffffffffu, relu);
-          if (lane == 0) {
-            if (nc) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.checked) + ti.b, (unsigned long long)nc);
-            if (nv) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.violated) + ti.b, (unsigned long long)nv);
-            if (nf) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.flagged) + ti.b, (unsigned long long)nf);
-            if (mn != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex) + ti.b, (unsigned long long)(ti.start + mn));
-            if (mnu != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex_unflagged) + ti.b, (unsigned long long)(ti.start + mnu));
-          }
+          for (int i = 0; i < 16; i++) if (i < n3 && i != cls && y[i] > top2) top2 = y[i];
+          flag = n3 > 1 && top1 - top2 < a.cov.near_tie;
+          viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != bcls;
         }
-        if (e == 0) TR(tcount, 13);
+        if (!valid) { viol = false; flag = false; }
+        const uint32_t nv = __reduce_add_sync(0xffffffffu, viol ? 1u : 0u);
+        const uint32_t nf = __reduce_add_sync(0xffffffffu, flag ? 1u : 0u);
+        const uint32_t nc = __reduce_add_sync(0xffffffffu, valid ? 1u : 0u);
+        const uint32_t rel = viol ? (uint32_t)grow : 0xFFFFFFFFu;
+        const uint32_t relu = (viol && !flag) ? (uint32_t)grow : 0xFFFFFFFFu;
+        const uint32_t mn = __reduce_min_sync(0xffffffffu, rel), mnu = __reduce_min_sync(0xffffffffu, relu);
+        if (lane == 0) {
+          if (nc) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.checked) + ti.b, (unsigned long long)nc);
+          if (nv) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.violated) + ti.b, (unsigned long long)nv);
+          if (nf) atomicAdd(reinterpret_cast<unsigned long long*>(a.res.flagged) + ti.b, (unsigned long long)nf);
+          if (mn != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex) + ti.b, (unsigned long long)(ti.start + mn));
+          if (mnu != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex_unflagged) + ti.b, (unsigned long long)(ti.start + mnu));
+        }
       }
+      if (et == 0) TR(tl, 13);
     }
   }
   fence_before();
@@ -721,7 +790,7 @@ extern "C" int mlpv_f3_trace_read(void* host) {
 // ------------------------------------------------------------------------------------------- host
 bool fused3_applicable(const DevNet& net) {
   return net.numeric == MLPV_NUM_BF16 && net.L == 3 && net.sizes[1] == f3::kN1 && net.sizes[2] == f3::kN2 &&
-         net.sizes[3] <= 16 && net.sizes[0] % 2 == 0 && net.sizes[0] + 3 <= f3::kMaxN0;
+         net.sizes[3] <= f3::kN3P && net.sizes[0] % 2 == 0 && net.sizes[0] + 3 <= f3::kMaxN0;
 }
 
 static size_t sw128_h(uint32_t row, uint32_t byte) {
@@ -744,26 +813,33 @@ static uint16_t f2h(float f) {
   memcpy(&u, &h, 2);
   return u;
 }
+static float h2f(uint16_t u) {
+  __half h;
+  memcpy(&h, &u, 2);
+  return __half2float(h);
+}
 
-// Weight layouts of k_fused3 (host-side, once per handle):
+// Device weight block of k_fused3 (host-side, once per handle), see f3::Layout:
 //   stream [rank][nkb1 + 4][16 KB]: W1 rows [128 rank, +128) per K block (bias hi/mid/lo at K = n0..n0+2),
 //          then W2 (fp16) rows [128 rank, +128) per K block of 64 layer-1 neurons;
-//   w3 [rank][8][2 KB]: W3 (fp16) rows [16 rank, +16) (rows >= n3 zero), chunk p = [W3[:, 32p..] | same].
-cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const void* const* b_host, void** stream_dev,
-                           void** w3_dev) {
+//   w3 [rank][8][1 KB]: W3 (fp16) rows [8 rank, +8) (rows >= n3 zero), chunk p = [W3[:, 32p..] | same];
+//   ones [16 KB]: A operand of the layer-2 bias MMA (1.0 at K = 0, 1 of every row);
+//   bias2 [rank][16 KB]: B operand, row n = [RN_f16(b2[n]), RN_f16(b2[n] - hi), 0 ...] (K-major).
+cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const void* const* b_host, void** blk_dev) {
   const int n0 = net.sizes[0], n3 = net.sizes[3];
-  const int nkb1 = (2 * (n0 + 3) + 127) / 128;
-  const int nst = nkb1 + f3::kNkb2;
-  std::vector<uint8_t> st((size_t)2 * nst * f3::kTile, 0), w3((size_t)2 * f3::kChunks * f3::kW3Chunk, 0);
+  const f3::Layout L = f3::layout_of(n0);
+  std::vector<uint8_t> blk(L.total, 0);
   const uint16_t* W1 = static_cast<const uint16_t*>(W_host[0]);
   const uint16_t* W2 = static_cast<const uint16_t*>(W_host[1]);
   const uint16_t* W3 = static_cast<const uint16_t*>(W_host[2]);
   const float* b1 = static_cast<const float*>(b_host[0]);
+  const float* b2 = static_cast<const float*>(b_host[1]);
   auto put16 = [&](uint8_t* tile, int row, int kelem, uint16_t v) {
     const size_t o = sw128_h((uint32_t)row, (uint32_t)(2 * (kelem % 64)));
     tile[o] = (uint8_t)(v & 0xFF);
     tile[o + 1] = (uint8_t)(v >> 8);
   };
+  uint8_t* st = blk.data() + L.stream;
   for (int rk = 0; rk < 2; rk++) {
     for (int rr = 0; rr < 128; rr++) {
       const int n = 128 * rk + rr;
@@ -778,19 +854,26 @@ cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const v
           const float r2 = r1 - bf2f(p2);
           v = k == n0 ? p1 : (k == n0 + 1 ? p2 : f2bf(r2));
         }
-        put16(st.data() + ((size_t)rk * nst + k / 64) * f3::kTile, rr, k, v);
+        put16(st + ((size_t)rk * L.nst + k / 64) * f3::kTile, rr, k, v);
       }
       for (int k = 0; k < f3::kN1; k++) {
         const uint16_t h = f2h(bf2f(W2[(size_t)n * f3::kN1 + k]));      // exact for |w| >= 2^-17
-        put16(st.data() + ((size_t)rk * nst + nkb1 + k / 64) * f3::kTile, rr, k, h);
+        put16(st + ((size_t)rk * L.nst + L.nkb1 + k / 64) * f3::kTile, rr, k, h);
       }
+      // bias-2 B operand: row rr of this CTA's half
+      const float b = b2[n];
+      const uint16_t bh = f2h(b);
+      const uint16_t bl = f2h(b - h2f(bh));
+      uint8_t* bt = blk.data() + L.bias2 + (size_t)rk * f3::kTile;
+      put16(bt, rr, 0, bh);
+      put16(bt, rr, 1, bl);
     }
-    for (int rr = 0; rr < 16; rr++) {
-      const int n = 16 * rk + rr;
+    for (int rr = 0; rr < 8; rr++) {
+      const int n = 8 * rk + rr;
       for (int p = 0; p < f3::kChunks; p++)
         for (int i = 0; i < 32; i++) {
           const uint16_t h = n < n3 ? f2h(bf2f(W3[(size_t)n * f3::kN2 + 32 * p + i])) : (uint16_t)0;
-          uint8_t* tile = w3.data() + ((size_t)rk * f3::kChunks + p) * f3::kW3Chunk;
+          uint8_t* tile = blk.data() + L.w3 + ((size_t)rk * f3::kChunks + p) * f3::kW3Chunk;
           for (int half = 0; half < 2; half++) {
             const size_t o = sw128_h((uint32_t)rr, (uint32_t)(64 * half + 2 * i));
             tile[o] = (uint8_t)(h & 0xFF);
@@ -799,27 +882,27 @@ cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const v
         }
     }
   }
-  cudaError_t e = cudaMalloc(stream_dev, st.size());
+  for (int rr = 0; rr < 128; rr++) {
+    put16(blk.data() + L.ones, rr, 0, 0x3C00u);          // fp16 1.0
+    put16(blk.data() + L.ones, rr, 1, 0x3C00u);
+  }
+  cudaError_t e = cudaMalloc(blk_dev, blk.size());
   if (e != cudaSuccess) return e;
-  e = cudaMemcpy(*stream_dev, st.data(), st.size(), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return e;
-  e = cudaMalloc(w3_dev, w3.size());
-  if (e != cudaSuccess) return e;
-  return cudaMemcpy(*w3_dev, w3.data(), w3.size(), cudaMemcpyHostToDevice);
+  return cudaMemcpy(*blk_dev, blk.data(), blk.size(), cudaMemcpyHostToDevice);
 }
 
-cudaError_t launch_fused3(const DevNet& net, const void* stream_w, const void* w3, const void* bases, int n_base,
-                          const DevPert& pert, const DevProp& prop, const DevCov& cov, const DevResult& res,
-                          BaseWS ws, const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
-                          int num_sms, cudaStream_t st) {
+cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases, int n_base, const DevPert& pert,
+                          const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
+                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
+                          cudaStream_t st) {
   f3::Args a;
   memset(&a, 0, sizeof a);
   a.n0 = net.sizes[0];
   a.n3 = net.sizes[3];
-  a.nkb1 = (2 * (a.n0 + 3) + 127) / 128;
-  a.wstream = static_cast<const uint8_t*>(stream_w);
-  a.w3 = static_cast<const uint8_t*>(w3);
-  a.b2 = static_cast<const float*>(net.b[1]);
+  a.lay = f3::layout_of(a.n0);
+  a.nkb1 = a.lay.nkb1;
+  a.nk16 = a.lay.nk16;
+  a.wblk = static_cast<const uint8_t*>(blk);
   a.b3 = static_cast<const float*>(net.b[2]);
   a.bases = static_cast<const uint16_t*>(bases);
   a.pert = pert; a.prop = prop; a.cov = cov; a.res = res;

@@ -597,23 +597,22 @@ static size_t sw128_host(uint32_t row, uint32_t byte) {
 }
 
 bool fused3_applicable(const DevNet& net);
-cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const void* const* b_host, void** stream_dev,
-                           void** w3_dev);
-cudaError_t launch_fused3(const DevNet& net, const void* stream_w, const void* w3, const void* bases, int n_base,
-                          const DevPert& pert, const DevProp& prop, const DevCov& cov, const DevResult& res,
-                          BaseWS ws, const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
-                          int num_sms, cudaStream_t st);
+cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const void* const* b_host, void** blk_dev);
+cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases, int n_base, const DevPert& pert,
+                          const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
+                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
+                          cudaStream_t st);
 
 static bool use_fused3(const DevNet& net) {
   const char* env = getenv("MLPV_NO_FUSED3");
   return fused3_applicable(net) && !(env && env[0] == '1');
 }
 
-// Wt_dev[0]: generic tiles; Wt_dev[1], Wt_dev[2]: k_fused3 weight stream and W3 (when applicable)
+// Wt_dev[0]: generic tiles; Wt_dev[1]: k_fused3 weight block (when applicable)
 cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const void* const* b_host, void** Wt_dev,
                           std::string* why) {
   if (fused3_applicable(net)) {
-    cudaError_t e = prepare_fused3(net, W_host, b_host, &Wt_dev[1], &Wt_dev[2]);
+    cudaError_t e = prepare_fused3(net, W_host, b_host, &Wt_dev[1]);
     if (e != cudaSuccess) return e;
   }
   LargeGeom g;
@@ -666,9 +665,9 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* b
                          const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
                          cudaStream_t st, bool* supported, std::string* why) {
-  if (use_fused3(net) && Wt[1] && Wt[2]) {
+  if (use_fused3(net) && Wt[1]) {
     *supported = true;
-    return launch_fused3(net, Wt[1], Wt[2], bases, n_base, pert, prop, cov, res, ws, eval_idx, eval_n, eval_base,
+    return launch_fused3(net, Wt[1], bases, n_base, pert, prop, cov, res, ws, eval_idx, eval_n, eval_base,
                          eval_out, num_sms, st);
   }
   LargeGeom g;
