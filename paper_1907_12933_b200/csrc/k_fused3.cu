@@ -15,15 +15,17 @@
 //            with a candidate whose sc1 count is <= 1 (the only ones a covering method can fire on).
 //   layer 2  A = H1 straight from TMEM, B = W2 (fp16, duplicated for the lo half); the bias is one
 //            more SS MMA (ones column x [b_hi | b_lo]); accumulator TMEM cols [256,512).
-//   E2       4 warps: pass A sign words sc2; pass B fp16 hi/lo of h2 into 32-neuron shared-memory
-//            chunks for layer 3, plus the pair-(1,2) coverage and pair-(2,3) predicates on the
-//            (warp-uniform) slow path.
-//   layer 3  N = 16 (n_3 <= 16), one MMA chain per chunk, accumulator in the drained cols [256,272).
+//   E2       4 warps: pass A sign words sc2; pass B turns u2 in place into the fp16 hi/lo split of
+//            h2 (neurons 0-239; 240-255 go to a small shared-memory tile so that their 16 columns
+//            can hold the layer-3 accumulator), plus the pair-(1,2) coverage and pair-(2,3)
+//            predicates on the (warp-uniform) slow path.
+//   layer 3  N = 16 (n_3 <= 16): A = H2 from TMEM (and the tail tile), accumulator TMEM cols
+//            [496,512).
 //   E3       E2's warps: logits, pair (2,3), argmax / margin / property, counts, first counterexample.
 //
 // Warp roles (20 warps): 0 weight producer, 1 MMA issuer (leader) / weight relay (peer) and TMEM
-// owner, 2 layer-3 issuer (leader), 3 idle, 4-11 generator (8 warps: row quadrant x half K block),
-// 12-15 E1, 16-19 E2/E3.
+// owner, 2 layer-3 issuer (leader), 3 idle, 4-11 generator (two groups of four warps taking
+// alternate ring stages), 12-15 E1, 16-19 E2/E3.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -44,14 +46,20 @@ namespace f3 {
 // debug timeline (tools/trace_fused3.py): clock64 stamps of the first 64 tiles of cluster 0
 __device__ unsigned long long g_trace[2][64][32];
 #define TR(tl, ev) do { if (cluster == 0 && (tl) < 64) g_trace[rank][(tl)][(ev)] = clock64(); } while (0)
+// generator detail: [rank][h][tile 8..11][kb 0..12][event 0..4]
+__device__ unsigned long long g_trace_gen[2][2][4][13][5];
+#define TRG(tl, kb, ev) do { if (cluster == 0 && lane == 0 && (gw & 3) == 0 && (tl) >= 8 && (tl) < 12) \
+    g_trace_gen[rank][grp][(tl) - 8][(kb)][(ev)] = clock64(); } while (0)
 #else
 #define TR(tl, ev) do { } while (0)
+#define TRG(tl, kb, ev) do { } while (0)
 #endif
 
 constexpr int kThreads = 640;
-constexpr int kSG = 4;                       // generator ring stages
-constexpr int kSW = 4;                       // weight ring stages
-constexpr int kSH = 2;                       // layer-3 A chunk ring
+constexpr int kSG = 6;                       // generator ring stages
+constexpr int kSW = 5;                       // weight ring stages
+constexpr int kLead = 4;                     // layer-1 stages the issuer may run ahead of the tensor pipe
+constexpr uint32_t kBiasTile = 4096;         // 128 rows x K 16 (fp16), no-swizzle layout
 constexpr uint32_t kTile = 16384;            // 128 rows x 128 B
 constexpr int kN1 = 256, kN2 = 256, kN3P = 16;
 constexpr int kNkb2 = kN1 / 64;              // W2 K blocks (64 fp16 per 128-B row)
@@ -73,8 +81,8 @@ __host__ __device__ inline Layout layout_of(int n0) {
   L.stream = 0;
   L.w3 = L.stream + (size_t)2 * L.nst * kTile;
   L.ones = L.w3 + (size_t)2 * kChunks * kW3Chunk;
-  L.bias2 = L.ones + kTile;
-  L.total = L.bias2 + 2 * (size_t)kTile;
+  L.bias2 = L.ones + kBiasTile;
+  L.total = L.bias2 + 2 * (size_t)kBiasTile;
   return L;
 }
 
@@ -97,13 +105,14 @@ struct Args {
   int64_t eval_n;
   int eval_base;
   float* eval_out;
+  uint32_t stepS2, org2;                     // bf16x2 lattice constants: step * 2^130, origin
 };
 
 struct alignas(16) Smem {
   uint64_t g_full[kSG], g_empty[kSG], w_full[kSW], w_empty[kSW];
   uint64_t acc1_full, acc2_full, acc3_full, acc2_free;
   uint64_t h1_kb[kNkb2];
-  uint64_t h2_full[kSH], h2_empty[kSH];
+  uint64_t h2_kb[kNkb2];
   uint64_t info_full[2];
   uint32_t tbase;
   int base_g, base_e1, base_e2;
@@ -121,11 +130,11 @@ struct alignas(16) Smem {
   // E1 -> E2, per tile parity and row: bit 0 cond1, bit 1 (nsc1 == 1), bit 2 amb1, bits 8.. i*
   int info[2][128];
   uint32_t sc2[8][128];                      // E2: sign-change words of layer 2
-  uint32_t vc2[8][128];                      // E2 slow path: value-change words of layer 2
+  uint16_t vc2[16][128];                     // E2 slow path: value-change bits of layer 2 (16 neurons)
   alignas(16) uint16_t xg[kMaxN0 + 64];     // base image (bf16) for the generator, zero padded
 };
 
-constexpr size_t kTilesBytes = (size_t)(kSG + kSW + kSH + 2) * kTile + (size_t)kChunks * kW3Chunk;
+constexpr size_t kTilesBytes = (size_t)(kSG + kSW) * kTile + (size_t)kChunks * kW3Chunk + 4 * kBiasTile;
 constexpr size_t kSmemBytes = 1024 + kTilesBytes + sizeof(Smem);
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
@@ -185,26 +194,25 @@ __device__ __forceinline__ uint32_t hmin2(uint32_t a, uint32_t b) {
   asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
-__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
 
-// 4 lattice pixel pairs from one Philox word (nibble n -> pixel n), x2[k] = base pixels (bf16x2).
-// x' = min(relu(RNE(x + RNE(l*step + origin))), 1)  (reading C14)
-__device__ __forceinline__ uint4 lattice_word(uint32_t w, uint4 x2, uint32_t step2, uint32_t org2) {
-  const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
-  const uint32_t one2 = 0x3F803F80u, c128 = 0x43004300u;
+// 4 lattice pixel pairs from one Philox word (nibble n -> pixel n, LSB first), x2[k] = base pixels
+// (bf16x2).  x' = min(relu(RNE(x + RNE(l*step + origin))), 1)  (reading C14).  The level pair is
+// built by one PRMT as the bf16 subnormals (l_a * 2^-130, l_b * 2^-130) -- nibble at bits 3..6 of
+// each byte, the other byte zero by PRMT's sign replication -- so one FMA with stepS = step * 2^130
+// gives l*step + origin exactly before its single rounding.
+__device__ __forceinline__ uint4 lattice_word(uint32_t w, uint4 x2, uint32_t stepS2, uint32_t org2) {
+  const uint32_t lo = (w << 3) & 0x78787878u;             // nibbles 0,2,4,6 -> bits 3..6 of bytes 0..3
+  const uint32_t hi = (w >> 1) & 0x78787878u;             // nibbles 1,3,5,7
+  const uint32_t one2 = 0x3F803F80u;
   uint32_t o[4];
   const uint32_t xs[4] = {x2.x, x2.y, x2.z, x2.w};
 #pragma unroll
   for (int k = 0; k < 4; k++) {
-    // bytes [lo_k, -, hi_k, -] -> bf16x2 (128 + la, 128 + lb): one PRMT + one LOP3
-    const uint32_t sel = (uint32_t)k * 0x11u + (4u + (uint32_t)k) * 0x1100u;
-    const uint32_t pair = (__byte_perm(lo, hi, sel) & 0x00FF00FFu) | c128;
-    const uint32_t l = hsub2(pair, c128);                 // exact: (la, lb)
-    const uint32_t off = hfma2(l, step2, org2);           // RNE(l*step + origin)
+    const uint32_t sel = (uint32_t)k | ((8u + k) << 4) | ((4u + k) << 8) | ((12u + k) << 12);
+    uint32_t l;                                           // bf16x2 subnormals (l_a, l_b) * 2^-130
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(l) : "r"(lo), "r"(hi), "r"(sel));   // (__byte_perm drops the
+                                                                              //  sign-replicate bit)
+    const uint32_t off = hfma2(l, stepS2, org2);          // RNE(l*step + origin)
     o[k] = hmin2(hfma2_relu(xs[k], one2, off), one2);     // min(relu(RNE(x + off)), 1)
   }
   return make_uint4(o[0], o[1], o[2], o[3]);
@@ -221,6 +229,13 @@ __device__ __forceinline__ void split_pair(float u0, float u1, uint32_t& hi2, ui
   asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(lo2) : "f"(d1), "f"(d0));
 }
 
+// sign bits of 32 potentials -> one word (bit i = neuron i): one funnel shift per neuron
+__device__ __forceinline__ uint32_t sign_word(const uint32_t (&v)[32]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 31; i >= 0; i--) m = __funnelshift_l(v[i], m, 1);
+  return m;
+}
 // sign bits of 16 potentials shifted into m from the top (bit i of the final word = neuron i when
 // the upper half is folded first): one funnel shift per neuron
 __device__ __forceinline__ uint32_t sign_fold(const uint32_t (&v)[16], uint32_t m) {
@@ -240,11 +255,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sG = base;                                    // [kSG][16 KB] generated A tiles
   uint8_t* sW = sG + kSG * kTile;                        // [kSW][16 KB] W1 / W2 half tiles
-  uint8_t* sH2 = sW + kSW * kTile;                       // [kSH][16 KB] layer-3 A chunks
-  uint8_t* sOnes = sH2 + kSH * kTile;                    // [16 KB] ones column (bias MMA A)
-  uint8_t* sB2 = sOnes + kTile;                          // [16 KB] [b2_hi | b2_lo] half (bias MMA B)
-  uint8_t* sW3 = sB2 + kTile;                            // [kChunks][1 KB] W3 half (resident)
-  Smem& S = *reinterpret_cast<Smem*>(sW3 + kChunks * kW3Chunk);
+  uint8_t* sW3 = sW + kSW * kTile;                       // [kChunks][1 KB] W3 half (resident)
+  uint8_t* sOnes = sW3 + kChunks * kW3Chunk;             // [4 KB] ones column (bias MMA A)
+  uint8_t* sB2 = sOnes + kBiasTile;                      // [4 KB] [b2_hi | b2_lo] half (bias MMA B)
+  uint8_t* sT = sB2 + kBiasTile;                         // [2][4 KB] h2 hi / lo of neurons 240-255
+  Smem& S = *reinterpret_cast<Smem*>(sT + 2 * kBiasTile);
 
   const uint32_t rank = cluster_ctarank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -254,12 +269,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 
   if (threadIdx.x == 0) {
     const uint32_t two = rank == 0 ? 2u : 1u;
-    for (int i = 0; i < kSG; i++) { mbar_init(&S.g_full[i], 16); mbar_init(&S.g_empty[i], 1); }
+    for (int i = 0; i < kSG; i++) { mbar_init(&S.g_full[i], 8); mbar_init(&S.g_empty[i], 1); }
     for (int i = 0; i < kSW; i++) { mbar_init(&S.w_full[i], two); mbar_init(&S.w_empty[i], 1); }
     mbar_init(&S.acc1_full, 1); mbar_init(&S.acc2_full, 1); mbar_init(&S.acc3_full, 1);
     mbar_init(&S.acc2_free, 8);
     for (int i = 0; i < kNkb2; i++) mbar_init(&S.h1_kb[i], 8);
-    for (int i = 0; i < kSH; i++) { mbar_init(&S.h2_full[i], 8); mbar_init(&S.h2_empty[i], 1); }
+    for (int i = 0; i < kNkb2; i++) mbar_init(&S.h2_kb[i], 8);
     for (int i = 0; i < 2; i++) mbar_init(&S.info_full[i], 4);
     S.base_g = S.base_e1 = S.base_e2 = -1;
     fence_mbar_init();
@@ -271,17 +286,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     uint4* d3 = reinterpret_cast<uint4*>(sW3);
     for (int i = threadIdx.x; i < (int)(kChunks * kW3Chunk / 16); i += kThreads) d3[i] = s3[i];
     const uint4* so = reinterpret_cast<const uint4*>(a.wblk + a.lay.ones);
-    const uint4* sb = reinterpret_cast<const uint4*>(a.wblk + a.lay.bias2 + (size_t)rank * kTile);
+    const uint4* sb = reinterpret_cast<const uint4*>(a.wblk + a.lay.bias2 + (size_t)rank * kBiasTile);
     uint4* dO = reinterpret_cast<uint4*>(sOnes);
     uint4* dB = reinterpret_cast<uint4*>(sB2);
-    for (int i = threadIdx.x; i < (int)(kTile / 16); i += kThreads) { dO[i] = so[i]; dB[i] = sb[i]; }
+    for (int i = threadIdx.x; i < (int)(kBiasTile / 16); i += kThreads) { dO[i] = so[i]; dB[i] = sb[i]; }
   }
   fence_proxy_async();
   fence_before();
   cluster_sync();
   fence_after();
   const uint32_t tb = S.tbase;
-  const uint32_t R1 = tb, R2 = tb + 256u;
+  const uint32_t R1 = tb, R2 = tb + 256u, R3 = tb + 496u;
   const int nst = a.lay.nst;
 
   if (warp == 0) {
@@ -292,7 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       for (uint64_t t = t_begin; t < t_end; t++)
         for (int s = 0; s < nst; s++) {
           const uint32_t st = ws % kSW, ph = (ws / kSW) & 1u;
-          mbar_wait(&S.w_empty[st], ph ^ 1u);
+          mbar_wait_sleep(&S.w_empty[st], ph ^ 1u, 32);
           mbar_expect_tx(&S.w_full[st], kTile);
           bulk_g2s(sW + st * kTile, src0 + (size_t)s * kTile, kTile, &S.w_full[st]);
           ws++;
@@ -319,8 +334,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         // layer 1 into R1 (issued after the previous tile's layer 2, which read R1: in-order pipe)
         for (int kb = 0; kb < a.nkb1; kb++) {
           const uint32_t g = gs % kSG, w = ws % kSW;
+          if (gs >= (uint32_t)kLead) {                    // keep the tensor-pipe queue short so the
+            const uint32_t o = gs - kLead;                // layer-3 MMAs of the previous tile get in
+            mbar_wait(&S.g_empty[o % kSG], (o / kSG) & 1u);
+          }
           mbar_wait(&S.g_full[g], (gs / kSG) & 1u);
-          if (kb < 13) TR(tl, 16 + kb);
+          if (kb < 10) TR(tl, 16 + kb);
           mbar_wait(&S.w_full[w], (ws / kSW) & 1u);
           fence_after();
           const uint32_t ab = smem_u32(sG + g * kTile), bb = smem_u32(sW + w * kTile);
@@ -338,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         mbar_wait(&S.acc2_free, (tl & 1u) ^ 1u);
         TR(tl, 4);
         fence_after();
-        mma2_f16_ss(R2, sdesc_sw128(smem_u32(sOnes)), sdesc_sw128(smem_u32(sB2)), id2, 0u);
+        mma2_f16_ss(R2, sdesc_none(smem_u32(sOnes), 128, 256), sdesc_none(smem_u32(sB2), 128, 256), id2, 0u);
         for (int kb = 0; kb < kNkb2; kb++) {
           const uint32_t w = ws % kSW;
           mbar_wait(&S.h1_kb[kb], tl & 1u);
@@ -363,20 +382,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   } else if (warp == 2) {
     if (lane == 0 && rank == 0) {
       // ---------------------------------------------------------------- layer-3 issuer (leader)
-      uint32_t hs = 0, tl = 0;
+      // D = R3 (16 cols) <- sum over neuron groups g of [hi_g | lo_g] x W3[:, 16g..16g+16]: A from the
+      // in-place H2 in TMEM (groups 0-14) or the shared-memory tail tiles (group 15).
+      uint32_t tl = 0;
       const uint32_t id3 = idesc_f16(256, kN3P, 0, 0);
       for (uint64_t t = t_begin; t < t_end; t++, tl++) {
-        for (int p = 0; p < kChunks; p++) {
-          const uint32_t slot = hs % kSH;
-          mbar_wait(&S.h2_full[slot], (hs / kSH) & 1u);
-          if (p == 0) TR(tl, 14);
+        for (int kb = 0; kb < kNkb2; kb++) {
+          mbar_wait(&S.h2_kb[kb], tl & 1u);
+          if (kb == 0) TR(tl, 14);
           fence_after();
-          const uint32_t ab = smem_u32(sH2 + slot * kTile), bb = smem_u32(sW3 + p * kW3Chunk);
 #pragma unroll
-          for (int kk = 0; kk < 4; kk++)
-            mma2_f16_ss(R2, sdesc_sw128(ab + 32u * kk), sdesc_sw128(bb + 32u * kk), id3, (p | kk) ? 1u : 0u);
-          mma2_commit(&S.h2_empty[slot], 0x3);
-          hs++;
+          for (int kk = 0; kk < 4; kk++) {
+            const int g = 4 * kb + kk;
+            const uint64_t bd = sdesc_sw128(smem_u32(sW3 + (g >> 1) * kW3Chunk) + 32u * (g & 1));
+            if (g < 15) {
+              mma2_f16_ts(R3, R2 + 16u * g, bd, id3, g ? 1u : 0u);
+              mma2_f16_ts(R3, R2 + 16u * g + 8u, bd, id3, 1u);
+            } else {
+              mma2_f16_ss(R3, sdesc_none(smem_u32(sT), 128, 256), bd, id3, 1u);
+              mma2_f16_ss(R3, sdesc_none(smem_u32(sT + kBiasTile), 128, 256), bd, id3, 1u);
+            }
+          }
         }
         mma2_commit(&S.acc3_full, 0x3);
         TR(tl, 15);
@@ -384,14 +410,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
   } else if (warp >= kWGen && warp < kWE1) {
     // ------------------------------------------------------------------ generator (both CTAs)
-    const int gw = warp - kWGen, h = gw >> 2;
+    // Two groups of four warps take alternate ring stages; a warp generates a whole 64-pixel K block
+    // of its 32 rows (two Philox calls) into registers before it waits for the slot.
+    const int gw = warp - kWGen, grp = gw >> 2;
     const int r = 32 * (gw & 3) + lane;                    // row of this CTA's A tile
     const int gt = threadIdx.x - 32 * kWGen;               // 0..255
     uint32_t gs = 0, tl = 0;
     const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
-    const __nv_bfloat162 st2 = __floats2bfloat162_rn(a.pert.step_f, a.pert.step_f);
-    const __nv_bfloat162 or2 = __floats2bfloat162_rn(a.pert.origin_f, a.pert.origin_f);
-    const uint32_t step2 = *reinterpret_cast<const uint32_t*>(&st2), org2 = *reinterpret_cast<const uint32_t*>(&or2);
+    const uint32_t stepS2 = a.stepS2, org2 = a.org2;
     const int n0 = a.n0;
     const int kneed = 16 * a.nk16;                         // K elements the MMA reads
     for (uint64_t t = t_begin; t < t_end; t++, tl++) {
@@ -408,44 +434,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       if (a.eval_idx) c = grow < ti.nvalid ? a.eval_idx[ti.start + grow] : 0;
       else c = ti.start + (uint64_t)grow;
       const uint32_t c0 = (uint32_t)c, c1 = (uint32_t)(c >> 32), cb = (uint32_t)ti.b;
-      for (int kb = 0; kb < a.nkb1; kb++) {
-        const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
-        mbar_wait(&S.g_empty[st], ph ^ 1u);
-        uint8_t* slot = sG + st * kTile;
-        const int j = 2 * kb + h;                          // 32-pixel Philox block
-        const int e0 = 32 * j;                             // first K element of this half
-        if (e0 + 32 <= n0) {
-          const uint4 w = philox(c0, c1, cb, (uint32_t)j, k0, k1);
+      for (int kb = 0; kb < a.nkb1; kb++, gs++) {
+        if ((gs & 1u) != (uint32_t)grp) continue;
+        TRG(tl, kb, 0);
+        uint4 out[8];
+        const int e0 = 64 * kb;
+        if (e0 + 64 <= n0) {
+          const uint4 w0 = philox(c0, c1, cb, (uint32_t)(2 * kb), k0, k1);
+          const uint4 w1 = philox(c0, c1, cb, (uint32_t)(2 * kb + 1), k0, k1);
           const uint4* xv = reinterpret_cast<const uint4*>(S.xg + e0);
-          const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
+          out[0] = lattice_word(w0.x, xv[0], stepS2, org2);
+          out[1] = lattice_word(w0.y, xv[1], stepS2, org2);
+          out[2] = lattice_word(w0.z, xv[2], stepS2, org2);
+          out[3] = lattice_word(w0.w, xv[3], stepS2, org2);
+          out[4] = lattice_word(w1.x, xv[4], stepS2, org2);
+          out[5] = lattice_word(w1.y, xv[5], stepS2, org2);
+          out[6] = lattice_word(w1.z, xv[6], stepS2, org2);
+          out[7] = lattice_word(w1.w, xv[7], stepS2, org2);
+        } else {
+          // tail block: remaining pixels, then the bias columns (1.0) at K = n0 .. n0+2, then zeros
 #pragma unroll
-          for (int ww = 0; ww < 4; ww++)
-            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (4 * h + ww))) = lattice_word(wsr[ww], xv[ww], step2, org2);
-        } else if (e0 < kneed) {
-          // tail: remaining pixels, then the bias columns (1.0) at K = n0 .. n0+2, then zeros
-          uint4 w = make_uint4(0, 0, 0, 0);
-          if (e0 < n0) w = philox(c0, c1, cb, (uint32_t)j, k0, k1);
-          const uint4* xv = reinterpret_cast<const uint4*>(S.xg + e0);
-          const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
+          for (int hh = 0; hh < 2; hh++) {
+            const int eh = e0 + 32 * hh;
+            uint4 w = make_uint4(0, 0, 0, 0);
+            if (eh < n0) w = philox(c0, c1, cb, (uint32_t)(2 * kb + hh), k0, k1);
+            const uint4* xv = reinterpret_cast<const uint4*>(S.xg + eh);
+            const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-          for (int ww = 0; ww < 4; ww++) {
-            const uint4 y = lattice_word(wsr[ww], xv[ww], step2, org2);
-            uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+            for (int ww = 0; ww < 4; ww++) {
+              const uint4 y = lattice_word(wsr[ww], xv[ww], stepS2, org2);
+              uint32_t ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-              const int e = e0 + 8 * ww + 2 * k;          // K index of the low element
-              uint32_t lo = ys[k] & 0xFFFFu, hi = ys[k] >> 16;
-              if (e >= n0) lo = (e < n0 + 3) ? 0x3F80u : 0u;
-              if (e + 1 >= n0) hi = (e + 1 < n0 + 3) ? 0x3F80u : 0u;
-              ys[k] = lo | (hi << 16);
+              for (int k = 0; k < 4; k++) {
+                const int e = eh + 8 * ww + 2 * k;        // K index of the low element
+                uint32_t lo = ys[k] & 0xFFFFu, hi = ys[k] >> 16;
+                if (e >= n0) lo = (e < n0 + 3) ? 0x3F80u : 0u;
+                if (e + 1 >= n0) hi = (e + 1 < n0 + 3) ? 0x3F80u : 0u;
+                ys[k] = lo | (hi << 16);
+              }
+              out[4 * hh + ww] = make_uint4(ys[0], ys[1], ys[2], ys[3]);
             }
-            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (4 * h + ww))) = make_uint4(ys[0], ys[1], ys[2], ys[3]);
           }
         }
+        const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
+        TRG(tl, kb, 1);
+        mbar_wait_sleep(&S.g_empty[st], ph ^ 1u, 32);
+        TRG(tl, kb, 2);
+        uint8_t* slot = sG + st * kTile;
+#pragma unroll
+        for (int ch = 0; ch < 8; ch++)
+          if (kneed > e0 + 8 * ch)                           // only the K steps the MMA reads
+            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = out[ch];
         fence_proxy_async();
         __syncwarp();
+        TRG(tl, kb, 3);
         if (lane == 0) arrive_leader(&S.g_full[st], rank);
-        gs++;
+        TRG(tl, kb, 4);
       }
       if (gt == 0) TR(tl, 7);
     }
@@ -481,63 +525,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         named_bar(2, 128);
         if (et == 0) S.base_e1 = ti.b;
       }
-      mbar_wait(&S.acc1_full, tl & 1u);
+      mbar_wait_sleep(&S.acc1_full, tl & 1u, 64);
       if (et == 0) TR(tl, 8);
       fence_after();
-      // pass A: sign-change count and the first changed neuron i*
+      // pass A: sign-change count and the first changed neuron i* (two 32-column loads per wait)
       int nsc = 0, istar = -1;
 #pragma unroll 1
-      for (int p = 0; p < 8; p++) {
-        uint32_t m = 0;
+      for (int p = 0; p < 8; p += 2) {
+        uint32_t va[32], vb[32];
+        tmem_ld32(R1 + loff + 32u * p, va);
+        tmem_ld32(R1 + loff + 32u * p + 32u, vb);
+        tmem_ld_wait();
+        const uint32_t sa = sign_word(va) ^ S.nb1[p], sb = sign_word(vb) ^ S.nb1[p + 1];
+        nsc += __popc(sa) + __popc(sb);
+        if (istar < 0 && sa) istar = 32 * p + __ffs(sa) - 1;
+        if (istar < 0 && sb) istar = 32 * p + 32 + __ffs(sb) - 1;
+        if (eval && valid) {
 #pragma unroll
-        for (int hf = 1; hf >= 0; hf--) {
-          uint32_t v[16];
-          tmem_ld16(R1 + loff + 32u * p + 16u * hf, v);
-          tmem_ld_wait();
-          m = sign_fold(v, m);
-          if (eval && valid) {
-#pragma unroll
-            for (int i = 0; i < 16; i++) a.eval_out[cidx * a.T + 32 * p + 16 * hf + i] = __uint_as_float(v[i]);
+          for (int i = 0; i < 32; i++) {
+            a.eval_out[cidx * a.T + 32 * p + i] = __uint_as_float(va[i]);
+            a.eval_out[cidx * a.T + 32 * p + 32 + i] = __uint_as_float(vb[i]);
           }
         }
-        const uint32_t scw = m ^ S.nb1[p];
-        nsc += __popc(scw);
-        if (istar < 0 && scw) istar = 32 * p + __ffs(scw) - 1;
       }
-      // pass B: predicates on the slow path, H1 = fp16 hi | lo in place, handed over per K block
+      // pass B: predicates on the slow path, H1 = fp16 hi | lo in place (16-column groups), handed
+      // over per K block; the next group's load is in flight while this one is processed
       const bool slow = __any_sync(0xffffffffu, need12 && valid && nsc <= 1);
       float linf = 0.f, minab = 3.0e38f;
-#pragma unroll 1
-      for (int p = 0; p < 8; p++) {
+      uint32_t vbuf[2][16];
+      tmem_ld16(R1 + loff, vbuf[0]);
+      tmem_ld_wait();
+#pragma unroll 2
+      for (int g = 0; g < 16; g++) {
+        uint32_t (&v)[16] = vbuf[g & 1];
+        if (g < 15) tmem_ld16(R1 + loff + 16u * (g + 1), vbuf[(g + 1) & 1]);
+        if (slow) {
+          const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 16 * g);
 #pragma unroll
-        for (int hf = 0; hf < 2; hf++) {                   // 16 neurons at a time (register budget)
-          uint32_t v[16];
-          tmem_ld16(R1 + loff + 32u * p + 16u * hf, v);
-          tmem_ld_wait();
-          if (slow) {
-            const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 32 * p + 16 * hf);
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-              const float4 b4 = ub[k];
-              const float u0 = __uint_as_float(v[4 * k]), u1 = __uint_as_float(v[4 * k + 1]);
-              const float u2 = __uint_as_float(v[4 * k + 2]), u3 = __uint_as_float(v[4 * k + 3]);
-              linf = fmaxf(linf, fmaxf(fmaxf(fabsf(u0 - b4.x), fabsf(u1 - b4.y)), fmaxf(fabsf(u2 - b4.z), fabsf(u3 - b4.w))));
-              minab = fminf(minab, fminf(fminf(fabsf(u0), fabsf(u1)), fminf(fabsf(u2), fabsf(u3))));
-            }
+          for (int k = 0; k < 4; k++) {
+            const float4 b4 = ub[k];
+            const float u0 = __uint_as_float(v[4 * k]), u1 = __uint_as_float(v[4 * k + 1]);
+            const float u2 = __uint_as_float(v[4 * k + 2]), u3 = __uint_as_float(v[4 * k + 3]);
+            linf = fmaxf(linf, fmaxf(fmaxf(fabsf(u0 - b4.x), fabsf(u1 - b4.y)), fmaxf(fabsf(u2 - b4.z), fabsf(u3 - b4.w))));
+            minab = fminf(minab, fminf(fminf(fabsf(u0), fabsf(u1)), fminf(fabsf(u2), fabsf(u3))));
           }
-          uint32_t hi[8], lo[8];
-#pragma unroll
-          for (int k = 0; k < 8; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hi[k], lo[k]);
-          // in place: the 16 fp32 columns of these neurons become [hi (8 cols) | lo (8 cols)]
-          tmem_st8(R1 + loff + 32u * p + 16u * hf, hi);
-          tmem_st8(R1 + loff + 32u * p + 16u * hf + 8u, lo);
         }
-        if (p & 1) {
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hi[k], lo[k]);
+        // in place: the 16 fp32 columns of these neurons become [hi (8 cols) | lo (8 cols)]
+        tmem_st8(R1 + loff + 16u * g, hi);
+        tmem_st8(R1 + loff + 16u * g + 8u, lo);
+        if ((g & 3) == 3) {
           tmem_st_wait();
           fence_before();
           __syncwarp();
-          if (lane == 0) arrive_leader(&S.h1_kb[p >> 1], rank);
+          if (lane == 0) arrive_leader(&S.h1_kb[g >> 2], rank);
         }
+        tmem_ld_wait();
       }
       if (et == 0) TR(tl, 9);
       // summary for E2 (pair (1, 2) is decided by layer 1 alone)
@@ -558,7 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const float tau2 = a.cov.tau_dev ? a.cov.tau_dev[2] : a.cov.tau[2];
     const bool eval = a.eval_idx != nullptr;
     const bool need23 = a.pair23 >= 0 && !eval;
-    uint32_t tl = 0, hs = 0;
+    uint32_t tl = 0;
     for (uint64_t t = t_begin; t < t_end; t++, tl++) {
       const TileInfo ti = tile_info(a, t);
       const int grow = 128 * (int)rank + r;
@@ -594,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         named_bar(3, 128);
         if (et == 0) S.base_e2 = ti.b;
       }
-      mbar_wait(&S.acc2_full, tl & 1u);
+      mbar_wait_sleep(&S.acc2_full, tl & 1u, 64);
       if (et == 0) TR(tl, 10);
       fence_after();
       mbar_wait(&S.info_full[tl & 1], (tl >> 1) & 1u);
@@ -604,70 +649,78 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       // pass A: sign-change words of layer 2 (kept in shared memory, row-private)
       int nsc = 0, istar2 = -1;
 #pragma unroll 1
-      for (int p = 0; p < 8; p++) {
-        uint32_t m = 0;
+      for (int p = 0; p < 8; p += 2) {
+        uint32_t va[32], vb[32];
+        tmem_ld32(R2 + loff + 32u * p, va);
+        tmem_ld32(R2 + loff + 32u * p + 32u, vb);
+        tmem_ld_wait();
+        const uint32_t sa = sign_word(va) ^ S.nb2[p], sb = sign_word(vb) ^ S.nb2[p + 1];
+        S.sc2[p][r] = sa;
+        S.sc2[p + 1][r] = sb;
+        nsc += __popc(sa) + __popc(sb);
+        if (istar2 < 0 && sa) istar2 = 32 * p + __ffs(sa) - 1;
+        if (istar2 < 0 && sb) istar2 = 32 * p + 32 + __ffs(sb) - 1;
+        if (eval && valid) {
 #pragma unroll
-        for (int hf = 1; hf >= 0; hf--) {
-          uint32_t v[16];
-          tmem_ld16(R2 + loff + 32u * p + 16u * hf, v);
-          tmem_ld_wait();
-          m = sign_fold(v, m);
-          if (eval && valid) {
-#pragma unroll
-            for (int i = 0; i < 16; i++) a.eval_out[cidx * a.T + kN1 + 32 * p + 16 * hf + i] = __uint_as_float(v[i]);
+          for (int i = 0; i < 32; i++) {
+            a.eval_out[cidx * a.T + kN1 + 32 * p + i] = __uint_as_float(va[i]);
+            a.eval_out[cidx * a.T + kN1 + 32 * p + 32 + i] = __uint_as_float(vb[i]);
           }
         }
-        const uint32_t scw = m ^ S.nb2[p];
-        S.sc2[p][r] = scw;
-        nsc += __popc(scw);
-        if (istar2 < 0 && scw) istar2 = 32 * p + __ffs(scw) - 1;
       }
-      // pass B: H2 chunks for layer 3; slow path: value changes / L-inf / min|u| of layer 2
+      // pass B: H2 = fp16 hi | lo in place for groups 0-14, group 15 (processed first: its columns
+      // become the layer-3 accumulator) into the shared-memory tail tiles; slow path: value changes,
+      // L-inf and min|u| of layer 2
       const bool slow = __any_sync(0xffffffffu, cond1 || (need23 && valid && nsc <= 1));
       float linf = 0.f, minab = 3.0e38f, vcamb = 3.0e38f;
-#pragma unroll 1
-      for (int p = 0; p < 8; p++) {
-        const uint32_t slot = hs % kSH;
-        mbar_wait(&S.h2_empty[slot], ((hs / kSH) & 1u) ^ 1u);
-        uint8_t* dst = sH2 + slot * kTile;
-        uint32_t vw = 0;
+      uint32_t vbuf[2][16];
+      tmem_ld16(R2 + loff + 240u, vbuf[0]);
+      tmem_ld_wait();
+#pragma unroll 2
+      for (int i = 0; i < 16; i++) {
+        const int g = i == 0 ? 15 : i - 1;
+        uint32_t (&v)[16] = vbuf[i & 1];
+        if (i < 15) tmem_ld16(R2 + loff + 16u * i, vbuf[(i + 1) & 1]);     // group i (= next item)
+        if (slow) {
+          const float4* ub = reinterpret_cast<const float4*>(S.ub2 + 16 * g);
+          uint32_t vw = 0;
 #pragma unroll
-        for (int hf = 0; hf < 2; hf++) {                   // 16 neurons at a time (register budget)
-          uint32_t v[16];
-          tmem_ld16(R2 + loff + 32u * p + 16u * hf, v);
-          tmem_ld_wait();
-          if (slow) {
-            const float4* ub = reinterpret_cast<const float4*>(S.ub2 + 32 * p + 16 * hf);
+          for (int k = 0; k < 4; k++) {
+            const float4 b4 = ub[k];
+            const float uu[4] = {__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]),
+                                 __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])};
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-              const float4 b4 = ub[k];
-              const float uu[4] = {__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]),
-                                   __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])};
-              const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-              for (int i = 0; i < 4; i++) {
-                const float d = fabsf(uu[i] - bb[i]);
-                linf = fmaxf(linf, d);
-                minab = fminf(minab, fabsf(uu[i]));
-                vcamb = fminf(vcamb, fabsf(d - tg2));
-                vw |= (d >= tg2 ? 1u : 0u) << (16 * hf + 4 * k + i);
-              }
+            for (int j = 0; j < 4; j++) {
+              const float d = fabsf(uu[j] - bb[j]);
+              linf = fmaxf(linf, d);
+              minab = fminf(minab, fabsf(uu[j]));
+              vcamb = fminf(vcamb, fabsf(d - tg2));
+              vw |= (d >= tg2 ? 1u : 0u) << (4 * k + j);
             }
           }
-          uint32_t hi[8], lo[8];
-#pragma unroll
-          for (int k = 0; k < 8; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hi[k], lo[k]);
-#pragma unroll
-          for (int m = 0; m < 2; m++) {
-            *reinterpret_cast<uint4*>(dst + sw128_off(r, 32 * hf + 16 * m)) = make_uint4(hi[4 * m], hi[4 * m + 1], hi[4 * m + 2], hi[4 * m + 3]);
-            *reinterpret_cast<uint4*>(dst + sw128_off(r, 64 + 32 * hf + 16 * m)) = make_uint4(lo[4 * m], lo[4 * m + 1], lo[4 * m + 2], lo[4 * m + 3]);
-          }
+          S.vc2[g][r] = (uint16_t)vw;
         }
-        if (slow) S.vc2[p][r] = vw & ~S.sc2[p][r];
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) arrive_leader(&S.h2_full[slot], rank);
-        hs++;
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hi[k], lo[k]);
+        if (g < 15) {
+          tmem_st8(R2 + loff + 16u * g, hi);
+          tmem_st8(R2 + loff + 16u * g + 8u, lo);
+        } else {
+          *reinterpret_cast<uint4*>(sT + none16_off(r, 0)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(sT + none16_off(r, 8)) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+          *reinterpret_cast<uint4*>(sT + kBiasTile + none16_off(r, 0)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          *reinterpret_cast<uint4*>(sT + kBiasTile + none16_off(r, 8)) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+          fence_proxy_async();
+        }
+        if (g == 3 || g == 7 || g == 11 || g == 14) {
+          tmem_st_wait();
+          fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_leader(&S.h2_kb[g >> 2], rank);
+        }
+        tmem_ld_wait();
       }
       if (et == 0) TR(tl, 11);
       minab = fminf(minab, S.minub2);
@@ -682,18 +735,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           else { is = off[2] + p; iv = off[3] + p; }
           const uint32_t scw = S.sc2[p][r];
           if (scw) { atomicOr(&a.res.cov_all[is], scw); if (certain) atomicOr(&a.res.cov_certain[is], scw); }
-          const uint32_t vcw = S.vc2[p][r];
+          const uint32_t vcw = ((uint32_t)S.vc2[2 * p][r] | ((uint32_t)S.vc2[2 * p + 1][r] << 16)) & ~scw;
           if (vcw) { atomicOr(&a.res.cov_all[iv], vcw); if (certain) atomicOr(&a.res.cov_certain[iv], vcw); }
         }
       }
       const bool cond2 = need23 && valid && ((nsc == 1) || (nsc == 0 && linf >= th2));
       const bool amb2 = minab < tau1 || (nsc == 0 && fabsf(linf - th2) < tau1);
       // ============================ E3: logits -> pair (2, 3), argmax, property, counts
-      mbar_wait(&S.acc3_full, tl & 1u);
+      mbar_wait_sleep(&S.acc3_full, tl & 1u, 64);
       if (et == 0) TR(tl, 12);
       fence_after();
       uint32_t v[16];
-      tmem_ld16(R2 + loff, v);
+      tmem_ld16(R3 + loff, v);
       tmem_ld_wait();
       fence_before();
       __syncwarp();
@@ -703,8 +756,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 #pragma unroll
       for (int i = 0; i < 16; i++) y[i] = __uint_as_float(v[i]) + S.b3[i];
       if (eval) {
-        if (valid)
-          for (int i = 0; i < n3; i++) a.eval_out[cidx * a.T + kN1 + kN2 + i] = y[i];
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 16; i++) if (i < n3) a.eval_out[cidx * a.T + kN1 + kN2 + i] = y[i];
+        }
       } else {
         const int bcls = S.bcls;
         if (cond2) {
@@ -785,12 +840,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 extern "C" int mlpv_f3_trace_read(void* host) {
   return (int)cudaMemcpyFromSymbol(host, f3::g_trace, sizeof f3::g_trace);
 }
+extern "C" int mlpv_f3_trace_gen_read(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, f3::g_trace_gen, sizeof f3::g_trace_gen);
+}
 #endif
 
 // ------------------------------------------------------------------------------------------- host
 bool fused3_applicable(const DevNet& net) {
   return net.numeric == MLPV_NUM_BF16 && net.L == 3 && net.sizes[1] == f3::kN1 && net.sizes[2] == f3::kN2 &&
          net.sizes[3] <= f3::kN3P && net.sizes[0] % 2 == 0 && net.sizes[0] + 3 <= f3::kMaxN0;
+}
+
+static uint16_t f2bf(float f);
+// the lattice trick needs step * 2^130 as a normal bf16: |step| normal with exponent field <= 124
+bool fused3_pert_ok(const DevPert& pert) {
+  const uint32_t e = (f2bf(pert.step_f) >> 7) & 0xFFu;
+  return e >= 1 && e <= 124;
 }
 
 static size_t sw128_h(uint32_t row, uint32_t byte) {
@@ -864,9 +929,9 @@ cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const v
       const float b = b2[n];
       const uint16_t bh = f2h(b);
       const uint16_t bl = f2h(b - h2f(bh));
-      uint8_t* bt = blk.data() + L.bias2 + (size_t)rk * f3::kTile;
-      put16(bt, rr, 0, bh);
-      put16(bt, rr, 1, bl);
+      uint8_t* bt = blk.data() + L.bias2 + (size_t)rk * f3::kBiasTile;
+      memcpy(bt + tc::none16_off((uint32_t)rr, 0), &bh, 2);
+      memcpy(bt + tc::none16_off((uint32_t)rr, 1), &bl, 2);
     }
     for (int rr = 0; rr < 8; rr++) {
       const int n = 8 * rk + rr;
@@ -883,8 +948,9 @@ cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const v
     }
   }
   for (int rr = 0; rr < 128; rr++) {
-    put16(blk.data() + L.ones, rr, 0, 0x3C00u);          // fp16 1.0
-    put16(blk.data() + L.ones, rr, 1, 0x3C00u);
+    const uint16_t one = 0x3C00u;                         // fp16 1.0
+    memcpy(blk.data() + L.ones + tc::none16_off((uint32_t)rr, 0), &one, 2);
+    memcpy(blk.data() + L.ones + tc::none16_off((uint32_t)rr, 1), &one, 2);
   }
   cudaError_t e = cudaMalloc(blk_dev, blk.size());
   if (e != cudaSuccess) return e;
@@ -915,6 +981,12 @@ cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases,
     if (cov.lower[p] == 2) a.pair23 = p;
   }
   a.eval_idx = eval_idx; a.eval_n = eval_n; a.eval_base = eval_base; a.eval_out = static_cast<float*>(eval_out);
+  {
+    const uint16_t sb = f2bf(pert.step_f), ob = f2bf(pert.origin_f);
+    const uint16_t sS = (uint16_t)(sb + (130u << 7));   // step * 2^130 (exponent field + 130)
+    a.stepS2 = (uint32_t)sS | ((uint32_t)sS << 16);
+    a.org2 = (uint32_t)ob | ((uint32_t)ob << 16);
+  }
   if (eval_idx) {
     a.tiles_per_base = (uint64_t)((eval_n + 255) / 256);
     a.n_pairs_tiles = a.tiles_per_base;

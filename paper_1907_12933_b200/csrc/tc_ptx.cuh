@@ -51,6 +51,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #endif
 }
 
+// wait with a nanosleep back-off between polls: for warps whose waits are long and off the critical
+// path, so their polling does not steal issue slots from the working warps of the same SMSP
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns) {
+  while (!mbar_try(bar, phase)) __nanosleep(ns);
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -128,6 +134,21 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
   return d;
+}
+// Shared-memory matrix descriptor, K-major, no swizzle (canonical INTERLEAVE layout): 8-row x 16-byte
+// core matrices stored contiguously (128 B), K-adjacent core matrices `lbo` bytes apart, 8-row groups
+// `sbo` bytes apart (cute/atom/mma_traits_sm100.hpp: ((8,m),(T,2)):((1T,SBO),(1,LBO))).
+__device__ __forceinline__ uint64_t sdesc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  return d;                               // layout type 0 = SWIZZLE_NONE
+}
+// byte offset of (row, k) (16-bit elements, K = 16) in that layout with lbo = 128, sbo = 256
+__host__ __device__ __forceinline__ uint32_t none16_off(uint32_t row, uint32_t k) {
+  return (row >> 3) * 256u + (k >> 3) * 128u + (row & 7u) * 16u + (k & 7u) * 2u;
 }
 // byte offset of (row, byte-in-row) inside a SWIZZLE_128B K-major tile
 __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t byte) {

@@ -51,3 +51,20 @@ for name, a, b in (("L1 gen-wait span kb0->kblast", 1, 2), ("h1 wait after kblas
                    ("gen tile", 6, 7)):
     d = r0[8:60, b] - r0[8:60, a]
     print(f"{name:32s} median {np.median(d):8.0f}  min {d.min():8d}  max {d.max():8d}")
+
+g = np.zeros((2, 2, 4, 13, 5), np.uint64)
+assert P.lib().mlpv_f3_trace_gen_read(g.ctypes.data_as(C.c_void_p)) == 0
+g = g.astype(np.int64)
+for rank in (0, 1):
+    for grp in (0, 1):
+        d = g[rank, grp]
+        m = d[:, :, 0] != 0
+        comp = (d[:, :, 1] - d[:, :, 0])[m]
+        wait = (d[:, :, 2] - d[:, :, 1])[m]
+        store = (d[:, :, 3] - d[:, :, 2])[m]
+        arr = (d[:, :, 4] - d[:, :, 3])[m]
+        print(f"gen rank {rank} grp {grp}: per-stage median compute {np.median(comp):.0f} wait {np.median(wait):.0f} "
+              f"store+fence {np.median(store):.0f} arrive {np.median(arr):.0f}")
+        row = d[1]
+        print("   tile 9 stage starts", [int(x - row[0, 0]) if x else None for x in row[:, 0]])
+        print("   tile 9 waits       ", [int(a - b) if a else None for a, b in zip(row[:, 2], row[:, 1])])
