@@ -28,6 +28,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
         return lib
     tmp = lib + f".tmp{os.getpid()}"
     extra = ["-DMLPV_TRACE"] if trace else []
+    if trace and os.environ.get("MLPV_EXP"):          # timing experiments (results are wrong by design)
+        extra.append(f"-DMLPV_EXP={int(os.environ['MLPV_EXP'])}")
     if os.environ.get("MLPV_WAIT_TIMEOUT"):            # debug: trap instead of hanging on a lost arrive
         extra.append(f"-DMLPV_WAIT_TIMEOUT={int(os.environ['MLPV_WAIT_TIMEOUT'])}")
     cmd = [NVCC, *FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]

@@ -51,10 +51,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #endif
 }
 
-// wait with a nanosleep back-off between polls: for warps whose waits are long and off the critical
-// path, so their polling does not steal issue slots from the working warps of the same SMSP
+// Long waits.  try_wait suspends the thread only until the next mbarrier event of the CTA (it
+// returns almost at once in a busy CTA, measured), so a polling loop burns issue slots; a nanosleep
+// between polls caps that at one poll per `ns` (and adds at most ~ns of wake-up latency).  Only one
+// warp per role polls; the others sleep in a named barrier.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns) {
-  while (!mbar_try(bar, phase)) __nanosleep(ns);
+#ifdef MLPV_WAIT_TIMEOUT
+  const long long t0 = clock64();
+#endif
+  while (!mbar_try(bar, phase)) {
+    __nanosleep(ns);
+#ifdef MLPV_WAIT_TIMEOUT
+    if (clock64() - t0 > (long long)MLPV_WAIT_TIMEOUT) {
+      printf("mlpv wait timeout: block %d thread %d bar smem 0x%x phase %u\n", blockIdx.x, threadIdx.x,
+             smem_u32(bar), phase);
+      __trap();
+    }
+#endif
+  }
 }
 
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
@@ -294,6 +308,13 @@ __device__ __forceinline__ void mma2_f16_ts(uint32_t d, uint32_t a_tmem, uint64_
       "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
+}
+// one lane of a converged warp (the MMA-issuing warps run their loops warp-uniformly so that
+// descriptors live in uniform registers; only the elected lane issues)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; selp.u32 %0, 1, 0, e; }" : "=r"(p));
+  return p != 0;
 }
 // commit the leader's previously issued MMAs to the mbarrier at `bar`'s offset in every CTA of mask
 __device__ __forceinline__ void mma2_commit(uint64_t* bar, uint16_t mask) {

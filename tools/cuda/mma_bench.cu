@@ -1,0 +1,192 @@
+// Throughput microbenchmark of tcgen05.mma forms used by k_fused3 (tools only, not product).
+// mode 0: cta_group::2 SS M=256 N=256 K=16 (bf16); 1: cta_group::2 TS (A in TMEM);
+// mode 2: cta_group::2 SS N=128; mode 3: cta_group::1 SS M=128 N=256.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include "../../paper_1907_12933_b200/csrc/tc_ptx.cuh"
+using namespace mlpv::tc;
+
+__device__ __forceinline__ void mma1_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) { mma_f16_ss(d, a, b, idesc, acc); }
+
+__device__ unsigned int g_sink;
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int reps, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t ready, done, scratch[4], pre;
+  __shared__ uint32_t tbase;
+  const uint32_t rank = cluster_ctarank();
+  const int t = threadIdx.x, w = t >> 5;
+  uint8_t* sA = smem;                 // 4 x 16 KB
+  uint8_t* sB = smem + 4 * 16384;     // 4 x 16 KB
+  for (int i = t; i < 8 * 16384 / 16; i += blockDim.x) {
+    if (MODE >= 7) {                                   // random bf16 in [-1, 1) / [0, 1)
+      uint32_t x = (uint32_t)(i * 2654435761u) ^ (rank * 97u);
+      uint32_t v[4];
+      for (int k = 0; k < 4; k++) {
+        x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+        const uint32_t lo = 0x3f00u | (x & 0x7fu) | ((x >> 8) & 0x8000u), hi = 0x3e80u | ((x >> 16) & 0x7fu);
+        v[k] = lo | (hi << 16);
+      }
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(v[0], v[1], v[2], v[3]);
+    } else reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0, 0);
+  }
+  if (t == 0) {
+    mbar_init(&ready, (MODE != 3 && rank == 0) ? 2 : 1); mbar_init(&done, 1);
+    for (int i = 0; i < 4; i++) mbar_init(&scratch[i], 1);
+    mbar_init(&pre, 1);
+    fence_mbar_init();
+  }
+  if (w == 0) { if (MODE == 3) { tmem_alloc(&tbase, 512); tmem_relinquish(); } else { tmem_alloc2(&tbase, 512); tmem_relinquish2(); } }
+  fence_proxy_async();
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const uint32_t tb = tbase;
+  if (t == 0) { if (rank == 0 || MODE == 3) mbar_arrive(&ready); else mbar_arrive_cluster(&ready, 0); }
+  if (t == 0) mbar_arrive(&pre);                       // phase 0 of `pre` completes: waits on it are no-ops
+  const bool issuer = (MODE == 3) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15);
+  __shared__ volatile int stop;
+  if (t == 0) stop = 0;
+  __syncthreads();
+  __shared__ unsigned long long ld_cnt;
+  if (t == 0) ld_cnt = 0;
+  __syncthreads();
+  if ((MODE == 14 || MODE == 15 || MODE == 16 || MODE == 17) && w >= 4 && w < 8) {
+    const uint32_t loff = (uint32_t)(32 * (w & 3)) << 16;
+    const uint32_t lcol = MODE == 16 ? 0u : (MODE == 17 ? 256u : 256u);
+    unsigned long long n = 0;
+    uint32_t acc = 0;
+    const long long t0 = clock64();
+    while (!stop) {
+#pragma unroll
+      for (int g = 0; g < 16; g++) {
+        uint32_t v[16];
+        tmem_ld16(tbase + loff + lcol + 16 * g, v);
+        tmem_ld_wait();
+        acc += v[0] ^ v[15];
+      }
+      n += 16;
+      if (MODE == 15 && n >= 16 * 2000) break;
+    }
+    const long long t1 = clock64();
+    if ((t & 31) == 0 && w == 4 && blockIdx.x == 0) printf("  ld16 rate: %.1f cycles per ld16+wait (warp), %.1f B/clk/SM (4 warps)\n",
+        (double)(t1 - t0) / n, 4.0 * n * 32 * 16 * 4 / (double)(t1 - t0));
+    if (acc == 0x1234567u) g_sink = acc;
+  } else if (w >= 4 && MODE >= 10 && MODE < 14) {
+    // background load while the MMAs run (warps 4..11)
+    uint32_t c0 = t, c1 = t * 7, c2 = t * 13, c3 = t * 31, acc = 0;
+    uint8_t* scratch = smem + 8 * 16384;                 // 32 KB scratch
+    int it = 0;
+    while (!stop) {
+      if (MODE == 10 || MODE == 12) {
+#pragma unroll
+        for (int r = 0; r < 10; r++) {
+          const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+          const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+          c0 = hi1 ^ c1 ^ r; c1 = lo1; c2 = hi0 ^ c3 ^ (r * 3); c3 = lo0;
+        }
+        acc += c0 ^ c2;
+      }
+      if (MODE == 11 || MODE == 12) {
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          *reinterpret_cast<uint4*>(scratch + ((t * 16 + (it * 4 + k) * 4096) & 32767)) = make_uint4(c0, c1, acc, it);
+      }
+      it++;
+    }
+    if (acc == 0x12345u) g_sink = acc;
+  }
+  if (issuer) {
+    if (MODE != 3) mbar_wait_cluster(&ready, 0); else mbar_wait(&ready, 0);
+    fence_after();
+    const uint32_t N = MODE == 2 ? 128 : 256;
+    const uint32_t idesc = MODE == 3 ? idesc_f16(128, N, 1, 1) : idesc_f16(256, N, 1, 1);
+    long long t0 = clock64();
+    if (MODE == 13) {                                    // k_fused3's rings: A 6 x 16 KB, B 5 x 16 KB
+      uint32_t gsl = 0, wsl = 0;
+      for (int r = 0; r < reps / 4; r++)
+        for (int kb = 0; kb < 13; kb++) {
+          const uint32_t ab = smem_u32(smem + gsl * 16384), bb = smem_u32(smem + 6 * 16384 + wsl * 16384);
+          if (++gsl == 6) gsl = 0;
+          if (++wsl == 5) wsl = 0;
+          const int nk = kb == 12 ? 2 : 4;
+#pragma unroll
+          for (int kk = 0; kk < 4; kk++)
+            if (kk < nk) mma2_f16_ss(tb, sdesc_sw128(ab + 32u * kk), sdesc_sw128(bb + 32u * kk), idesc, (kb | kk) ? 1u : 0u);
+          mma2_commit(&scratch[0], 0x3);
+          mma2_commit(&scratch[1], 0x3);
+        }
+    } else
+    for (int r = 0; r < reps; r++)
+      for (int kb = 0; kb < 4; kb++) {
+        if (MODE == 5 || MODE == 6) { mbar_wait(&pre, 0); mbar_wait(&pre, 0); fence_after(); }
+#pragma unroll
+        for (int kk = 0; kk < 4; kk++) {
+          const uint64_t ad = sdesc_sw128(smem_u32(sA + kb * 16384 + kk * 32));
+          const uint64_t bd = sdesc_sw128(smem_u32(sB + kb * 16384 + kk * 32));
+          const uint32_t acc = (r | kb | kk) ? 1u : 0u;
+          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16)) mma2_f16_ss(tb, ad, bd, idesc, acc);
+          else if (MODE == 1) mma2_f16_ts(tb, tb + 256 + kb * 32 + kk * 8, bd, idesc, acc);
+          else if (MODE == 16 || MODE == 17) mma2_f16_ts(tb + 256, tb + kb * 32 + kk * 8, bd, idesc_f16(256, 128, 1, 1), acc);
+          else mma1_ss(tb, ad, bd, idesc, acc);
+        }
+        if (MODE == 4 || MODE == 6) { mma2_commit(&scratch[0], 0x3); mma2_commit(&scratch[1], 0x3); }
+      }
+    if (MODE == 3) mma_commit(&done); else mma2_commit(&done, 0x3);
+    mbar_wait(&done, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) *cyc = (unsigned long long)(t1 - t0);
+  }
+  if (t == 0) {                                        // stop the background warps of both CTAs
+    if (issuer || MODE == 3) stop = 1;
+  }
+  if (MODE != 3) { if (t < 32 && !issuer) {} }
+  __syncwarp();
+  if (!issuer && t == 0 && MODE != 3 && MODE != 15) { mbar_wait(&done, 0); stop = 1; }
+  fence_before();
+  __syncthreads();
+  cluster_sync();
+  fence_after();
+  if (w == 0) { if (MODE == 3) tmem_dealloc(tb, 512); else tmem_dealloc2(tb, 512); }
+}
+
+template <int MODE>
+void run(const char* name) {
+  const size_t smem = (MODE == 13 ? 13 : 10) * 16384 + 1024;
+  cudaFuncSetAttribute(k_bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, 8);
+  const int reps = 2000;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int nt = MODE >= 10 ? 384 : 128;
+  k_bench<MODE><<<148, nt, smem>>>(10, cyc);
+  cudaEventRecord(e0);
+  k_bench<MODE><<<148, nt, smem>>>(reps, cyc);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  unsigned long long c = 0;
+  cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  const double M = MODE == 3 ? 128 : 256, N = MODE == 2 ? 128 : 256;
+  const double groups = MODE == 3 ? 148 : 74;
+  const double flops = MODE == 13 ? 2.0 * M * N * 16 * 50 * (reps / 4) * groups : 2.0 * M * N * 16 * 16 * reps * groups;
+  printf("%-28s err=%d  %.3f ms  %.1f TFLOP/s  cycles/MMA (cluster 0) %.1f\n", name, (int)e, ms, flops / (ms * 1e-3) / 1e12,
+         (double)c / (MODE == 13 ? 50.0 * (reps / 4) : 16.0 * reps));
+}
+
+int main() {
+  run<0>("2CTA SS M256 N256 K16");
+  run<1>("2CTA TS M256 N256 K16");
+  run<2>("2CTA SS M256 N128 K16");
+  run<7>("2CTA SS random data");
+  run<13>("2CTA SS k_fused3 rings");
+  run<14>("2CTA SS + 4 warps tcgen05.ld");
+  run<15>("tcgen05.ld only (no MMA)");
+  run<16>("TS MMA (A cols 0-127, D 256+) + ld cols 0-255");
+  run<17>("TS MMA (A cols 0-127, D 256+) + ld cols 256+");
+  return 0;
+}

@@ -68,3 +68,41 @@ for rank in (0, 1):
         row = d[1]
         print("   tile 9 stage starts", [int(x - row[0, 0]) if x else None for x in row[:, 0]])
         print("   tile 9 waits       ", [int(a - b) if a else None for a, b in zip(row[:, 2], row[:, 1])])
+
+q = np.zeros((4, 13, 8), np.uint64)
+assert P.lib().mlpv_f3_trace_iss_read(q.ctypes.data_as(C.c_void_p)) == 0
+q = q.astype(np.int64)
+thr = q[:, :, 1] - q[:, :, 0]
+gf = q[:, :, 2] - q[:, :, 1]
+wf = q[:, :, 3] - q[:, :, 2]
+print(f"issuer per-stage median: throttle wait {np.median(thr):.0f}  g_full wait {np.median(gf):.0f}  w_full wait {np.median(wf):.0f}")
+print("  tile 9 throttle", thr[1].tolist())
+print("  tile 9 g_full  ", gf[1].tolist())
+print("  tile 9 w_full  ", wf[1].tolist())
+print("  tile 9 stage-to-stage", np.diff(q[1, :, 0]).tolist())
+print("  tile 9 mma issue     ", (q[1, :, 4] - q[1, :, 3]).tolist())
+print("  tile 9 serialized stage latency", (q[1, :, 7] - q[1, :, 6]).tolist())
+print("  tile 9 commits       ", (q[1, :, 5] - q[1, :, 4]).tolist())
+print("  tile 9 to next top   ", (q[1, 1:, 0] - q[1, :-1, 5]).tolist())
+
+dn = np.zeros((4, 13), np.uint64)
+assert P.lib().mlpv_f3_trace_done_read(dn.ctypes.data_as(C.c_void_p)) == 0
+dn = dn.astype(np.int64)
+print("stage completion - issue (tile 9):", (dn[1] - q[1, :, 3]).tolist())
+print("completion intervals (tile 9):   ", np.diff(dn[1]).tolist())
+
+ep = np.zeros((2, 4, 8), np.uint64)
+assert P.lib().mlpv_f3_trace_epi_read(ep.ctypes.data_as(C.c_void_p)) == 0
+ep = ep.astype(np.int64)
+for team, nm in ((0, "E1"), (1, "E2")):
+    for k in range(4):
+        r = ep[team, k]
+        print(f"{nm} tile {8 + k}: passA {r[1] - r[0]}  kb signals " + " ".join(str(r[2 + j] - r[0]) for j in range(4)))
+
+e2 = np.zeros((16, 5), np.uint64)
+assert P.lib().mlpv_f3_trace_e2_read(e2.ctypes.data_as(C.c_void_p)) == 0
+e2 = e2.astype(np.int64)
+print("E2 tile 9 per item: stats / split / stores / wait_ld / total")
+for i in range(16):
+    r = e2[i]
+    print(f"  item {i:2d}: {r[1]-r[0]:5d} {r[2]-r[1]:5d} {r[3]-r[2]:5d} {r[4]-r[3]:5d}   {r[4]-r[0]:5d}")
