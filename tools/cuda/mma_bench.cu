@@ -53,7 +53,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
   __shared__ unsigned long long ld_cnt;
   if (t == 0) ld_cnt = 0;
   __syncthreads();
-  if ((MODE == 14 || MODE == 15 || MODE == 16 || MODE == 17) && w >= 4 && w < 8) {
+  if (MODE == 19 && w == 4 && rank == 0) {
+    // second issuer: small TS MMAs (N = 16, A from TMEM cols 256.., D cols 496..) like layer 3
+    const bool el = elect_one();
+    unsigned long long n = 0;
+    const uint32_t id3 = idesc_f16(256, 16, 0, 0);
+    const uint64_t bd = sdesc_sw128(smem_u32(smem + 8 * 16384));
+    while (!stop) {
+      if (el) {
+#pragma unroll
+        for (int g = 0; g < 8; g++) mma2_f16_ts(tbase + 496, tbase + 256 + 16 * g, bd, id3, g ? 1u : 0u);
+      }
+      __syncwarp();
+      n++;
+      __nanosleep(400);
+    }
+    if (el && blockIdx.x == 0) printf("  L3-like batches issued: %llu\n", n);
+  } else if (MODE == 18 && w >= 4 && w < 8) {
+    const uint32_t loff = (uint32_t)(32 * (w & 3)) << 16;
+    unsigned long long n = 0;
+    uint32_t v[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+    const long long t0 = clock64();
+    while (!stop) {
+#pragma unroll
+      for (int g = 0; g < 16; g++) {
+        uint32_t x[16];
+        tmem_ld16(tbase + loff + 256 + 16 * g, x);
+        tmem_ld_wait();
+        v[0] += x[3];
+        tmem_st8(tbase + loff + 256 + 16 * g, v);
+        tmem_st8(tbase + loff + 256 + 16 * g + 8, v);
+      }
+      tmem_st_wait();
+      n += 16;
+    }
+    const long long t1 = clock64();
+    if ((t & 31) == 0 && w == 4 && blockIdx.x == 0) printf("  ld16+2xst8 rate: %.1f cycles per group (warp)\n", (double)(t1 - t0) / n);
+  } else if ((MODE == 14 || MODE == 15 || MODE == 16 || MODE == 17) && w >= 4 && w < 8) {
     const uint32_t loff = (uint32_t)(32 * (w & 3)) << 16;
     const uint32_t lcol = MODE == 16 ? 0u : (MODE == 17 ? 256u : 256u);
     unsigned long long n = 0;
@@ -127,7 +163,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
           const uint64_t ad = sdesc_sw128(smem_u32(sA + kb * 16384 + kk * 32));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + kb * 16384 + kk * 32));
           const uint32_t acc = (r | kb | kk) ? 1u : 0u;
-          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16)) mma2_f16_ss(tb, ad, bd, idesc, acc);
+          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16) || MODE == 18 || MODE == 19) mma2_f16_ss(tb, ad, bd, idesc, acc);
           else if (MODE == 1) mma2_f16_ts(tb, tb + 256 + kb * 32 + kk * 8, bd, idesc, acc);
           else if (MODE == 16 || MODE == 17) mma2_f16_ts(tb + 256, tb + kb * 32 + kk * 8, bd, idesc_f16(256, 128, 1, 1), acc);
           else mma1_ss(tb, ad, bd, idesc, acc);
@@ -180,13 +216,8 @@ void run(const char* name) {
 
 int main() {
   run<0>("2CTA SS M256 N256 K16");
-  run<1>("2CTA TS M256 N256 K16");
-  run<2>("2CTA SS M256 N128 K16");
-  run<7>("2CTA SS random data");
-  run<13>("2CTA SS k_fused3 rings");
   run<14>("2CTA SS + 4 warps tcgen05.ld");
-  run<15>("tcgen05.ld only (no MMA)");
-  run<16>("TS MMA (A cols 0-127, D 256+) + ld cols 0-255");
-  run<17>("TS MMA (A cols 0-127, D 256+) + ld cols 256+");
+  run<18>("2CTA SS + 4 warps ld16/st8 in place");
+  run<19>("2CTA SS + L3-like TS N=16 batches");
   return 0;
 }

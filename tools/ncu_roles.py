@@ -20,7 +20,7 @@ src = open('paper_1907_12933_b200/csrc/k_fused3.cu').read().splitlines()
 def find(tag):
     return [i for i, l in enumerate(src) if tag in l][0] + 1
 marks = [("ctl", find("weight producer (both CTAs)")), ("gen", find("---- generator (both CTAs)")),
-         ("E1", find("E1: layer-1 epilogue")), ("E2", find("E2 / E3: layers 2 and 3")),
+         ("E", find("---- epilogue team")),
          ("end", [i for i, l in enumerate(src) if l.startswith('  fence_before();')][-1] + 1)]
 tot_s = sum(l[3] for l in lines); tot_i = sum(l[4] for l in lines)
 for (nm, lo), (_, hi) in zip(marks[:-1], marks[1:]):

@@ -72,7 +72,7 @@ for rank in (0, 1):
 q = np.zeros((4, 13, 8), np.uint64)
 assert P.lib().mlpv_f3_trace_iss_read(q.ctypes.data_as(C.c_void_p)) == 0
 q = q.astype(np.int64)
-thr = q[:, :, 1] - q[:, :, 0]
+thr = q[:, :, 1] - q[:, :, 0]     # stage top -> before the next-stage waits (2 MMAs issued)
 gf = q[:, :, 2] - q[:, :, 1]
 wf = q[:, :, 3] - q[:, :, 2]
 print(f"issuer per-stage median: throttle wait {np.median(thr):.0f}  g_full wait {np.median(gf):.0f}  w_full wait {np.median(wf):.0f}")
