@@ -100,6 +100,13 @@ typedef struct {
  *                  BF16: x'_p = RNE_bf16(clamp(x_p + RNE_bf16(l_p*step + origin), 0, 1)), exact sums.
  *                  INT8: x'_p = clamp(x_p + l_p*step + origin, 0, 255), integer step / origin.
  *                  c < n_samples <= 2^32.  BF16 and INT8 numerics only.
+ *   PHILOX_BOX     the same Philox levels, applied exactly: x'_p = x_p + origin + l_p * step as a
+ *                  real number (no rounding to the input type, no clamping), i.e. the 16-point
+ *                  lattice of the L-inf box [x - eps, x + eps] with origin = -eps, step = 2 eps / 15
+ *                  (reading C14b).  Linear in the levels, so u_1 = W_1 x + b_1 +
+ *                  origin W_1 1 + step W_1 l.  BF16 numerics, 3-layer nets with 256-wide hidden
+ *                  layers (the k_fused3 path); other nets return MLPV_E_UNSUPPORTED.
+ *                  mlpv_decode writes the candidate as n_0 doubles.
  * `levels` element type: float (FP32) | uint16 bf16 bits (BF16) | int16 (Q4_12, INT8).
  * Every call processes the half-open index range [index_begin, index_end) of EVERY base input;
  * disjoint ranges merge by sum / min / OR (mlpv_merge). */
@@ -107,7 +114,8 @@ typedef enum {
     MLPV_PERT_TUPLE_REPLACE = 0,
     MLPV_PERT_SUBSET_OFFSET = 1,
     MLPV_PERT_SUBSET_REPLACE = 2,
-    MLPV_PERT_PHILOX_LATTICE = 3
+    MLPV_PERT_PHILOX_LATTICE = 3,
+    MLPV_PERT_PHILOX_BOX = 4
 } mlpv_pert_kind;
 
 typedef struct {

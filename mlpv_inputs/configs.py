@@ -18,7 +18,7 @@ import numpy as np
 # enum values mirror include/mlpv.h (plain integers; the oracle has its own copy)
 NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8 = 0, 1, 2, 3
 ACT_SIGMOID, ACT_PL_SIGMOID, ACT_RELU = 0, 1, 2
-PERT_TUPLE_REPLACE, PERT_SUBSET_OFFSET, PERT_SUBSET_REPLACE, PERT_PHILOX_LATTICE = 0, 1, 2, 3
+PERT_TUPLE_REPLACE, PERT_SUBSET_OFFSET, PERT_SUBSET_REPLACE, PERT_PHILOX_LATTICE, PERT_PHILOX_BOX = 0, 1, 2, 3, 4
 PROP_ARGMAX_UNCHANGED, PROP_TARGET_NEVER, PROP_THRESHOLD_LITERAL = 0, 1, 2
 
 CONFIG_IDS = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5_bf16", "cfg5_int8"]
@@ -251,8 +251,8 @@ def _cfg4() -> Config:
     bases = f32_to_bf16_bits(img)
     seed = int(_rng(4, 3).integers(2 ** 64, dtype=np.uint64))
     net = Net(sizes, ACT_RELU, NUM_BF16, Wb, b, acc_scale=[1.0, 1.0, 1.0])
-    pert = Pert(PERT_PHILOX_LATTICE, seed=seed, n_samples=2 ** 32,
-                lattice_step=_bf16_scalar(0.1 / 15.0), lattice_origin=_bf16_scalar(-0.05))
+    # the exact L-inf box lattice (reading C14b): offsets -0.05 + l * 0.1/15, l = 0..15
+    pert = Pert(PERT_PHILOX_BOX, seed=seed, n_samples=2 ** 32, lattice_step=0.1 / 15.0, lattice_origin=-0.05)
     pert.index_end = pert.n_samples
     return Config("cfg4", "784-256-256-10 ReLU bf16, 1000 bases, 2^32 Philox L-inf eps=0.05 samples/base",
                   net, bases, pert, Prop(), CovSpec([1, 2]))

@@ -35,7 +35,7 @@
 
 enum { O_FP32 = 0, O_BF16 = 1, O_Q412 = 2, O_INT8 = 3 };
 enum { O_SIGMOID = 0, O_PLSIG = 1, O_RELU = 2 };
-enum { O_TUPLE = 0, O_SUB_OFF = 1, O_SUB_REP = 2, O_PHILOX = 3 };
+enum { O_TUPLE = 0, O_SUB_OFF = 1, O_SUB_REP = 2, O_PHILOX = 3, O_BOX = 4 };
 enum { O_UNCHANGED = 0, O_TARGET = 1, O_LITERAL = 2 };
 
 typedef struct {
@@ -210,9 +210,9 @@ static void dnet_free(dnet *d) {
 
 /* potentials of layers 1..L, concatenated, into trace; h, hn: scratch of maxw doubles.
  * Returns 0, or -1 if a fixed-point accumulator leaves int32 (the C-ABI rejects such nets). */
-static int forward_d(const dnet *d, const void *img, double *trace, double *h, double *hn) {
+static int forward_d(const dnet *d, const void *img, const double *ximg, double *trace, double *h, double *hn) {
     const onet *n = d->n;
-    for (int j = 0; j < n->sizes[0]; j++) h[j] = in_get(n->numeric, img, j);
+    for (int j = 0; j < n->sizes[0]; j++) h[j] = ximg ? ximg[j] : in_get(n->numeric, img, j);
     int off = 0, rc = 0;
     for (int l = 1; l <= n->L; l++) {
         int nl = n->sizes[l], fan = n->sizes[l - 1];
@@ -258,7 +258,7 @@ int orc_forward(const onet *n, const void *img, double *trace) {
     dnet d;
     dnet_init(&d, n);
     double *h = (double *)malloc(sizeof(double) * d.maxw), *hn = (double *)malloc(sizeof(double) * d.maxw);
-    int rc = forward_d(&d, img, trace, h, hn);
+    int rc = forward_d(&d, img, NULL, trace, h, hn);
     free(h); free(hn);
     dnet_free(&d);
     return rc;
@@ -340,6 +340,36 @@ void orc_decode(int numeric, const opert *p, const void *base, int n0, int base_
                 in_set(numeric, out, px, v);
             }
     }
+}
+
+/* PHILOX_BOX (reading C14b): the same Philox levels as PHILOX_LATTICE, applied exactly,
+ * x'_p = x_p + origin + l_p * step as a real number (no rounding to the input type, no clamping):
+ * the 16-point lattice of the L-inf box of radius -origin around x.  Written as n0 doubles. */
+void orc_decode_box(int numeric, const opert *p, const void *base, int n0, int base_id, uint64_t index, double *out) {
+    uint32_t key[2] = { (uint32_t)p->seed, (uint32_t)(p->seed >> 32) };
+    int nblk = (n0 + 31) / 32;
+    for (int j = 0; j < nblk; j++) {
+        uint32_t ctr[4] = { (uint32_t)index, (uint32_t)(index >> 32), (uint32_t)base_id, (uint32_t)j };
+        uint32_t w[4];
+        orc_philox(ctr, key, w);
+        for (int ww = 0; ww < 4; ww++)
+            for (int nb = 0; nb < 8; nb++) {
+                int px = 32 * j + 8 * ww + nb;
+                if (px >= n0) continue;
+                int l = (int)((w[ww] >> (4 * nb)) & 15u);
+                out[px] = in_get(numeric, base, px) + (p->origin + (double)l * p->step);
+            }
+    }
+}
+
+int orc_forward_dbl(const onet *n, const double *x, double *trace) {
+    dnet d;
+    dnet_init(&d, n);
+    double *h = (double *)malloc(sizeof(double) * d.maxw), *hn = (double *)malloc(sizeof(double) * d.maxw);
+    int rc = forward_d(&d, NULL, x, trace, h, hn);
+    free(h); free(hn);
+    dnet_free(&d);
+    return rc;
 }
 
 /* ------------------------------------------------------------------ covering methods (§III.B) */
@@ -492,7 +522,7 @@ int orc_check(const onet *n, const void *bases, int n_base, const opert *p, cons
         double *tb = (double *)malloc(sizeof(double) * T);
         {
             double *h = (double *)malloc(sizeof(double) * dn.maxw), *hn = (double *)malloc(sizeof(double) * dn.maxw);
-            if (forward_d(&dn, base, tb, h, hn)) bad = 1;
+            if (forward_d(&dn, base, NULL, tb, h, hn)) bad = 1;
             free(h); free(hn);
         }
         int base_cls = argmax_of(tb + T - nL, nL);
@@ -502,6 +532,7 @@ int orc_check(const onet *n, const void *bases, int n_base, const opert *p, cons
             double *tc = (double *)malloc(sizeof(double) * T);
             double *h = (double *)malloc(sizeof(double) * dn.maxw), *hn = (double *)malloc(sizeof(double) * dn.maxw);
             void *img = malloc(esz * (size_t)n0);
+            double *ximg = p->kind == O_BOX ? (double *)malloc(sizeof(double) * (size_t)n0) : NULL;
             uint32_t *wa = (uint32_t *)calloc(nwords + 1, 4), *wc = (uint32_t *)calloc(nwords + 1, 4);
             uint32_t *wt = (uint32_t *)calloc(nwords + 1, 4);
             int cert[64];
@@ -510,8 +541,9 @@ int orc_check(const onet *n, const void *bases, int n_base, const opert *p, cons
 #pragma omp for schedule(dynamic, 8)
             for (int64_t ci = (int64_t)p->begin; ci < (int64_t)p->end; ci++) {
                 uint64_t c = (uint64_t)ci;
-                orc_decode(n->numeric, p, base, n0, b, c, img);
-                if (forward_d(&dn, img, tc, h, hn)) lbad = 1;
+                if (ximg) orc_decode_box(n->numeric, p, base, n0, b, c, ximg);
+                else orc_decode(n->numeric, p, base, n0, b, c, img);
+                if (forward_d(&dn, img, ximg, tc, h, hn)) lbad = 1;
                 int flag;
                 int v = property_eval(pr, tc + T - nL, nL, base_cls, V, fl, cov->near_tie, &flag);
                 lchk++;
@@ -544,7 +576,7 @@ int orc_check(const onet *n, const void *bases, int n_base, const opert *p, cons
                 for (size_t x = 0; x < nwords; x++) { res->cov_all[x] |= wa[x]; res->cov_certain[x] |= wc[x]; }
                 if (lbad) bad = 1;
             }
-            free(tc); free(h); free(hn); free(img); free(wa); free(wc); free(wt);
+            free(tc); free(h); free(hn); free(img); free(ximg); free(wa); free(wc); free(wt);
         }
         res->checked[b] = checked;
         res->violated[b] = viol;

@@ -82,6 +82,10 @@ def lib():
         _lib.orc_space_size.argtypes = [C.POINTER(_Pert), C.c_int]
         _lib.orc_decode.argtypes = [C.c_int, C.POINTER(_Pert), C.c_void_p, C.c_int, C.c_int,
                                     C.c_uint64, C.c_void_p]
+        _lib.orc_decode_box.argtypes = [C.c_int, C.POINTER(_Pert), C.c_void_p, C.c_int, C.c_int,
+                                        C.c_uint64, C.POINTER(C.c_double)]
+        _lib.orc_forward_dbl.restype = C.c_int
+        _lib.orc_forward_dbl.argtypes = [C.POINTER(_Net), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib.orc_coverage_layout.restype = C.c_size_t
         _lib.orc_coverage_layout.argtypes = [C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_int32),
                                              C.POINTER(C.c_size_t)]
@@ -154,13 +158,17 @@ def philox(ctr, key) -> np.ndarray:
 
 
 def forward(net, img) -> List[np.ndarray]:
-    """Potentials u_1..u_L (Eq. 1) of one image given in the net's input type."""
+    """Potentials u_1..u_L (Eq. 1) of one image given in the net's input type, or as exact
+    real values (float64, the PHILOX_BOX candidates)."""
     keep = _Keep()
     n = _mk_net(net, keep)
     x = keep.arr(img, img.dtype)
     T = int(sum(net.sizes[1:]))
     out = np.zeros(T, np.float64)
-    rc = lib().orc_forward(C.byref(n), x.ctypes.data, _p(out, C.c_double))
+    if img.dtype == np.float64:
+        rc = lib().orc_forward_dbl(C.byref(n), _p(x, C.c_double), _p(out, C.c_double))
+    else:
+        rc = lib().orc_forward(C.byref(n), x.ctypes.data, _p(out, C.c_double))
     if rc != 0:
         raise OverflowError("fixed-point accumulator left int32")
     res, o = [], 0
@@ -176,9 +184,16 @@ def space_size(pert, n0: int) -> int:
 
 
 def decode(numeric: int, pert, base: np.ndarray, base_id: int, index: int) -> np.ndarray:
+    """Candidate `index` of base `base_id` in the net's input type; PHILOX_BOX candidates are
+    exact real values and come back as float64."""
     keep = _Keep()
     p = _mk_pert(pert, keep)
     b = keep.arr(base, base.dtype)
+    if pert.kind == 4:
+        out = np.empty(b.shape[0], np.float64)
+        lib().orc_decode_box(numeric, C.byref(p), b.ctypes.data, b.shape[0], base_id, C.c_uint64(index),
+                             _p(out, C.c_double))
+        return out
     out = np.empty_like(b)
     lib().orc_decode(numeric, C.byref(p), b.ctypes.data, b.shape[0], base_id, C.c_uint64(index),
                      out.ctypes.data)

@@ -143,11 +143,12 @@ def _stream_ptr(stream):
 
 
 def decode(numeric: int, pert, base: np.ndarray, base_id: int, index: int) -> np.ndarray:
-    """Host-side candidate reconstruction (counterexample images)."""
+    """Host-side candidate reconstruction (counterexample images); PHILOX_BOX candidates are exact
+    reals and come back as float64."""
     keep = _Keep()
     p = _mk_pert(pert, keep)
     b = keep.arr(base, base.dtype)
-    out = np.empty_like(b)
+    out = np.empty(b.shape[0], np.float64) if pert.kind == 4 else np.empty_like(b)
     _ck(lib().mlpv_decode(numeric, C.byref(p), b.ctypes.data, b.shape[0], base_id, C.c_uint64(int(index)),
                           out.ctypes.data))
     return out

@@ -5,9 +5,11 @@
 // (cluster rank 0) issues every tcgen05.mma with cta_group::2 (M = 256: rows 0-127 of the tile in
 // CTA 0's TMEM lanes, rows 128-255 in CTA 1's), each CTA supplying half of every B operand.
 //
-//   layer 1  A = Philox-lattice candidates generated on chip into a SWIZZLE_128B ring; B = W1 half
-//            tiles streamed by cp.async.bulk; the layer-1 bias rides along as three extra K columns
-//            (bf16 hi / mid / lo of the fp32 bias), so TMEM cols [0,256) hold u1 (Eq. 1).
+//   layer 1  the exact L-inf box lattice (PHILOX_BOX, reading C14b) is linear in the Philox levels,
+//            u1 = W1 x + b1 + origin W1 1 + step W1 l: A = the levels l of every pixel (fp16
+//            subnormals l * 2^-24, one PRMT per pixel pair) generated on chip into a SWIZZLE_128B
+//            ring; B = W1 (fp16) half tiles streamed by cp.async.bulk; TMEM cols [0,256) accumulate
+//            2^-24 W1 l and E1 forms u1 = base1 + (step 2^24) acc with base1 from the prologue.
 //   E1       4 warps, thread = candidate row, all 256 neurons: pass A builds the sign-change words
 //            sc1 against the base potentials (one funnel shift per neuron); pass B turns u1 in
 //            place into the fp16 hi/lo split of h1 = ReLU(u1) (reading C19; each 16-column group
@@ -84,7 +86,6 @@ __device__ unsigned long long g_trace_gen[2][2][4][13][5];
 constexpr int kThreads = 768;
 constexpr int kSG = 6;                       // generator ring stages
 constexpr int kSW = 5;                       // weight ring stages
-constexpr int kLead = 4;                     // layer-1 stages the issuer may run ahead of the tensor pipe
 constexpr uint32_t kBiasTile = 4096;         // 128 rows x K 16 (fp16), no-swizzle layout
 constexpr uint32_t kTile = 16384;            // 128 rows x 128 B
 constexpr int kN1 = 256, kN2 = 256, kN3P = 16;
@@ -113,7 +114,7 @@ struct Layout {
 };
 __host__ __device__ inline Layout layout_of(int n0) {
   Layout L;
-  L.nk16 = (n0 + 3 + 15) / 16;               // K steps of layer 1 (pixels + 3 bias columns)
+  L.nk16 = (n0 + 15) / 16;                   // K steps of layer 1 (the bias enters through base1)
   L.nkb1 = (L.nk16 + 3) / 4;
   L.nst = L.nkb1 + kNkb2;
   L.stream = 0;
@@ -143,7 +144,8 @@ struct Args {
   int64_t eval_n;
   int eval_base;
   float* eval_out;
-  uint32_t stepS2, org2;                     // bf16x2 lattice constants: step * 2^130, origin
+  float stepS;                               // PHILOX_BOX: step * 2^24 (u1 = base1 + stepS * acc)
+  const float* base1;                        // [n_base][256] W1 x + b1 + origin W1 1
 };
 
 struct alignas(16) Smem {
@@ -152,9 +154,10 @@ struct alignas(16) Smem {
   uint64_t h1_kb[kNkb2];
   uint64_t h2_kb[kNkb2];
   uint32_t tbase;
-  int base_g, base_e;
+  int base_e;
   // epilogue team: base data
   alignas(16) float ub1[kN1];
+  alignas(16) float b1[kN1];                 // base1 of the staged base input (PHILOX_BOX)
   uint32_t nb1[8];
   float minub1;
   alignas(16) float ub2[kN2];
@@ -168,7 +171,6 @@ struct alignas(16) Smem {
   float xf[2][3][128];
   uint32_t sc2[8][128];                      // E2: sign-change words of layer 2
   uint16_t vc2[16][128];                     // E2 slow path: value-change bits of layer 2 (16 neurons)
-  alignas(16) uint16_t xg[kMaxN0 + 64];     // base image (bf16) for the generator, zero padded
 };
 
 constexpr size_t kTilesBytes = (size_t)(kSG + kSW) * kTile + (size_t)kChunks * kW3Chunk + 4 * kBiasTile;
@@ -216,42 +218,19 @@ __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
   return make_uint4(c0, c1, c2, c3);
 }
 
-__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-__device__ __forceinline__ uint32_t hfma2_relu(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("fma.rn.relu.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-__device__ __forceinline__ uint32_t hmin2(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
-
-// 4 lattice pixel pairs from one Philox word (nibble n -> pixel n, LSB first), x2[k] = base pixels
-// (bf16x2).  x' = min(relu(RNE(x + RNE(l*step + origin))), 1)  (reading C14).  The level pair is
-// built by one PRMT as the bf16 subnormals (l_a * 2^-130, l_b * 2^-130) -- nibble at bits 3..6 of
-// each byte, the other byte zero by PRMT's sign replication -- so one FMA with stepS = step * 2^130
-// gives l*step + origin exactly before its single rounding.
-__device__ __forceinline__ uint4 lattice_word(uint32_t w, uint4 x2, uint32_t stepS2, uint32_t org2) {
-  const uint32_t lo = (w << 3) & 0x78787878u;             // nibbles 0,2,4,6 -> bits 3..6 of bytes 0..3
-  const uint32_t hi = (w >> 1) & 0x78787878u;             // nibbles 1,3,5,7
-  const uint32_t one2 = 0x3F803F80u;
+// The 8 levels of one Philox word (nibble n -> pixel n, LSB first) as the fp16 subnormals
+// l * 2^-24, two per 32-bit word: one PRMT per pixel pair (the zero high bytes come from PRMT's
+// sign replication of the nibble bytes).  The layer-1 MMA then computes 2^-24 * W1 l exactly in
+// fp32 (products of an fp16 subnormal and an fp16 weight are exact; tools/test_subnormal_mma.py).
+__device__ __forceinline__ uint4 nibble_word(uint32_t w) {
+  const uint32_t lo = w & 0x0F0F0F0Fu;                   // nibbles 0, 2, 4, 6 in bytes 0..3
+  const uint32_t hi = (w >> 4) & 0x0F0F0F0Fu;            // nibbles 1, 3, 5, 7
   uint32_t o[4];
-  const uint32_t xs[4] = {x2.x, x2.y, x2.z, x2.w};
 #pragma unroll
   for (int k = 0; k < 4; k++) {
     const uint32_t sel = (uint32_t)k | ((8u + k) << 4) | ((4u + k) << 8) | ((12u + k) << 12);
-    uint32_t l;                                           // bf16x2 subnormals (l_a, l_b) * 2^-130
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(l) : "r"(lo), "r"(hi), "r"(sel));   // (__byte_perm drops the
-                                                                              //  sign-replicate bit)
-    const uint32_t off = hfma2(l, stepS2, org2);          // RNE(l*step + origin)
-    o[k] = hmin2(hfma2_relu(xs[k], one2, off), one2);     // min(relu(RNE(x + off)), 1)
-  }
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(o[k]) : "r"(lo), "r"(hi), "r"(sel));   // (__byte_perm drops
+  }                                                                             //  the sign-replicate bit)
   return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
@@ -315,6 +294,19 @@ __device__ __forceinline__ uint32_t sign_fold(const uint32_t (&v)[16], uint32_t 
   return m;
 }
 
+// layer-1 accumulators -> potentials: u1 = base1 + stepS * acc (reading C14b), in place
+template <int N>
+__device__ __forceinline__ void acc_to_u1(uint32_t (&v)[N], const float* b1, float stepS) {
+  const float4* b4 = reinterpret_cast<const float4*>(b1);
+#pragma unroll
+  for (int k = 0; k < N / 4; k++) {
+    const float4 bb = b4[k];
+    v[4 * k] = __float_as_uint(fmaf(__uint_as_float(v[4 * k]), stepS, bb.x));
+    v[4 * k + 1] = __float_as_uint(fmaf(__uint_as_float(v[4 * k + 1]), stepS, bb.y));
+    v[4 * k + 2] = __float_as_uint(fmaf(__uint_as_float(v[4 * k + 2]), stepS, bb.z));
+    v[4 * k + 3] = __float_as_uint(fmaf(__uint_as_float(v[4 * k + 3]), stepS, bb.w));
+  }
+}
 // sign bits of 32 potentials as four independent funnel-shift chains (bit i = neuron i)
 __device__ __forceinline__ uint32_t sign32(const uint32_t (&v)[32]) {
   uint32_t a = 0, b = 0, c = 0, d = 0;
@@ -382,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     mbar_init(&S.acc2_free, 8);
     for (int i = 0; i < kNkb2; i++) mbar_init(&S.h1_kb[i], 8);
     for (int i = 0; i < kNkb2; i++) mbar_init(&S.h2_kb[i], 8);
-    S.base_g = S.base_e = -1;
+    S.base_e = -1;
     fence_mbar_init();
   }
   if (warp == kWIss) { tmem_alloc2(&S.tbase, 512); tmem_relinquish2(); }
@@ -450,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       // depends on E1 and so on this tile's own layer-1 MMAs).  The whole warp runs the loop
       // (warp-uniform descriptors in uniform registers); one elected lane issues.
       const bool el = elect_one();
-      const uint32_t id1 = idesc_f16(256, kN1, 1, 1);     // bf16 x bf16 -> f32
+      const uint32_t id1 = idesc_f16(256, kN1, 0, 0);     // f16 levels x f16 W1 -> f32
       const uint32_t id2 = idesc_f16(256, kN2, 0, 0);     // f16 x f16 -> f32
       uint32_t gslot = 0, gph = 0, wslot = 0, wph = 0;    // ring position of the next stage
       int pend_g = -1, pend_w = -1;                       // slots of the previous stage, not yet committed
@@ -594,96 +586,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   } else {
     // ------------------------------------------------------------------ generator (both CTAs)
     // Three groups of four warps take the ring stages in turn; a warp generates a whole 64-pixel K
-    // block of its 32 rows (two Philox calls) into registers before it waits for the slot.
+    // block of its 32 rows (two Philox calls) into registers before it waits for the slot.  The A
+    // operand is the level l of every pixel (reading C14b: x' = x + origin + l * step, linear in l);
+    // the base image enters through base1 in the epilogue.
     const int gw = gen_index(warp), grp = gw >> 2;
     const int r = 32 * (gw & 3) + lane;                    // row of this CTA's A tile
     const int gt = 32 * gw + lane;                         // 0..383
-    uint32_t gs = 0, tl = 0, gm = 0;                       // gm = gs mod kNGenGroups
+    uint32_t tl = 0;
     const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
-    const uint32_t stepS2 = a.stepS2, org2 = a.org2;
-    const int n0 = a.n0;
+    const int nblk = (a.n0 + 31) / 32;                     // Philox blocks holding pixels
     const int kneed = 16 * a.nk16;                         // K elements the MMA reads
     for (uint64_t t = t_begin; t < t_end; t++, tl++) {
       if (gt == 0) TR(tl, 6);
       const TileInfo ti = tile_info(a, t);
-      if (ti.b != S.base_g) {                              // stage the base image (bf16) once per base
-        named_bar(1, 32 * 4 * kNGenGroups);
-        for (int i = gt; i < a.nkb1 * 64; i += 32 * 4 * kNGenGroups) S.xg[i] = i < n0 ? a.bases[(size_t)ti.b * n0 + i] : (uint16_t)0;
-        named_bar(1, 32 * 4 * kNGenGroups);
-        if (gt == 0) S.base_g = ti.b;
-      }
       const int grow = 128 * (int)rank + r;
       uint64_t c;
       if (a.eval_idx) c = grow < ti.nvalid ? a.eval_idx[ti.start + grow] : 0;
       else c = ti.start + (uint64_t)grow;
       const uint32_t c0 = (uint32_t)c, c1 = (uint32_t)(c >> 32), cb = (uint32_t)ti.b;
-      for (int kb = 0; kb < a.nkb1; kb++, gs++, gm = gm + 1 == kNGenGroups ? 0 : gm + 1) {
-        if (gm != (uint32_t)grp) continue;
+      const uint32_t gs0 = tl * (uint32_t)a.nkb1;          // global index of this tile's first stage
+      for (int kb = (int)((grp + kNGenGroups - gs0 % kNGenGroups) % kNGenGroups); kb < a.nkb1; kb += kNGenGroups) {
+        const uint32_t gs = gs0 + kb;
         TRG(tl, kb, 0);
-#if MLPV_EXP == 4 || MLPV_EXP == 13 || !EXP_ON(EXPB_GENC)
         uint4 out[8];
-        const int e0 = 64 * kb;
-#pragma unroll
-        for (int ch = 0; ch < 8; ch++) out[ch] = make_uint4(c0, 0, 0, 0);
-#else
-        uint4 out[8];
-        const int e0 = 64 * kb;
-        if (e0 + 64 <= n0) {
-          const uint4 w0 = philox(c0, c1, cb, (uint32_t)(2 * kb), k0, k1);
-          const uint4 w1 = philox(c0, c1, cb, (uint32_t)(2 * kb + 1), k0, k1);
-          const uint4* xv = reinterpret_cast<const uint4*>(S.xg + e0);
-          out[0] = lattice_word(w0.x, xv[0], stepS2, org2);
-          out[1] = lattice_word(w0.y, xv[1], stepS2, org2);
-          out[2] = lattice_word(w0.z, xv[2], stepS2, org2);
-          out[3] = lattice_word(w0.w, xv[3], stepS2, org2);
-          out[4] = lattice_word(w1.x, xv[4], stepS2, org2);
-          out[5] = lattice_word(w1.y, xv[5], stepS2, org2);
-          out[6] = lattice_word(w1.z, xv[6], stepS2, org2);
-          out[7] = lattice_word(w1.w, xv[7], stepS2, org2);
-        } else {
-          // tail block: remaining pixels, then the bias columns (1.0) at K = n0 .. n0+2, then zeros
-#pragma unroll
-          for (int hh = 0; hh < 2; hh++) {
-            const int eh = e0 + 32 * hh;
-            uint4 w = make_uint4(0, 0, 0, 0);
-            if (eh < n0) w = philox(c0, c1, cb, (uint32_t)(2 * kb + hh), k0, k1);
-            const uint4* xv = reinterpret_cast<const uint4*>(S.xg + eh);
-            const uint32_t wsr[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int ww = 0; ww < 4; ww++) {
-              const uint4 y = lattice_word(wsr[ww], xv[ww], stepS2, org2);
-              uint32_t ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-              for (int k = 0; k < 4; k++) {
-                const int e = eh + 8 * ww + 2 * k;        // K index of the low element
-                uint32_t lo = ys[k] & 0xFFFFu, hi = ys[k] >> 16;
-                if (e >= n0) lo = (e < n0 + 3) ? 0x3F80u : 0u;
-                if (e + 1 >= n0) hi = (e + 1 < n0 + 3) ? 0x3F80u : 0u;
-                ys[k] = lo | (hi << 16);
-              }
-              out[4 * hh + ww] = make_uint4(ys[0], ys[1], ys[2], ys[3]);
-            }
-          }
+        {
+          const int j = 2 * kb;
+          const uint4 z = make_uint4(0, 0, 0, 0);
+          const uint4 w0 = j < nblk ? philox(c0, c1, cb, (uint32_t)j, k0, k1) : z;
+          const uint4 w1 = j + 1 < nblk ? philox(c0, c1, cb, (uint32_t)(j + 1), k0, k1) : z;
+          out[0] = nibble_word(w0.x); out[1] = nibble_word(w0.y);
+          out[2] = nibble_word(w0.z); out[3] = nibble_word(w0.w);
+          out[4] = nibble_word(w1.x); out[5] = nibble_word(w1.y);
+          out[6] = nibble_word(w1.z); out[7] = nibble_word(w1.w);
         }
-#endif
         const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
         TRG(tl, kb, 1);
         if ((gw & 3) == 0) mbar_wait_sleep(&S.g_empty[st], ph ^ 1u, 128);   // one poller per group
         named_bar(6 + grp, 128);
         TRG(tl, kb, 2);
         uint8_t* slot = sG + st * kTile;
-#if MLPV_EXP != 1 && MLPV_EXP != 6 && MLPV_EXP != 13 && EXP_ON(EXPB_GENS)
+        const int e0 = 64 * kb;
 #pragma unroll
         for (int ch = 0; ch < 8; ch++)
           if (kneed > e0 + 8 * ch)                           // only the K steps the MMA reads
             *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = out[ch];
-#else
-        if (out[0].x == 0x12345678u && out[7].w == 0x9abcdefu) *reinterpret_cast<uint4*>(slot) = out[1];
-#endif
         fence_proxy_async();
         __syncwarp();
         TRG(tl, kb, 3);
-        if (lane == 0 && (MLPV_EXP != 11 || rank == 0)) arrive_leader(&S.g_full[st], rank);
+        if (lane == 0) arrive_leader(&S.g_full[st], rank);
         TRG(tl, kb, 4);
       }
       if (gt == 0) TR(tl, 7);
@@ -706,6 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const float tau2 = a.cov.tau_dev ? a.cov.tau_dev[2] : a.cov.tau[2];
     const bool eval = a.eval_idx != nullptr;
     const bool need12 = a.pair12 >= 0 && !eval, need23 = a.pair23 >= 0 && !eval;
+    const float stepS = a.stepS;
     uint32_t tl = 0;
     for (uint64_t t = t_begin; t < t_end; t++, tl++) {
       const TileInfo ti = tile_info(a, t);
@@ -715,7 +666,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       if (ti.b != S.base_e) {                              // stage the base traces once per base input
         named_bar(2, 256);
         const float* tr = a.trace + (size_t)ti.b * a.T;
-        for (int i = et; i < kN1; i += 256) S.ub1[i] = tr[i];
+        for (int i = et; i < kN1; i += 256) {
+          S.ub1[i] = tr[i];
+          S.b1[i] = a.base1[(size_t)ti.b * kN1 + i];
+        }
         for (int i = et; i < kN2; i += 256) S.ub2[i] = tr[kN1 + i];
         if (et < kN3P) {
           S.ub3[et] = et < a.n3 ? tr[kN1 + kN2 + et] : 0.f;
@@ -767,6 +721,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         tmem_ld32(R1 + loff + 32u * p, va);
         tmem_ld32(R1 + loff + 32u * p + 32u, vb);
         tmem_ld_wait();
+        acc_to_u1(va, S.b1 + 32 * p, stepS);
+        acc_to_u1(vb, S.b1 + 32 * p + 32, stepS);
         const uint32_t sa = sign32(va) ^ S.nb1[p], sb = sign32(vb) ^ S.nb1[p + 1];
         nsc1 += __popc(sa) + __popc(sb);
         if (istar1 < 0 && sa) istar1 = 32 * p + __ffs(sa) - 1;
@@ -796,6 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           const int g = g0 + i;
           uint32_t (&v)[16] = vbuf[i & 1];
           if (i < 7) tmem_ld16(R1 + loff + 16u * (g + 1), vbuf[(i + 1) & 1]);
+          acc_to_u1(v, S.b1 + 16 * g, stepS);
           if (slow1) {
             const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 16 * g);
             float uu[16], d[16];
@@ -1076,23 +1033,11 @@ extern "C" int mlpv_f3_trace_gen_read(void* host) {
 // ------------------------------------------------------------------------------------------- host
 bool fused3_applicable(const DevNet& net) {
   return net.numeric == MLPV_NUM_BF16 && net.L == 3 && net.sizes[1] == f3::kN1 && net.sizes[2] == f3::kN2 &&
-         net.sizes[3] <= f3::kN3P && net.sizes[0] % 2 == 0 && net.sizes[0] + 3 <= f3::kMaxN0;
-}
-
-static uint16_t f2bf(float f);
-// the lattice trick needs step * 2^130 as a normal bf16: |step| normal with exponent field <= 124
-bool fused3_pert_ok(const DevPert& pert) {
-  const uint32_t e = (f2bf(pert.step_f) >> 7) & 0xFFu;
-  return e >= 1 && e <= 124;
+         net.sizes[3] <= f3::kN3P && net.sizes[0] % 2 == 0 && net.sizes[0] <= f3::kMaxN0;
 }
 
 static size_t sw128_h(uint32_t row, uint32_t byte) {
   return (row >> 3) * 1024u + (row & 7u) * 128u + ((((byte >> 4) ^ row) & 7u) << 4) + (byte & 15u);
-}
-static uint16_t f2bf(float f) {
-  uint32_t u;
-  memcpy(&u, &f, 4);
-  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
 }
 static float bf2f(uint16_t b) {
   const uint32_t u = (uint32_t)b << 16;
@@ -1125,7 +1070,6 @@ cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const v
   const uint16_t* W1 = static_cast<const uint16_t*>(W_host[0]);
   const uint16_t* W2 = static_cast<const uint16_t*>(W_host[1]);
   const uint16_t* W3 = static_cast<const uint16_t*>(W_host[2]);
-  const float* b1 = static_cast<const float*>(b_host[0]);
   const float* b2 = static_cast<const float*>(b_host[1]);
   auto put16 = [&](uint8_t* tile, int row, int kelem, uint16_t v) {
     const size_t o = sw128_h((uint32_t)row, (uint32_t)(2 * (kelem % 64)));
@@ -1136,19 +1080,10 @@ cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const v
   for (int rk = 0; rk < 2; rk++) {
     for (int rr = 0; rr < 128; rr++) {
       const int n = 128 * rk + rr;
-      for (int k = 0; k < n0 + 3; k++) {
-        uint16_t v;
-        if (k < n0) v = W1[(size_t)n * n0 + k];
-        else {
-          const float b = b1[n];
-          const uint16_t p1 = f2bf(b);
-          const float r1 = b - bf2f(p1);
-          const uint16_t p2 = f2bf(r1);
-          const float r2 = r1 - bf2f(p2);
-          v = k == n0 ? p1 : (k == n0 + 1 ? p2 : f2bf(r2));
-        }
-        put16(st + ((size_t)rk * L.nst + k / 64) * f3::kTile, rr, k, v);
-      }
+      // W1 in fp16 (the A operand holds fp16 levels): exact for |w| >= 2^-17, the smaller weights
+      // round with absolute error <= 2^-25 (reading C19); K beyond n0 stays zero
+      for (int k = 0; k < n0; k++)
+        put16(st + ((size_t)rk * L.nst + k / 64) * f3::kTile, rr, k, f2h(bf2f(W1[(size_t)n * n0 + k])));
       for (int k = 0; k < f3::kN1; k++) {
         const uint16_t h = f2h(bf2f(W2[(size_t)n * f3::kN1 + k]));      // exact for |w| >= 2^-17
         put16(st + ((size_t)rk * L.nst + L.nkb1 + k / 64) * f3::kTile, rr, k, h);
@@ -1209,12 +1144,8 @@ cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases,
     if (cov.lower[p] == 2) a.pair23 = p;
   }
   a.eval_idx = eval_idx; a.eval_n = eval_n; a.eval_base = eval_base; a.eval_out = static_cast<float*>(eval_out);
-  {
-    const uint16_t sb = f2bf(pert.step_f), ob = f2bf(pert.origin_f);
-    const uint16_t sS = (uint16_t)(sb + (130u << 7));   // step * 2^130 (exponent field + 130)
-    a.stepS2 = (uint32_t)sS | ((uint32_t)sS << 16);
-    a.org2 = (uint32_t)ob | ((uint32_t)ob << 16);
-  }
+  a.stepS = (float)(pert.step_d * 16777216.0);         // step * 2^24 (the levels are l * 2^-24)
+  a.base1 = ws.base1;
   if (eval_idx) {
     a.tiles_per_base = (uint64_t)((eval_n + 255) / 256);
     a.n_pairs_tiles = a.tiles_per_base;

@@ -597,14 +597,13 @@ static size_t sw128_host(uint32_t row, uint32_t byte) {
 }
 
 bool fused3_applicable(const DevNet& net);
-bool fused3_pert_ok(const DevPert& pert);
 cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const void* const* b_host, void** blk_dev);
 cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases, int n_base, const DevPert& pert,
                           const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
                           const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
                           cudaStream_t st);
 
-static bool use_fused3(const DevNet& net) {
+static bool use_fused3(const DevNet& net) {     // MLPV_NO_FUSED3=1: debugging only (box -> unsupported)
   const char* env = getenv("MLPV_NO_FUSED3");
   return fused3_applicable(net) && !(env && env[0] == '1');
 }
@@ -666,7 +665,12 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* b
                          const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
                          cudaStream_t st, bool* supported, std::string* why) {
-  if (use_fused3(net) && Wt[1] && fused3_pert_ok(pert)) {
+  if (pert.kind == MLPV_PERT_PHILOX_BOX) {              // the exact box is built on the fused path only
+    if (!(use_fused3(net) && Wt[1])) {
+      *supported = false;
+      *why = "PHILOX_BOX is built for 3-layer BF16 nets with 256-wide hidden layers (k_fused3)";
+      return cudaSuccess;
+    }
     *supported = true;
     return launch_fused3(net, Wt[1], bases, n_base, pert, prop, cov, res, ws, eval_idx, eval_n, eval_base,
                          eval_out, num_sms, st);

@@ -92,6 +92,15 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
     else hf[j] = in_f(x, net.numeric, j);
   }
   __syncthreads();
+  if (ws.base1 != nullptr) {                        // PHILOX_BOX: W1 x + b1 + origin W1 1 (fp64 sum)
+    const int n1 = net.sizes[1];
+    for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+      double acc = (double)static_cast<const float*>(net.b[0])[i];
+      for (int j = 0; j < n0; j++)
+        acc += (double)wload_f(net.W[0], net.numeric, (size_t)i * n0 + j) * ((double)hf[j] + pert.origin_d);
+      ws.base1[(size_t)b * n1 + i] = (float)acc;
+    }
+  }
   const int T = net.trace_len;
   for (int l = 1; l <= net.L; l++) {
     const int nl = net.sizes[l], fan = net.sizes[l - 1];

@@ -315,10 +315,22 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
       }
       dp->seed = p->seed;
       break;
+    case MLPV_PERT_PHILOX_BOX:
+      if (num != MLPV_NUM_BF16) return fail(h, MLPV_E_UNSUPPORTED, "PHILOX_BOX is built for BF16 nets");
+      if (p->n_samples < 1 || p->n_samples > (1ull << 32)) return fail(h, MLPV_E_INVALID, "pert.n_samples = %llu (1..2^32)", (unsigned long long)p->n_samples);
+      if (!std::isfinite(p->lattice_step) || !std::isfinite(p->lattice_origin) || std::fabs(p->lattice_step) > 1.0 ||
+          std::fabs(p->lattice_origin) > 1.0)
+        return fail(h, MLPV_E_INVALID, "pert.lattice_step / lattice_origin must be finite, |.| <= 1");
+      dp->step_f = (float)p->lattice_step;
+      dp->origin_f = (float)p->lattice_origin;
+      dp->step_d = p->lattice_step;
+      dp->origin_d = p->lattice_origin;
+      dp->seed = p->seed;
+      break;
     default:
       return fail(h, MLPV_E_INVALID, "pert.kind = %d", (int)p->kind);
   }
-  if (p->kind != MLPV_PERT_PHILOX_LATTICE) {
+  if (p->kind != MLPV_PERT_PHILOX_LATTICE && p->kind != MLPV_PERT_PHILOX_BOX) {
     if (p->n_levels < 1 || p->n_levels > 256) return fail(h, MLPV_E_INVALID, "pert.n_levels = %d (1..256)", p->n_levels);
     if (!p->levels) return fail(h, MLPV_E_INVALID, "pert.levels is NULL");
     for (int q = 0; q < p->n_levels; q++) {
@@ -391,13 +403,15 @@ static mlpv_status prepare(mlpv_ctx* h, const void* bases, int n_base, const mlp
                            DevCov* dc, Plan* plan, cudaStream_t st, bool need_tau) {
   const DevNet& n = h->net;
   const int T = n.trace_len;
-  const bool subset = pert->kind != MLPV_PERT_PHILOX_LATTICE;
+  const bool subset = pert->kind != MLPV_PERT_PHILOX_LATTICE && pert->kind != MLPV_PERT_PHILOX_BOX;
+  const bool box = pert->kind == MLPV_PERT_PHILOX_BOX;
   const int S = pert->kind == MLPV_PERT_TUPLE_REPLACE ? n.sizes[0] : pert->n_pixels;
   const size_t delta_bytes = subset ? 4ull * n_base * S * dp.n_levels * n.sizes[1] : 0;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t o_trace = 0, o_cls = al(4ull * n_base * T), o_tau = o_cls + al(4ull * n_base);
   const size_t o_delta = o_tau + al(4 * kMaxL), o_pix = o_delta + al(delta_bytes);
-  const size_t o_lv = o_pix + al(4 * 64), total = o_lv + al(4 * 256);
+  const size_t o_lv = o_pix + al(4 * 64), o_b1 = o_lv + al(4 * 256);
+  const size_t total = o_b1 + (box ? al(4ull * n_base * n.sizes[1]) : 0);
   mlpv_status s = ensure_ws(h, total);
   if (s != MLPV_OK) return s;
   char* w = static_cast<char*>(h->ws);
@@ -405,6 +419,7 @@ static mlpv_status prepare(mlpv_ctx* h, const void* bases, int n_base, const mlp
   plan->ws.cls = reinterpret_cast<int32_t*>(w + o_cls);
   plan->ws.delta = subset ? w + o_delta : nullptr;
   plan->ws.S = S;
+  plan->ws.base1 = box ? reinterpret_cast<float*>(w + o_b1) : nullptr;
   plan->tau_dev = reinterpret_cast<float*>(w + o_tau);
   plan->pixels_dev = reinterpret_cast<int32_t*>(w + o_pix);
   plan->levels_dev = w + o_lv;
@@ -437,7 +452,7 @@ static mlpv_status run_kernel(mlpv_ctx* h, const void* bases, int n_base, const 
   bool supported = false;
   cudaError_t e;
   if (h->ev_begin) CUDA_TRY(h, cudaEventRecord(h->ev_begin, st), "profile event");
-  if (pert->kind == MLPV_PERT_PHILOX_LATTICE) {
+  if (pert->kind == MLPV_PERT_PHILOX_LATTICE || pert->kind == MLPV_PERT_PHILOX_BOX) {
     if (!h->large_ready) return fail(h, MLPV_E_UNSUPPORTED, "large-net path unavailable for this net: %s", h->large_why.c_str());
     std::string why;
     e = launch_large(h->net, h->Wt, bases, n_base, dp, dprop, dc, dr, plan.ws, eval_idx, eval_n, eval_base, eval_out,
@@ -604,6 +619,20 @@ extern "C" mlpv_status mlpv_decode(mlpv_numeric numeric, const mlpv_pert* p, con
     return MLPV_OK;
   }
   const uint32_t k0 = (uint32_t)p->seed, k1 = (uint32_t)(p->seed >> 32);
+  if (p->kind == MLPV_PERT_PHILOX_BOX) {        // exact real candidate, written as doubles
+    double* o = static_cast<double*>(out);
+    for (int j = 0; j < n0; j++) o[j] = get(base, j);
+    for (int j = 0; j < (n0 + 31) / 32; j++) {
+      uint32_t w[4] = {(uint32_t)index, (uint32_t)(index >> 32), (uint32_t)base_id, (uint32_t)j};
+      philox_host(w, k0, k1);
+      for (int ww = 0; ww < 4; ww++)
+        for (int nb = 0; nb < 8; nb++) {
+          const int px = 32 * j + 8 * ww + nb;
+          if (px < n0) o[px] += p->lattice_origin + (double)((w[ww] >> (4 * nb)) & 15) * p->lattice_step;
+        }
+    }
+    return MLPV_OK;
+  }
   for (int j = 0; j < (n0 + 31) / 32; j++) {
     uint32_t w[4] = {(uint32_t)index, (uint32_t)(index >> 32), (uint32_t)base_id, (uint32_t)j};
     philox_host(w, k0, k1);

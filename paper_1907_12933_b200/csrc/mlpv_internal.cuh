@@ -48,7 +48,8 @@ struct DevPert {
   const int32_t* pixels;      // device [n_pixels]
   uint64_t begin, end;        // index range
   uint64_t seed;
-  float step_f, origin_f;     // PHILOX (BF16 values)
+  float step_f, origin_f;     // PHILOX (BF16 values) / PHILOX_BOX (fp32 of the doubles)
+  double step_d, origin_d;    // PHILOX_BOX
   int step_i, origin_i;       // PHILOX (INT8)
   uint64_t q2;                // TUPLE: q^2
 };
@@ -64,6 +65,7 @@ struct BaseWS {
   int32_t* cls;               // [n_base] base class
   void* delta;                // [n_base x S x q x n_1] layer-1 delta tables (subset/tuple spaces)
   int S;                      // slots per base: n_0 (TUPLE) or K (SUBSET)
+  float* base1;               // PHILOX_BOX: [n_base x n_1] W1 x + b1 + origin W1 1 (fp64 sum, fp32)
 };
 
 // Launchers (kernels in k_small.cu / k_large.cu / k_util.cu)

@@ -418,7 +418,9 @@ def test_philox_lattice_values_and_uniformity(oracle_mod):
     torch = pytest.importorskip("torch")
     O = oracle_mod
     cfg = M.make_config("cfg4")
-    s, c = cfg.pert.lattice_step, cfg.pert.lattice_origin
+    s = float(M.bf16_bits_to_f32(M.f32_to_bf16_bits(np.float32(0.1 / 15.0)))[()])
+    c = float(M.bf16_bits_to_f32(M.f32_to_bf16_bits(np.float32(-0.05)))[()])
+    cfg.pert = Pert(M.PERT_PHILOX_LATTICE, seed=cfg.pert.seed, n_samples=2 ** 32, lattice_step=s, lattice_origin=c)
     offs = torch.tensor([l * s + c for l in range(16)], dtype=torch.float32).to(torch.bfloat16).to(torch.float32).numpy()
     # base pixels that are multiples of 2^-8 keep x + off exact in fp32
     x = (np.arange(784) % 257 / 256.0).astype(np.float32)
@@ -445,6 +447,44 @@ def test_philox_lattice_values_and_uniformity(oracle_mod):
     inner = (xb >= 8) & (xb <= 248)
     assert np.all((d[inner] >= -8) & (d[inner] <= 7))
     assert np.all((y >= 0) & (y <= 255))
+
+
+def test_philox_box_values_and_linearity(oracle_mod):
+    """PHILOX_BOX (reading C14b): every pixel moves by exactly origin + l*step for a level l in
+    0..15 (the same levels as PHILOX_LATTICE: pixels away from the clamp bounds pick the same l
+    in both spaces), |x' - x| <= eps, levels uniform (chi^2), and the layer-1 potentials of a
+    candidate equal W1 x' + b1 by numpy's float64 matmul (library routine)."""
+    O = oracle_mod
+    cfg = M.make_config("cfg4")
+    p = cfg.pert
+    assert p.kind == M.PERT_PHILOX_BOX
+    step, org = p.lattice_step, p.lattice_origin
+    xb = cfg.bases[3]
+    xv = M.bf16_bits_to_f32(xb).astype(np.float64)
+    lat = Pert(M.PERT_PHILOX_LATTICE, seed=p.seed, n_samples=p.n_samples,
+               lattice_step=float(M.bf16_bits_to_f32(M.f32_to_bf16_bits(np.float32(step)))[()]),
+               lattice_origin=float(M.bf16_bits_to_f32(M.f32_to_bf16_bits(np.float32(org)))[()]))
+    counts = np.zeros(16)
+    W1 = M.bf16_bits_to_f32(cfg.net.W[0]).astype(np.float64)
+    b1 = np.asarray(cfg.net.b[0], np.float64)
+    for idx in (0, 1, 77, 2 ** 31 + 5, 2 ** 32 - 1):
+        y = O.decode(cfg.net.numeric, p, xb, 3, idx)
+        assert y.dtype == np.float64
+        lv = (y - xv - org) / step
+        li = np.rint(lv)
+        assert np.all(np.abs(lv - li) < 1e-9) and li.min() >= 0 and li.max() <= 15
+        assert np.max(np.abs(y - xv)) <= 0.05 + 1e-12
+        counts += np.bincount(li.astype(int), minlength=16)
+        # same levels as the clamped lattice where no clamping can happen
+        yl = M.bf16_bits_to_f32(O.decode(cfg.net.numeric, lat, xb, 3, idx)).astype(np.float64)
+        mid = (xv > 0.06) & (xv < 0.94)
+        ol = np.array([float(M.bf16_bits_to_f32(M.f32_to_bf16_bits(np.float32(l * lat.lattice_step + lat.lattice_origin)))[()]) for l in range(16)])
+        cand = M.bf16_bits_to_f32(M.f32_to_bf16_bits((xv[:, None] + ol[None, :]).astype(np.float32))).astype(np.float64)
+        assert np.all(cand[mid, li[mid].astype(int)] == yl[mid])
+        u1 = O.forward(cfg.net, y)[0]
+        assert np.allclose(u1, W1 @ y + b1, rtol=1e-12, atol=1e-12)
+    e = counts.sum() / 16
+    assert float(np.sum((counts - e) ** 2 / e)) < 50.0
 
 
 def test_philox_is_counter_sensitive(oracle_mod):
