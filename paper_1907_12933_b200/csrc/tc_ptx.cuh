@@ -309,6 +309,38 @@ __device__ __forceinline__ void mma2_f16_ts(uint32_t d, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// The same MMA with both SWIZZLE_128B K-major descriptors given by their low words (start address
+// >> 4 | LBO 1, see sdesc_sw128) and the constant high word: the hot issue loops then add immediates
+// to two 32-bit values instead of rebuilding 64-bit descriptors per MMA.
+constexpr uint32_t kSw128Hi = (1024u >> 4) | (1u << 14) | (2u << 29);
+__device__ __forceinline__ uint32_t sdesc_sw128_lo(uint32_t saddr) { return ((saddr & 0x3FFFFu) >> 4) | (1u << 16); }
+__device__ __forceinline__ void mma2_f16_ss_lo(uint32_t d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; .reg .b64 da, db; setp.ne.b32 p, %4, 0;\n"
+      "mov.b64 da, {%1, %5}; mov.b64 db, {%2, %5};\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %3, p; }" ::"r"(d),
+      "r"(alo), "r"(blo), "r"(idesc), "r"(acc), "n"(kSw128Hi)
+      : "memory");
+}
+// non-blocking phase test: its result arrives asynchronously, so a test issued early and consumed
+// later hides the SYNCS round trip behind the instructions in between
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// two barriers polled together (their try_wait latencies overlap)
+__device__ __forceinline__ void mbar_wait2(uint64_t* b1, uint32_t ph1, uint64_t* b2, uint32_t ph2) {
+  bool d1 = false, d2 = false;
+  do {
+    if (!d1) d1 = mbar_try(b1, ph1);
+    if (!d2) d2 = mbar_try(b2, ph2);
+  } while (!(d1 && d2));
+}
 // one lane of a converged warp (the MMA-issuing warps run their loops warp-uniformly so that
 // descriptors live in uniform registers; only the elected lane issues)
 __device__ __forceinline__ bool elect_one() {

@@ -21,7 +21,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
   uint8_t* sA = smem;                 // 4 x 16 KB
   uint8_t* sB = smem + 4 * 16384;     // 4 x 16 KB
   for (int i = t; i < 8 * 16384 / 16; i += blockDim.x) {
-    if (MODE >= 7) {                                   // random bf16 in [-1, 1) / [0, 1)
+    if (MODE == 20) {                                  // A: fp16 subnormal levels 0..15, B: random fp16 |x| < 0.125
+      uint32_t x = (uint32_t)(i * 2654435761u) ^ (rank * 97u) ^ 0x9e3779b9u;
+      uint32_t v[4];
+      for (int k = 0; k < 4; k++) {
+        x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+        if (i < 4 * 16384 / 16) v[k] = (x & 0xFu) | (((x >> 8) & 0xFu) << 16);
+        else v[k] = (0x2c00u | (x & 0x3ffu) | ((x >> 2) & 0x8000u)) | ((0x2c00u | ((x >> 16) & 0x3ffu) | ((x << 14) & 0x80000000u)) & 0xffff0000u) ;
+      }
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(v[0], v[1], v[2], v[3]);
+    } else if (MODE >= 7) {                            // random bf16 in [-1, 1) / [0, 1)
       uint32_t x = (uint32_t)(i * 2654435761u) ^ (rank * 97u);
       uint32_t v[4];
       for (int k = 0; k < 4; k++) {
@@ -46,7 +55,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
   const uint32_t tb = tbase;
   if (t == 0) { if (rank == 0 || MODE == 3) mbar_arrive(&ready); else mbar_arrive_cluster(&ready, 0); }
   if (t == 0) mbar_arrive(&pre);                       // phase 0 of `pre` completes: waits on it are no-ops
-  const bool issuer = (MODE == 3) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15);
+  const bool issuer = (MODE == 3) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15 && MODE != 25);
   __shared__ volatile int stop;
   if (t == 0) stop = 0;
   __syncthreads();
@@ -69,6 +78,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
       __nanosleep(400);
     }
     if (el && blockIdx.x == 0) printf("  L3-like batches issued: %llu\n", n);
+  } else if ((MODE == 24 || MODE == 25) && w >= 4 && w < 12) {
+    // epilogue-like: 8 warps (two per lane quadrant), per 16-column group: prefetch ld16 of the next
+    // group, ~40 ALU ops, st16 in place, wait::ld
+    const uint32_t loff = (uint32_t)(32 * (w & 3)) << 16;
+    const uint32_t cb = 256u + 128u * (uint32_t)((w - 4) >> 2);
+    unsigned long long n = 0;
+    uint32_t buf[2][16];
+    long long tst = 0, tld = 0;
+    tmem_ld16(tbase + loff + cb, buf[0]);
+    tmem_ld_wait();
+    const long long t0 = clock64();
+    while (!stop) {
+#pragma unroll 2
+      for (int g = 0; g < 8; g++) {
+        uint32_t (&v)[16] = buf[g & 1];
+        tmem_ld16(tbase + loff + cb + 16 * ((g + 1) & 7), buf[(g + 1) & 1]);
+        uint32_t hl[16];
+#pragma unroll
+        for (int k = 0; k < 16; k++) hl[k] = (v[k] * 2654435761u) ^ (v[(k + 3) & 15] >> 3);
+        const long long a0 = clock64();
+        tmem_st16(tbase + loff + cb + 16 * g, hl);
+        const long long a1 = clock64();
+        tmem_ld_wait();
+        const long long a2 = clock64();
+        tst += a1 - a0; tld += a2 - a1;
+      }
+      tmem_st_wait();
+      n += 8;
+      if (MODE == 25 && n >= 8 * 4000) break;
+    }
+    const long long t1 = clock64();
+    if ((t & 31) == 0 && (w == 4 || w == 7) && blockIdx.x == 0)
+      printf("  w%d: %.1f cycles per group, st16 issue %.1f, ld wait %.1f\n", w, (double)(t1 - t0) / n, (double)tst / n, (double)tld / n);
   } else if (MODE == 18 && w >= 4 && w < 8) {
     const uint32_t loff = (uint32_t)(32 * (w & 3)) << 16;
     unsigned long long n = 0;
@@ -138,9 +180,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
     if (MODE != 3) mbar_wait_cluster(&ready, 0); else mbar_wait(&ready, 0);
     fence_after();
     const uint32_t N = MODE == 2 ? 128 : 256;
-    const uint32_t idesc = MODE == 3 ? idesc_f16(128, N, 1, 1) : idesc_f16(256, N, 1, 1);
+    const uint32_t idesc = MODE == 3 ? idesc_f16(128, N, 1, 1) : (MODE == 20 ? idesc_f16(256, N, 0, 0) : idesc_f16(256, N, 1, 1));
     long long t0 = clock64();
-    if (MODE == 13) {                                    // k_fused3's rings: A 6 x 16 KB, B 5 x 16 KB
+    if (MODE == 21 || MODE == 22 || MODE == 23) {      // rings + per-stage readiness checks (k_fused3 issuer)
+      uint32_t gsl = 0, wsl = 0;
+      const bool el = true;
+      for (int r = 0; r < reps / 4; r++)
+        for (int kb = 0; kb < 13; kb++) {
+          const uint32_t ab = smem_u32(smem + gsl * 16384), bb = smem_u32(smem + 6 * 16384 + wsl * 16384);
+          if (++gsl == 6) gsl = 0;
+          if (++wsl == 5) wsl = 0;
+          const bool rdy = MODE == 21 ? (mbar_test(&pre, 0) & mbar_test(&pre, 0)) : true;
+          mma2_f16_ss(tb, sdesc_sw128(ab), sdesc_sw128(bb), idesc, (kb | r) ? 1u : 0u);
+          mma2_commit(&scratch[0], 0x3);
+          mma2_commit(&scratch[1], 0x3);
+          mma2_f16_ss(tb, sdesc_sw128(ab + 32u), sdesc_sw128(bb + 32u), idesc, 1u);
+          if (MODE == 22) mbar_wait2(&pre, 0, &pre, 0);
+          if (MODE == 23) { mbar_wait(&pre, 0); mbar_wait(&pre, 0); }
+          mma2_f16_ss(tb, sdesc_sw128(ab + 64u), sdesc_sw128(bb + 64u), idesc, 1u);
+          mma2_f16_ss(tb, sdesc_sw128(ab + 96u), sdesc_sw128(bb + 96u), idesc, 1u);
+          if (MODE == 21 && !rdy) mbar_wait2(&pre, 0, &pre, 0);
+        }
+    } else if (MODE == 13) {                             // k_fused3's rings: A 6 x 16 KB, B 5 x 16 KB
       uint32_t gsl = 0, wsl = 0;
       for (int r = 0; r < reps / 4; r++)
         for (int kb = 0; kb < 13; kb++) {
@@ -163,7 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
           const uint64_t ad = sdesc_sw128(smem_u32(sA + kb * 16384 + kk * 32));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + kb * 16384 + kk * 32));
           const uint32_t acc = (r | kb | kk) ? 1u : 0u;
-          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16) || MODE == 18 || MODE == 19) mma2_f16_ss(tb, ad, bd, idesc, acc);
+          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16) || MODE == 18 || MODE == 19 || MODE == 20 || MODE == 24) mma2_f16_ss(tb, ad, bd, idesc, acc);
           else if (MODE == 1) mma2_f16_ts(tb, tb + 256 + kb * 32 + kk * 8, bd, idesc, acc);
           else if (MODE == 16 || MODE == 17) mma2_f16_ts(tb + 256, tb + kb * 32 + kk * 8, bd, idesc_f16(256, 128, 1, 1), acc);
           else mma1_ss(tb, ad, bd, idesc, acc);
@@ -180,7 +241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
   }
   if (MODE != 3) { if (t < 32 && !issuer) {} }
   __syncwarp();
-  if (!issuer && t == 0 && MODE != 3 && MODE != 15) { mbar_wait(&done, 0); stop = 1; }
+  if (!issuer && t == 0 && MODE != 3 && MODE != 15 && MODE != 25) { mbar_wait(&done, 0); stop = 1; }
   fence_before();
   __syncthreads();
   cluster_sync();
@@ -190,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
 
 template <int MODE>
 void run(const char* name) {
-  const size_t smem = (MODE == 13 ? 13 : 10) * 16384 + 1024;
+  const size_t smem = (MODE == 13 || MODE >= 21 ? 13 : 10) * 16384 + 1024;
   cudaFuncSetAttribute(k_bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   unsigned long long* cyc;
   cudaMalloc(&cyc, 8);
@@ -209,15 +270,20 @@ void run(const char* name) {
   cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
   const double M = MODE == 3 ? 128 : 256, N = MODE == 2 ? 128 : 256;
   const double groups = MODE == 3 ? 148 : 74;
-  const double flops = MODE == 13 ? 2.0 * M * N * 16 * 50 * (reps / 4) * groups : 2.0 * M * N * 16 * 16 * reps * groups;
+  const double flops = (MODE == 13 || MODE >= 21) ? 2.0 * M * N * 16 * 52 * (reps / 4) * groups : MODE == 13 ? 2.0 * M * N * 16 * 50 * (reps / 4) * groups : 2.0 * M * N * 16 * 16 * reps * groups;
   printf("%-28s err=%d  %.3f ms  %.1f TFLOP/s  cycles/MMA (cluster 0) %.1f\n", name, (int)e, ms, flops / (ms * 1e-3) / 1e12,
-         (double)c / (MODE == 13 ? 50.0 * (reps / 4) : 16.0 * reps));
+         (double)c / (MODE >= 21 ? 52.0 * (reps / 4) : MODE == 13 ? 50.0 * (reps / 4) : 16.0 * reps));
 }
 
 int main() {
-  run<0>("2CTA SS M256 N256 K16");
-  run<14>("2CTA SS + 4 warps tcgen05.ld");
-  run<18>("2CTA SS + 4 warps ld16/st8 in place");
-  run<19>("2CTA SS + L3-like TS N=16 batches");
+  // run<0>("2CTA SS M256 N256 K16");
+  // run<14>("2CTA SS + 4 warps tcgen05.ld");
+  // run<18>("2CTA SS + 4 warps ld16/st8 in place");
+  // run<19>("2CTA SS + L3-like TS N=16 batches");
+  // run<7>("2CTA SS random bf16");
+  // run<20>("2CTA SS fp16 subnormal A x fp16 B");
+  run<13>("2CTA SS rings like k_fused3 (random)");
+  run<24>("SS MMA + 8 epilogue-like warps");
+  run<25>("8 epilogue-like warps alone");
   return 0;
 }

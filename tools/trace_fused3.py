@@ -80,6 +80,10 @@ print("  tile 9 throttle", thr[1].tolist())
 print("  tile 9 g_full  ", gf[1].tolist())
 print("  tile 9 w_full  ", wf[1].tolist())
 print("  tile 9 stage-to-stage", np.diff(q[1, :, 0]).tolist())
+for kb in range(12):
+    e = q[1, kb]
+    print(f"  tile 9 stage {kb:2d}: mma0 {e[2]-e[0]:5d} commits {e[4]-e[2]:5d} mma1 {e[5]-e[4]:5d} ->wait {e[1]-e[5]:5d} "
+          f"wait {e[3]-e[1]:5d} mma2 {e[6]-e[3]:5d} mma3 {e[7]-e[6]:5d} ->next {q[1, kb+1, 0]-e[7]:5d}")
 print("  tile 9 mma issue     ", (q[1, :, 4] - q[1, :, 3]).tolist())
 print("  tile 9 serialized stage latency", (q[1, :, 7] - q[1, :, 6]).tolist())
 print("  tile 9 commits       ", (q[1, :, 5] - q[1, :, 4]).tolist())
@@ -99,10 +103,26 @@ for team, nm in ((0, "E1"), (1, "E2")):
         r = ep[team, k]
         print(f"{nm} tile {8 + k}: passA {r[1] - r[0]}  kb signals " + " ".join(str(r[2 + j] - r[0]) for j in range(4)))
 
-e2 = np.zeros((16, 5), np.uint64)
+e2 = np.zeros((2, 8, 2, 8), np.uint64)
 assert P.lib().mlpv_f3_trace_e2_read(e2.ctypes.data_as(C.c_void_p)) == 0
 e2 = e2.astype(np.int64)
-print("E2 tile 9 per item: stats / split / stores / wait_ld / total")
-for i in range(16):
-    r = e2[i]
-    print(f"  item {i:2d}: {r[1]-r[0]:5d} {r[2]-r[1]:5d} {r[3]-r[2]:5d} {r[4]-r[3]:5d}   {r[4]-r[0]:5d}")
+t0 = {team: e2[0, 0, team, 0] for team in (0, 1)}
+for team, nm in ((0, "E1"), (1, "E2")):
+    print(f"{nm} tile 9 per warp (relative to rank 0 warp 0 start): start, signs, kb0..kb3 signals, end")
+    for rk in range(2):
+        for w in range(8):
+            r = e2[rk, w, team]
+            rel = lambda x: str(int(x - t0[team])) if x else "-"
+            print(f"  rank {rk} warp {w}: start {rel(r[0])} signs {rel(r[1])} kb " + " ".join(rel(r[2 + j]) for j in range(4)) + f" end {rel(r[6])}")
+
+gp = np.zeros((8, 8, 5), np.uint64)
+assert P.lib().mlpv_f3_trace_grp_read(gp.ctypes.data_as(C.c_void_p)) == 0
+gp = gp.astype(np.int64)
+print("E2 pass B per group (rank 0, tile 9): stats / split / stores+signal / ld wait / to next top")
+for w in range(8):
+    row = []
+    for i in range(8):
+        e = gp[w, i]
+        nxt = gp[w, i + 1, 0] if i < 7 else e[4]
+        row.append(f"{e[1]-e[0]}/{e[2]-e[1]}/{e[3]-e[2]}/{e[4]-e[3]}/{nxt-e[4]}")
+    print(f"  warp {w} (q{w & 3} h{w >> 2}): " + "  ".join(row))
