@@ -92,30 +92,43 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
     else hf[j] = in_f(x, net.numeric, j);
   }
   __syncthreads();
+  // dense layers: one warp per output neuron, lanes stride the fan-in (coalesced weight rows),
+  // warp-shuffle sums
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (ws.base1 != nullptr) {                        // PHILOX_BOX: W1 x + b1 + origin W1 1 (fp64 sum)
     const int n1 = net.sizes[1];
-    for (int i = threadIdx.x; i < n1; i += blockDim.x) {
-      double acc = (double)static_cast<const float*>(net.b[0])[i];
-      for (int j = 0; j < n0; j++)
+    for (int i = wid; i < n1; i += nw) {
+      double acc = 0.0;
+      for (int j = lane; j < n0; j += 32)
         acc += (double)wload_f(net.W[0], net.numeric, (size_t)i * n0 + j) * ((double)hf[j] + pert.origin_d);
-      ws.base1[(size_t)b * n1 + i] = (float)acc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) ws.base1[(size_t)b * n1 + i] = (float)(acc + (double)static_cast<const float*>(net.b[0])[i]);
     }
   }
   const int T = net.trace_len;
   for (int l = 1; l <= net.L; l++) {
     const int nl = net.sizes[l], fan = net.sizes[l - 1];
-    for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+    for (int i = wid; i < nl; i += nw) {
       if (fixed) {
-        int32_t acc = static_cast<const int32_t*>(net.b[l - 1])[i];
-        for (int j = 0; j < fan; j++) acc += wload_i(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hi[j];
-        static_cast<int32_t*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
-        if (l < net.L) hin[i] = act_fixed(net.numeric, net.act, acc, net.shift[l - 1], net.knots);
+        int32_t acc = 0;
+        for (int j = lane; j < fan; j += 32) acc += wload_i(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hi[j];
+        acc = __reduce_add_sync(0xffffffffu, acc);
+        if (lane == 0) {
+          acc += static_cast<const int32_t*>(net.b[l - 1])[i];
+          static_cast<int32_t*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
+          if (l < net.L) hin[i] = act_fixed(net.numeric, net.act, acc, net.shift[l - 1], net.knots);
+        }
       } else {
         float acc = 0.f;
-        for (int j = 0; j < fan; j++) acc = fmaf(wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j), hf[j], acc);
-        acc += static_cast<const float*>(net.b[l - 1])[i];
-        static_cast<float*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
-        if (l < net.L) hn[i] = act_float(net.act, acc);
+        for (int j = lane; j < fan; j += 32) acc = fmaf(wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j), hf[j], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+          acc += static_cast<const float*>(net.b[l - 1])[i];
+          static_cast<float*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
+          if (l < net.L) hn[i] = act_float(net.act, acc);
+        }
       }
     }
     __syncthreads();

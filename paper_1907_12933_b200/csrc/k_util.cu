@@ -105,27 +105,31 @@ cudaError_t launch_neuron_cov(const DevNet& net, const DevCov& cov, const uint32
 }
 
 // tau_l = 1e-6 + 1e-5 * max over bases of max |u_l^base| (float potentials), one block per layer
-__global__ void k_tau(DevNet net, const float* trace, int n_base, float* tau) {
-  const int l = blockIdx.x + 1;
+// tau_l = 1e-6 + 1e-5 max_b max_i |u_l^base| (reading C20): a grid of (layer, base chunk) blocks,
+// max by atomicMax on the float bits (non-negative floats order as unsigned), then the affine map
+__global__ void k_tau_max(DevNet net, const float* trace, int n_base, int per_blk, unsigned* mx) {
+  const int l = blockIdx.y + 1;
   const int T = net.trace_len, n = net.sizes[l];
+  const int b0 = blockIdx.x * per_blk, b1 = min(n_base, b0 + per_blk);
   float m = 0.f;
-  for (size_t e = threadIdx.x; e < (size_t)n_base * n; e += blockDim.x) {
-    const size_t b = e / n, i = e % n;
-    m = fmaxf(m, fabsf(trace[b * T + net.loff[l] + i]));
-  }
-  __shared__ float red[32];
+  for (int b = b0; b < b1; b++)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(trace[(size_t)b * T + net.loff[l] + i]));
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmaxf(m, red[w]);
-    m = fmaxf(m, red[0]);
-    tau[l - 1] = 1e-6f + 1e-5f * m;
-  }
+  if ((threadIdx.x & 31) == 0) atomicMax(&mx[l - 1], __float_as_uint(m));
+}
+__global__ void k_tau_final(int L, float* tau) {
+  const int l = threadIdx.x;
+  if (l < L) tau[l] = 1e-6f + 1e-5f * __uint_as_float(reinterpret_cast<unsigned*>(tau)[l]);
 }
 
 cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* tau_out, cudaStream_t st) {
-  k_tau<<<net.L, 256, 0, st>>>(net, static_cast<const float*>(trace), n_base, tau_out);
+  cudaError_t e = cudaMemsetAsync(tau_out, 0, sizeof(float) * net.L, st);
+  if (e != cudaSuccess) return e;
+  const int per_blk = 8;
+  const dim3 grid((unsigned)((n_base + per_blk - 1) / per_blk), (unsigned)net.L);
+  k_tau_max<<<grid, 256, 0, st>>>(net, static_cast<const float*>(trace), n_base, per_blk,
+                                  reinterpret_cast<unsigned*>(tau_out));
+  k_tau_final<<<1, 32, 0, st>>>(net.L, tau_out);
   return cudaGetLastError();
 }
 
