@@ -177,6 +177,7 @@ struct alignas(16) Smem {
   float xf[2][3][128];
   uint32_t sc2[8][128];                      // E2: sign-change words of layer 2
   uint16_t vc2[16][128];                     // E2 slow path: value-change bits of layer 2 (16 neurons)
+  alignas(16) float c1row[8][128];           // E2: the layer-2 potentials of a warp's single cond1 row
 };
 
 constexpr size_t kTilesBytes = (size_t)(kSG + kSW) * kTile + (size_t)kChunks * kW3Chunk + 4 * kBiasTile;
@@ -482,7 +483,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             mma2_f16_ss(R3, sdesc_none(smem_u32(sT + kBiasTile), 128, 256), bd, id3, 1u);
           }
         }
-        if (l3_kb == kNkb2 - 1) mma2_commit(&S.acc3_full, 0x3);
+        if (l3_kb == 0) TR(l3_tl, 14);
+        if (l3_kb == kNkb2 - 1) { mma2_commit(&S.acc3_full, 0x3); TR(l3_tl, 15); }
       };
       auto drain_l3 = [&]() {                             // the rest of layer 3, blocking
         while (l3_kb < kNkb2) {
@@ -512,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           uint32_t notready = 0, l3go = 0;
           if (el) {
             const bool r1 = mbar_test(&S.g_full[gslot], gph), r2 = mbar_test(&S.w_full[wslot], wph);
-            const bool r3 = l3_kb < kNkb2 && mbar_test(&S.h2_kb[l3_kb & 3], l3_tl & 1u);
+            const bool r3 = l3_kb < kNkb2 && mbar_test(&S.h2_kb[MLPV_EXP == 37 ? 3 : (l3_kb & 3)], l3_tl & 1u);
             mma2_f16_ss_lo(R1, alo, blo, id1, kb ? 1u : 0u);
             TRI(tl, kb, 2);
             if (pend_g >= 0) mma2_commit(&S.g_empty[pend_g], 0x3);
@@ -829,7 +831,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
       pair_exchange_i(S, h, r, nsc2, istar2, 9 + q);
       const bool slow2 = __any_sync(0xffffffffu, cond1 || (need23 && valid && nsc2 <= 1));
-      const bool vcw_needed = __any_sync(0xffffffffu, cond1);
+      // value-change words of pair (1, 2) are needed only for cond1 rows (~1 % of candidates): a
+      // warp with exactly one such row copies that row's potentials to shared memory and the 32
+      // lanes evaluate them together after the hand-off (c1 path); two or more rows take the
+      // per-lane path inside the group loop
+      const uint32_t c1mask = __ballot_sync(0xffffffffu, cond1);
+      const bool c1path = __popc(c1mask) == 1;
+      const bool vcw_needed = __popc(c1mask) >= 2;
+      const bool statsB = vcw_needed || __any_sync(0xffffffffu, need23 && valid && nsc2 <= 1);
+      float* c1buf = S.c1row[warp - kWE];
       TRE(1, tl, 1);
       TRE2(tl, 1, 1);
       float linf2 = 0.f, minab2 = 3.0e38f, vcamb = 3.0e38f;
@@ -855,7 +865,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             if (MLPV_EXP == 33) tmem_ld_wait();
           }
           TRP(tl, i, 0);
-          if (slow2) {
+          if (c1path && cond1) {
+            float4* dst = reinterpret_cast<float4*>(c1buf + 16 * (g - 8 * h));
+            dst[0] = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
+            dst[1] = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]), __uint_as_float(v[7]));
+            dst[2] = make_float4(__uint_as_float(v[8]), __uint_as_float(v[9]), __uint_as_float(v[10]), __uint_as_float(v[11]));
+            dst[3] = make_float4(__uint_as_float(v[12]), __uint_as_float(v[13]), __uint_as_float(v[14]), __uint_as_float(v[15]));
+          }
+          if (statsB) {
             const float4* ub = reinterpret_cast<const float4*>(S.ub2 + 16 * g);
             float uu[16], d[16];
 #pragma unroll
@@ -912,6 +929,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
       if (et == 0) TR(tl, 11);
       TRE2(tl, 1, 6);
+      if (c1path) {
+        // lane l: neurons 4l..4l+3 of this half, the same fp32 operations as the per-lane path
+        __syncwarp();
+        const float4 u4 = reinterpret_cast<const float4*>(c1buf)[lane];
+        const float4 b4 = reinterpret_cast<const float4*>(S.ub2 + 128 * h)[lane];
+        const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
+        uint32_t nib = 0;
+        float mnu = 3.0e38f, mnv = 3.0e38f, mxd = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const float d = uu[k] - bb[k];
+          const float dt = fabsf(d) - tg2;
+          nib |= (__float_as_uint(dt) >> 31 ^ 1u) << k;
+          mnu = fminf(mnu, fabsf(uu[k]));
+          mnv = fminf(mnv, fabsf(dt));
+          mxd = fmaxf(mxd, fabsf(d));
+        }
+        // |x| >= 0: float order = unsigned order of the bits
+        const float rmnu = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mnu)));
+        const float rmnv = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mnv)));
+        const float rmxd = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mxd)));
+        uint32_t w[4];
+#pragma unroll
+        for (int pp = 0; pp < 4; pp++)
+          w[pp] = __reduce_or_sync(0xffffffffu, (lane >> 3) == pp ? nib << (4 * (lane & 7)) : 0u);
+        if (cond1) {
+          minab2 = fminf(minab2, rmnu);
+          vcamb = fminf(vcamb, rmnv);
+          linf2 = fmaxf(linf2, rmxd);
+#pragma unroll
+          for (int pp = 0; pp < 4; pp++) {
+            S.vc2[8 * h + 2 * pp][r] = (uint16_t)w[pp];
+            S.vc2[8 * h + 2 * pp + 1][r] = (uint16_t)(w[pp] >> 16);
+          }
+        }
+      }
       if (slow2) pair_exchange_f(S, h, r, linf2, minab2, vcamb, 9 + q);
       minab2 = fminf(minab2, S.minub2);
       // pair (1, 2): SS / SV row i* (nsc1 == 1) or VS / VV column masks (nsc1 == 0), reading C8;

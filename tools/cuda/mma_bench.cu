@@ -11,7 +11,7 @@ __device__ __forceinline__ void mma1_ss(uint32_t d, uint64_t a, uint64_t b, uint
 
 __device__ unsigned int g_sink;
 template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int reps, unsigned long long* cyc) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int reps, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t ready, done, scratch[4], pre;
@@ -55,7 +55,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
   const uint32_t tb = tbase;
   if (t == 0) { if (rank == 0 || MODE == 3) mbar_arrive(&ready); else mbar_arrive_cluster(&ready, 0); }
   if (t == 0) mbar_arrive(&pre);                       // phase 0 of `pre` completes: waits on it are no-ops
-  const bool issuer = (MODE == 3) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15 && MODE != 25);
+  const bool issuer = (MODE == 3) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15 && MODE != 25 && MODE != 27);
   __shared__ volatile int stop;
   if (t == 0) stop = 0;
   __syncthreads();
@@ -78,7 +78,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
       __nanosleep(400);
     }
     if (el && blockIdx.x == 0) printf("  L3-like batches issued: %llu\n", n);
-  } else if ((MODE == 24 || MODE == 25) && w >= 4 && w < 12) {
+  } else if ((MODE == 24 || MODE == 25 || MODE == 26 || MODE == 27 || MODE == 28) && w >= 4 && w < 12) {
     // epilogue-like: 8 warps (two per lane quadrant), per 16-column group: prefetch ld16 of the next
     // group, ~40 ALU ops, st16 in place, wait::ld
     const uint32_t loff = (uint32_t)(32 * (w & 3)) << 16;
@@ -99,6 +99,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
         for (int k = 0; k < 16; k++) hl[k] = (v[k] * 2654435761u) ^ (v[(k + 3) & 15] >> 3);
         const long long a0 = clock64();
         tmem_st16(tbase + loff + cb + 16 * g, hl);
+        if (MODE == 26 || MODE == 27 || MODE == 28) tmem_st_wait();
         const long long a1 = clock64();
         tmem_ld_wait();
         const long long a2 = clock64();
@@ -106,10 +107,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
       }
       tmem_st_wait();
       n += 8;
-      if (MODE == 25 && n >= 8 * 4000) break;
+      if ((MODE == 25 || MODE == 27) && n >= 8 * 4000) break;
     }
     const long long t1 = clock64();
-    if ((t & 31) == 0 && (w == 4 || w == 7) && blockIdx.x == 0)
+    if ((t & 31) == 0 && (w == 4 || w == 7) && (blockIdx.x == 0 || blockIdx.x == 1))
       printf("  w%d: %.1f cycles per group, st16 issue %.1f, ld wait %.1f\n", w, (double)(t1 - t0) / n, (double)tst / n, (double)tld / n);
   } else if (MODE == 18 && w >= 4 && w < 8) {
     const uint32_t loff = (uint32_t)(32 * (w & 3)) << 16;
@@ -152,13 +153,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
     if ((t & 31) == 0 && w == 4 && blockIdx.x == 0) printf("  ld16 rate: %.1f cycles per ld16+wait (warp), %.1f B/clk/SM (4 warps)\n",
         (double)(t1 - t0) / n, 4.0 * n * 32 * 16 * 4 / (double)(t1 - t0));
     if (acc == 0x1234567u) g_sink = acc;
-  } else if (w >= 4 && MODE >= 10 && MODE < 14) {
+  } else if ((w >= 4 && MODE >= 10 && MODE < 14) || (MODE == 28 && w >= 12)) {
     // background load while the MMAs run (warps 4..11)
     uint32_t c0 = t, c1 = t * 7, c2 = t * 13, c3 = t * 31, acc = 0;
     uint8_t* scratch = smem + 8 * 16384;                 // 32 KB scratch
     int it = 0;
     while (!stop) {
-      if (MODE == 10 || MODE == 12) {
+      if (MODE == 10 || MODE == 12 || MODE == 28) {
 #pragma unroll
         for (int r = 0; r < 10; r++) {
           const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
@@ -167,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
         }
         acc += c0 ^ c2;
       }
-      if (MODE == 11 || MODE == 12) {
+      if (MODE == 11 || MODE == 12 || MODE == 28) {
 #pragma unroll
         for (int k = 0; k < 4; k++)
           *reinterpret_cast<uint4*>(scratch + ((t * 16 + (it * 4 + k) * 4096) & 32767)) = make_uint4(c0, c1, acc, it);
@@ -224,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
           const uint64_t ad = sdesc_sw128(smem_u32(sA + kb * 16384 + kk * 32));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + kb * 16384 + kk * 32));
           const uint32_t acc = (r | kb | kk) ? 1u : 0u;
-          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16) || MODE == 18 || MODE == 19 || MODE == 20 || MODE == 24) mma2_f16_ss(tb, ad, bd, idesc, acc);
+          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16) || MODE == 18 || MODE == 19 || MODE == 20 || MODE == 24 || MODE == 26 || MODE == 28) mma2_f16_ss(tb, ad, bd, idesc, acc);
           else if (MODE == 1) mma2_f16_ts(tb, tb + 256 + kb * 32 + kk * 8, bd, idesc, acc);
           else if (MODE == 16 || MODE == 17) mma2_f16_ts(tb + 256, tb + kb * 32 + kk * 8, bd, idesc_f16(256, 128, 1, 1), acc);
           else mma1_ss(tb, ad, bd, idesc, acc);
@@ -241,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384) k_bench(int rep
   }
   if (MODE != 3) { if (t < 32 && !issuer) {} }
   __syncwarp();
-  if (!issuer && t == 0 && MODE != 3 && MODE != 15 && MODE != 25) { mbar_wait(&done, 0); stop = 1; }
+  if (!issuer && t == 0 && MODE != 3 && MODE != 15 && MODE != 25 && MODE != 27) { mbar_wait(&done, 0); stop = 1; }
   fence_before();
   __syncthreads();
   cluster_sync();
@@ -258,7 +259,7 @@ void run(const char* name) {
   const int reps = 2000;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int nt = MODE >= 10 ? 384 : 128;
+  const int nt = MODE == 28 ? 768 : (MODE >= 10 ? 384 : 128);
   k_bench<MODE><<<148, nt, smem>>>(10, cyc);
   cudaEventRecord(e0);
   k_bench<MODE><<<148, nt, smem>>>(reps, cyc);
@@ -283,7 +284,10 @@ int main() {
   // run<7>("2CTA SS random bf16");
   // run<20>("2CTA SS fp16 subnormal A x fp16 B");
   run<13>("2CTA SS rings like k_fused3 (random)");
-  run<24>("SS MMA + 8 epilogue-like warps");
-  run<25>("8 epilogue-like warps alone");
+  // run<24>("SS MMA + 8 epilogue-like warps");
+  // run<25>("8 epilogue-like warps alone");
+  run<26>("SS MMA + 8 epilogue-like warps, st waited");
+  run<27>("8 epilogue-like warps alone, st waited");
+  run<28>("SS MMA + 8 epilogue-like warps (st waited) + 12 philox/STS warps");
   return 0;
 }
