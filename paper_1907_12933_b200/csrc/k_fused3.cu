@@ -831,14 +831,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
       pair_exchange_i(S, h, r, nsc2, istar2, 9 + q);
       const bool slow2 = __any_sync(0xffffffffu, cond1 || (need23 && valid && nsc2 <= 1));
-      // value-change words of pair (1, 2) are needed only for cond1 rows (~1 % of candidates): a
-      // warp with exactly one such row copies that row's potentials to shared memory and the 32
-      // lanes evaluate them together after the hand-off (c1 path); two or more rows take the
-      // per-lane path inside the group loop
-      const uint32_t c1mask = __ballot_sync(0xffffffffu, cond1);
-      const bool c1path = __popc(c1mask) == 1;
-      const bool vcw_needed = __popc(c1mask) >= 2;
-      const bool statsB = vcw_needed || __any_sync(0xffffffffu, need23 && valid && nsc2 <= 1);
+      // Layer-2 statistics (min |u|, L-inf, value-change words and their margin) are needed only
+      // by rows with cond1 (pair (1, 2)) or with at most one layer-2 sign change (pair (2, 3)):
+      // under 1 % of the candidates.  A warp with exactly one such row copies that row's
+      // potentials to shared memory and its 32 lanes evaluate them together after the hand-off
+      // (c1 path); two or more rows take the per-lane path inside the group loop.
+      const bool statrow = cond1 || (need23 && valid && nsc2 <= 1);
+      const uint32_t smask = __ballot_sync(0xffffffffu, statrow);
+      const bool c1path = __popc(smask) == 1;
+      const bool statsB = __popc(smask) >= 2;
+      const bool vcw_needed = statsB && __any_sync(0xffffffffu, cond1);
       float* c1buf = S.c1row[warp - kWE];
       TRE(1, tl, 1);
       TRE2(tl, 1, 1);
@@ -865,7 +867,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             if (MLPV_EXP == 33) tmem_ld_wait();
           }
           TRP(tl, i, 0);
-          if (c1path && cond1) {
+          if (c1path && statrow) {
             float4* dst = reinterpret_cast<float4*>(c1buf + 16 * (g - 8 * h));
             dst[0] = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
             dst[1] = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]), __uint_as_float(v[7]));
@@ -954,7 +956,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 #pragma unroll
         for (int pp = 0; pp < 4; pp++)
           w[pp] = __reduce_or_sync(0xffffffffu, (lane >> 3) == pp ? nib << (4 * (lane & 7)) : 0u);
-        if (cond1) {
+        if (statrow) {
           minab2 = fminf(minab2, rmnu);
           vcamb = fminf(vcamb, rmnv);
           linf2 = fmaxf(linf2, rmxd);
