@@ -80,10 +80,14 @@ print("  tile 9 throttle", thr[1].tolist())
 print("  tile 9 g_full  ", gf[1].tolist())
 print("  tile 9 w_full  ", wf[1].tolist())
 print("  tile 9 stage-to-stage", np.diff(q[1, :, 0]).tolist())
-for kb in range(12):
-    e = q[1, kb]
-    print(f"  tile 9 stage {kb:2d}: mma0 {e[2]-e[0]:5d} commits {e[4]-e[2]:5d} mma1 {e[5]-e[4]:5d} ->wait {e[1]-e[5]:5d} "
-          f"wait {e[3]-e[1]:5d} mma2 {e[6]-e[3]:5d} mma3 {e[7]-e[6]:5d} ->next {q[1, kb+1, 0]-e[7]:5d}")
+for tt in range(4):
+    row = []
+    for kb in range(12):
+        e = q[tt, kb]
+        top = e[0]; nxt = q[tt, kb + 1, 0]
+        w = (e[3] - e[1]) if (e[1] > top and e[3] > e[1] and e[1] < nxt) else 0
+        row.append(f"{nxt - top}/{w}")
+    print(f"  tile {8 + tt} stage-to-stage/blocking-wait: " + " ".join(row))
 print("  tile 9 mma issue     ", (q[1, :, 4] - q[1, :, 3]).tolist())
 print("  tile 9 serialized stage latency", (q[1, :, 7] - q[1, :, 6]).tolist())
 print("  tile 9 commits       ", (q[1, :, 5] - q[1, :, 4]).tolist())
