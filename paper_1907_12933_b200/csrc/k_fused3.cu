@@ -845,9 +845,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       TRE(1, tl, 1);
       TRE2(tl, 1, 1);
       float linf2 = 0.f, minab2 = 3.0e38f, vcamb = 3.0e38f;
-      {
-        // pass B: half 1 starts with group 15 (its columns become the layer-3 accumulator, its h2
-        // goes to the shared-memory tail tiles)
+      if (!statsB) {
+        // pass B, two groups (32 columns) per step: one 32-column load and store, and two
+        // independent split chains for the scheduler to interleave.  Half 1 starts with groups
+        // 14-15 (15's columns become the layer-3 accumulator, its h2 goes to the shared-memory
+        // tail tiles).
+#pragma unroll 1
+        for (int ip = 0; ip < 4; ip++) {
+          const int g0 = h ? (ip == 0 ? 14 : 6 + 2 * ip) : 2 * ip;
+          uint32_t v[32];
+          tmem_ld32(R2 + loff + 16u * g0, v);
+          tmem_ld_wait();
+          if (h && ip == 0) {                              // group 15 has left TMEM: layer 3 may use its columns
+            fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_leader(&S.h2_kb[0], rank);
+          }
+          if (c1path && statrow) {
+            float4* dst = reinterpret_cast<float4*>(c1buf + 16 * (g0 - 8 * h));
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+              dst[k] = make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
+                                   __uint_as_float(v[4 * k + 3]));
+          }
+          uint32_t hl[32];                                   // [hi g0 | lo g0 | hi g0+1 | lo g0+1]
+#pragma unroll
+          for (int k = 0; k < 8; k++) {
+            split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hl[k], hl[8 + k]);
+            split_pair(__uint_as_float(v[16 + 2 * k]), __uint_as_float(v[16 + 2 * k + 1]), hl[16 + k], hl[24 + k]);
+          }
+          if (g0 < 14) {
+            tmem_st32(R2 + loff + 16u * g0, hl);
+          } else {
+            uint32_t h14[16];
+#pragma unroll
+            for (int k = 0; k < 16; k++) h14[k] = hl[k];
+            tmem_st16(R2 + loff + 16u * g0, h14);
+            *reinterpret_cast<uint4*>(sT + none16_off(r, 0)) = make_uint4(hl[16], hl[17], hl[18], hl[19]);
+            *reinterpret_cast<uint4*>(sT + none16_off(r, 8)) = make_uint4(hl[20], hl[21], hl[22], hl[23]);
+            *reinterpret_cast<uint4*>(sT + kBiasTile + none16_off(r, 0)) = make_uint4(hl[24], hl[25], hl[26], hl[27]);
+            *reinterpret_cast<uint4*>(sT + kBiasTile + none16_off(r, 8)) = make_uint4(hl[28], hl[29], hl[30], hl[31]);
+            fence_proxy_async();
+          }
+          if (h ? ip >= 2 : (ip & 1)) {                     // K block (g0 + 1) >> 2 complete on this half
+            const int kb = h ? ip : ip >> 1;
+            tmem_st_wait();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_leader(&S.h2_kb[kb], rank);
+            TRE(1, tl, 2 + kb);
+            TRE2(tl, 1, 2 + kb);
+          }
+        }
+      } else {
+        // pass B, per group (warps computing the statistics per lane): half 1 starts with group 15
         uint32_t vbuf[2][16];
         const int gfirst = h ? 15 : 0;
         tmem_ld16(R2 + loff + 16u * gfirst, vbuf[0]);
