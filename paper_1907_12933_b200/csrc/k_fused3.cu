@@ -728,35 +728,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       TRE(0, tl, 0);
       TRE2(tl, 0, 0);
       fence_after();
-      // single pass, 16-column groups; half h takes pieces (32-neuron words) h, h+2, h+4, h+6, so
-      // both halves contribute to every 64-neuron block and block 0 is handed to the MMA after each
-      // half has done two groups.  Per-group: u1 = base1 + stepS * acc (reading C14b), sign-change
-      // bits, L-inf / min |u| (only while some row of the warp can still end with <= 1 change), then
-      // H1 = fp16 hi | lo in place.
+      // single pass, one piece (32 neurons = 32 columns) per step; half h takes pieces h, h+2, h+4,
+      // h+6, so both halves contribute to every 64-neuron block and block k is handed to the MMA
+      // after step k of each half.  Per piece: u1 = base1 + stepS * acc (reading C14b), H1 = fp16
+      // hi | lo in place (one 32-column store), sign-change bits, and L-inf / min |u| while some row
+      // of the warp can still end with <= 1 change.  32 columns per step give the scheduler two
+      // independent 16-neuron chains (the step is latency-bound).
       int nsc1 = 0, istar1 = -1;
       float linf1 = 0.f, minab1 = 3.0e38f;
-      {
-        uint32_t vbuf[2][16];
-        tmem_ld16(R1 + loff + 32u * h, vbuf[0]);
+#pragma unroll 1
+      for (int k4 = 0; k4 < 4; k4++) {
+        const int p = 2 * k4 + h;                          // piece: groups 2p, 2p + 1
+        uint32_t v[32];
+        tmem_ld32(R1 + loff + 32u * p, v);
         tmem_ld_wait();
-#pragma unroll 2
-        for (int i = 0; i < 8; i++) {
-          const int g = 4 * (i >> 1) + 2 * h + (i & 1);  // group (16 neurons)
-          uint32_t (&v)[16] = vbuf[i & 1];
-          if (i < 7) {
-            const int gn = 4 * ((i + 1) >> 1) + 2 * h + ((i + 1) & 1);
-            tmem_ld16(R1 + loff + 16u * gn, vbuf[(i + 1) & 1]);
-          }
-          acc_to_u1(v, S.b1 + 16 * g, stepS);
-          const uint32_t s = sign16(v) ^ ((S.nb1[g >> 1] >> (16 * (g & 1))) & 0xFFFFu);
-          nsc1 += __popc(s);
-          if (istar1 < 0 && s) istar1 = 16 * g + __ffs(s) - 1;
-          if (eval && valid) {
+        acc_to_u1(v, S.b1 + 32 * p, stepS);
+        uint32_t hl[32];                                   // [hi 2p | lo 2p | hi 2p+1 | lo 2p+1]
 #pragma unroll
-            for (int j = 0; j < 16; j++) a.eval_out[cidx * a.T + 16 * g + j] = __uint_as_float(v[j]);
-          }
-          if (__any_sync(0xffffffffu, need12 && valid && nsc1 <= 1)) {
-            const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 16 * g);
+        for (int k = 0; k < 8; k++) {
+          split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hl[k], hl[8 + k]);
+          split_pair(__uint_as_float(v[16 + 2 * k]), __uint_as_float(v[16 + 2 * k + 1]), hl[16 + k], hl[24 + k]);
+        }
+        tmem_st32(R1 + loff + 32u * p, hl);
+        const uint32_t s = sign32(v) ^ S.nb1[p];
+        nsc1 += __popc(s);
+        if (istar1 < 0 && s) istar1 = 32 * p + __ffs(s) - 1;
+        if (eval && valid) {
+#pragma unroll
+          for (int j = 0; j < 32; j++) a.eval_out[cidx * a.T + 32 * p + j] = __uint_as_float(v[j]);
+        }
+        if (__any_sync(0xffffffffu, need12 && valid && nsc1 <= 1)) {
+#pragma unroll
+          for (int hh = 0; hh < 2; hh++) {
+            const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 32 * p + 16 * hh);
             float uu[16], d[16];
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -764,28 +768,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
               const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
               for (int j = 0; j < 4; j++) {
-                uu[4 * k + j] = __uint_as_float(v[4 * k + j]);
+                uu[4 * k + j] = __uint_as_float(v[16 * hh + 4 * k + j]);
                 d[4 * k + j] = uu[4 * k + j] - bb[j];
               }
             }
             linf1 = max_abs16(linf1, d);
             minab1 = min_abs16(minab1, uu);
           }
-          uint32_t hl[16];                                   // [hi (8 cols) | lo (8 cols)]
-#pragma unroll
-          for (int k = 0; k < 8; k++) split_pair(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]), hl[k], hl[8 + k]);
-          // in place: the 16 fp32 columns of these neurons become [hi | lo], one 16-column store
-          tmem_st16(R1 + loff + 16u * g, hl);
-          if (i & 1) {
-            tmem_st_wait();
-            fence_before();
-            __syncwarp();
-            if (lane == 0) arrive_leader(&S.h1_kb[g >> 2], rank);
-            TRE(0, tl, 2 + (g >> 2));
-            TRE2(tl, 0, 2 + (g >> 2));
-          }
-          tmem_ld_wait();
         }
+        tmem_st_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(&S.h1_kb[k4], rank);
+        TRE(0, tl, 2 + k4);
+        TRE2(tl, 0, 2 + k4);
       }
       TRE(0, tl, 1);
       pair_exchange_i(S, h, r, nsc1, istar1, 9 + q);
