@@ -722,8 +722,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
       // =========================== E1: layer-1 potentials -> predicates, H1 = fp16 hi | lo in place
       // (one warp polls; the others sleep in bar.sync)
-      if (et == 0) { mbar_wait_sleep(&S.acc1_full, tl & 1u, 64); }
-      named_bar(4, 256);
+      // each half waits on its own (half 1 comes from the previous tile's E3)
+      if ((et & 127) == 0) { mbar_wait_sleep(&S.acc1_full, tl & 1u, 64); }
+      named_bar(h ? 14 : 3, 128);
       if (et == 0) TR(tl, 8);
       TRE(0, tl, 0);
       TRE2(tl, 0, 0);
@@ -737,8 +738,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       int nsc1 = 0, istar1 = -1;
       float linf1 = 0.f, minab1 = 3.0e38f;
 #pragma unroll 1
-      for (int k4 = 0; k4 < 4; k4++) {
-        const int p = 2 * k4 + h;                          // piece: groups 2p, 2p + 1
+      for (int k4 = 0; k4 < (h ? 3 : 5); k4++) {
+        // half 0: pieces 0, 1, 2, 4, 6 (block 0 alone); half 1, which first finishes the previous
+        // tile's E3: pieces 3, 5, 7
+        const int p = h ? 2 * k4 + 3 : (k4 < 2 ? k4 : 2 * k4 - 2);   // piece: groups 2p, 2p + 1
+        const int kbs = p >> 1;                            // the 64-neuron block it completes a part of
         uint32_t v[32];
         tmem_ld32(R1 + loff + 32u * p, v);
         tmem_ld_wait();
@@ -776,12 +780,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             minab1 = min_abs16(minab1, uu);
           }
         }
-        tmem_st_wait();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_leader(&S.h1_kb[k4], rank);
-        TRE(0, tl, 2 + k4);
-        TRE2(tl, 0, 2 + k4);
+        {                                                  // every piece signs off its half of the block
+          tmem_st_wait();
+          fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_leader(&S.h1_kb[kbs], rank);
+          TRE(0, tl, 2 + kbs);
+          TRE2(tl, 0, 2 + kbs);
+        }
       }
       TRE(0, tl, 1);
       pair_exchange_i(S, h, r, nsc1, istar1, 9 + q);
@@ -1033,13 +1039,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           if (vcw) { atomicOr(&a.res.cov_all[iv], vcw); if (certain) atomicOr(&a.res.cov_certain[iv], vcw); }
         }
       }
-      if (h == 1) continue;                                // E3 is done by half 0
+      if (h == 0) continue;                                // E3 is done by half 1
       const bool cond2 = need23 && valid && ((nsc2 == 1) || (nsc2 == 0 && linf2 >= th2));
       const bool amb2 = minab2 < tau1 || (nsc2 == 0 && fabsf(linf2 - th2) < tau1);
       // =========================== E3: logits -> pair (2, 3), argmax, property, counts
-      if (et == 0) mbar_wait_sleep(&S.acc3_full, tl & 1u, 64);
+      if (et == 128) mbar_wait_sleep(&S.acc3_full, tl & 1u, 64);
       named_bar(5, 128);
-      if (et == 0) TR(tl, 12);
+      if (et == 128) TR(tl, 12);
       fence_after();
       uint32_t v[16];
       tmem_ld16(R3 + loff, v);
@@ -1120,7 +1126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           if (mnu != 0xFFFFFFFFu) atomicMin(reinterpret_cast<unsigned long long*>(a.res.first_cex_unflagged) + ti.b, (unsigned long long)(ti.start + mnu));
         }
       }
-      if (et == 0) TR(tl, 13);
+      if (et == 128) TR(tl, 13);
     }
   }
   fence_before();
