@@ -80,3 +80,90 @@ def test_cfg5_int8_bitexact(P, oracle_mod):
     assert_fixed_parity(run_gpu(chk, s), oracle_mod.check(s))
     g, o = _eval(P, chk, cfg, 1, [0, 1, 2 ** 30 - 1, 123456, 999], oracle_mod)
     assert np.array_equal(g.astype(np.int64), o.astype(np.int64))
+
+
+# ----------------------------------------------------------------------------- k_fused3 variants
+def _box_cfg(n0=784, n3=10, eps=0.05, n_base=6, w_var=2.0, seed=7, prop=None):
+    """A 3-layer n0-256-256-n3 ReLU bf16 net on the PHILOX_BOX space (reading C14b), i.e. the
+    k_fused3 path with another input width / class count / radius / property."""
+    rng = np.random.default_rng([12933, 900, seed])
+    sizes = [n0, 256, 256, n3]
+    W = [M.f32_to_bf16_bits(rng.normal(0.0, np.sqrt(w_var / sizes[l - 1]), (sizes[l], sizes[l - 1])).astype(np.float32))
+         for l in range(1, 4)]
+    b = [rng.normal(0.0, np.sqrt(1.0 / sizes[l - 1]), sizes[l]).astype(np.float32) for l in range(1, 4)]
+    net = M.Net(sizes, M.ACT_RELU, M.NUM_BF16, W, b, acc_scale=[1.0, 1.0, 1.0])
+    bases = M.f32_to_bf16_bits(rng.random((n_base, n0), dtype=np.float32))
+    pert = M.Pert(M.PERT_PHILOX_BOX, seed=int(rng.integers(2 ** 63)), n_samples=2 ** 32,
+                  lattice_step=2 * eps / 15.0, lattice_origin=-eps)
+    pert.index_end = pert.n_samples
+    return M.Config("box", "k_fused3 variant", net, bases, pert, prop or M.Prop(), M.CovSpec([1, 2]))
+
+
+def test_fused3_small_radius_coverage_paths(P, oracle_mod):
+    """eps = 0.002: most candidates keep (almost) every sign, so the rare-row statistics paths of
+    E1/E2 (cond1 rows, <= 1 layer-2 change, one and several such rows per warp) carry the load."""
+    cfg = _box_cfg(eps=0.002, n_base=4)
+    chk = P.Checker(cfg.net)
+    s = cfg.subset(begin=0, end=1500)
+    o = oracle_mod.check(s)
+    assert o.cov_all.any()
+    assert_float_parity(run_gpu(chk, s), o)
+
+
+def test_fused3_large_radius_verdicts(P, oracle_mod):
+    """eps = 0.4: many violations (first counterexample, flagged counts) on the fused path."""
+    cfg = _box_cfg(eps=0.4, n_base=5, seed=8)
+    chk = P.Checker(cfg.net)
+    s = cfg.subset(begin=1000, end=2300)
+    o = oracle_mod.check(s)
+    assert o.violated.sum() > 0
+    assert_float_parity(run_gpu(chk, s), o)
+
+
+@pytest.mark.parametrize("n0,n3", [(200, 7), (1024, 16), (2, 2)])
+def test_fused3_shapes(P, oracle_mod, n0, n3):
+    """Other input widths (K tail inside a stage, the largest K, a single K step) and class counts."""
+    cfg = _box_cfg(n0=n0, n3=n3, eps=0.05, n_base=3, seed=n0)
+    chk = P.Checker(cfg.net)
+    s = cfg.subset(begin=17, end=17 + 700)
+    assert_float_parity(run_gpu(chk, s), oracle_mod.check(s))
+    g, o = _eval(P, chk, cfg, 1, [0, 3, 2 ** 32 - 1, 99999], oracle_mod)
+    assert_logits_close(g[:, -n3:], o[:, -n3:])
+
+
+def test_fused3_properties(P, oracle_mod):
+    for prop in (M.Prop(M.PROP_TARGET_NEVER, 3, 0.0), M.Prop(M.PROP_THRESHOLD_LITERAL, -1, 0.2),
+                 M.Prop(M.PROP_THRESHOLD_LITERAL, 1, -0.1)):
+        cfg = _box_cfg(eps=0.2, n_base=3, seed=11, prop=prop)
+        chk = P.Checker(cfg.net)
+        s = cfg.subset(begin=0, end=900)
+        assert_float_parity(run_gpu(chk, s), oracle_mod.check(s))
+
+
+def test_cfg4_bench_launch(P, oracle_mod):
+    """The launch bench.py times (all 1000 bases x a 65,536-sample slice, the fused kernel over
+    256,000 tiles, base changes inside every cluster's tile range).  Base 0 (whose Philox base
+    index is the same in a one-base oracle run) against the oracle on the same slice; for the
+    other bases, properties that hold at any size: every candidate counted, and each reported
+    first counterexample re-evaluates (oracle decode + forward in double) to a changed class or
+    a flagged near-tie."""
+    cfg = M.make_config("cfg4")
+    chk = _checker(P, "cfg4")
+    lo, hi = 3 * 65536, 4 * 65536
+    g = run_gpu(chk, cfg.subset(begin=lo, end=hi))
+    assert np.all(g["checked"] == hi - lo)
+    tau = oracle_mod.default_tau(cfg)                       # tau_l from all 1000 bases, as on the GPU
+    o = oracle_mod.check(cfg.subset(n_base=1, base_start=0, begin=lo, end=hi), tau=tau)
+    vg, vo = int(g["violated"][0]), int(o.violated[0])
+    assert abs(vg - vo) <= min(int(g["flagged"][0]), int(o.flagged[0]))
+    assert int(g["first_cex"][0]) <= int(o.first_cex_unflagged[0])
+    assert int(o.first_cex[0]) <= int(g["first_cex_unflagged"][0])
+    assert not np.any(o.cov_certain & ~g["cov_all"][:len(o.cov_certain)])
+    bad = np.nonzero(g["first_cex"] != UMAX)[0]
+    for b in bad[:20]:
+        c = int(g["first_cex"][b])
+        assert lo <= c < hi
+        y = oracle_mod.forward(cfg.net, oracle_mod.decode(cfg.net.numeric, cfg.pert, cfg.bases[b], int(b), c))[-1]
+        yb = oracle_mod.forward(cfg.net, cfg.bases[b])[-1]
+        top = np.sort(y)[::-1]
+        assert int(np.argmax(y)) != int(np.argmax(yb)) or top[0] - top[1] < 1e-5, (b, c)
