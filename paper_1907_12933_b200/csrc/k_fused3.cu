@@ -10,25 +10,27 @@
 //            subnormals l * 2^-24, one PRMT per pixel pair) generated on chip into a SWIZZLE_128B
 //            ring; B = W1 (fp16) half tiles streamed by cp.async.bulk; TMEM cols [0,256) accumulate
 //            2^-24 W1 l and E1 forms u1 = base1 + (step 2^24) acc with base1 from the prologue.
-//   E1       8 warps (two per TMEM lane quadrant), thread = candidate row; one pass per 16-column
-//            group: u1, the sign-change bits against the base potentials, the L-inf / min|u|
-//            partials (only while some row of the warp can still end with <= 1 change, the only
-//            case a covering method can fire on), then u1 in place -> the fp16 hi/lo split of
-//            h1 = ReLU(u1) (reading C19; each group becomes [hi | lo]).  The halves interleave
-//            32-neuron pieces so that each 64-neuron K block is handed to the MMA after two groups.
-//   layer 2  A = H1 straight from TMEM, B = W2 (fp16, duplicated for the lo half); the bias is one
+//   E1       8 warps (two per TMEM lane quadrant, "halves"), thread = candidate row; one pass, one
+//            32-neuron piece per step: u1, h1 = ReLU(u1) -> fp16 [hi | lo] in place (reading C19),
+//            the sign-change bits against the base potentials, and the L-inf / min|u| partials
+//            while some row of the warp can still end with <= 1 change (the only case a covering
+//            method fires on).  Half 0 takes pieces 0,1,2,4,6 and starts at once; half 1 first
+//            finishes the previous tile's E3, then takes 3,5,7.  Each piece signs off its part of
+//            a 64-neuron K block of layer 2.
+//   layer 2  A = H1 straight from TMEM, B = W2 (fp16, the same tile for hi and lo); the bias is one
 //            more SS MMA (ones column x [b_hi | b_lo]); accumulator TMEM cols [256,512).
-//   E2       4 warps: pass A sign words sc2; pass B turns u2 in place into the fp16 hi/lo split of
-//            h2 (neurons 0-239; 240-255 go to a small shared-memory tile so that their 16 columns
-//            can hold the layer-3 accumulator), plus the pair-(1,2) coverage and pair-(2,3)
-//            predicates on the (warp-uniform) slow path.
+//   E2       pass A: sign words sc2 and counts; pass B: u2 -> [hi | lo] in place, one piece per step
+//            (neurons 240-255 go to a small shared-memory tile so that their 16 columns can hold
+//            the layer-3 accumulator).  The layer-2 statistics are needed by < 1 % of the rows: a
+//            warp's single such row is evaluated by all 32 lanes from a shared-memory copy, warps
+//            with several compute them per lane.  Then the pair-(1,2) coverage words.
 //   layer 3  N = 16 (n_3 <= 16): A = H2 from TMEM (and the tail tile), accumulator TMEM cols
-//            [496,512).
-//   E3       E2's warps: logits, pair (2,3), argmax / margin / property, counts, first counterexample.
+//            [496,512); issued by the MMA issuer between layer-1 stages of the next tile.
+//   E3       half 1: logits, pair (2,3), argmax / margin / property, counts, first counterexample.
 //
 // Warp roles (24 warps, see kW* below): 0-11 generator (three warpgroups taking ring stages in
-// turn), 12-19 epilogue team (two warps per TMEM lane quadrant, each half of the neurons), 20 idle,
-// 21 weight producer, 23 MMA issuer of all layers (leader) / weight relay (peer) and TMEM owner.
+// turn), 12-19 epilogue team, 20 idle, 21 weight producer, 23 MMA issuer of all layers (leader) /
+// weight relay (peer) and TMEM owner.  DESIGN.md §6 has the measured timeline.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -46,15 +48,10 @@ using namespace tc;
 
 namespace f3 {
 #ifndef MLPV_EXP
-#define MLPV_EXP 0                           // timing experiments only (tools/trace_fused3.py); 0 = product
+#define MLPV_EXP 0                           // timing experiments only (tools/exp_f3.sh); 0 = product
 #endif
-// experiment masks (MLPV_EXP >= 100): keep only the listed activities on top of the MMA chain
-#define EXP_ON(bit) (MLPV_EXP < 100 || (((MLPV_EXP - 100) & (bit)) != 0))
-#define EXPB_GENC 1
-#define EXPB_GENS 2
-#define EXPB_TMA 4
-#define EXPB_E 8
-#define EXPB_L3 16
+// MLPV_EXP = 21: the generators skip their shared-memory stores; 104: the weights are streamed
+// only for the first tile (results are wrong in both; they isolate a resource in the timeline)
 #ifdef MLPV_TRACE
 // debug timeline (tools/trace_fused3.py): clock64 stamps of the first 64 tiles of cluster 0
 __device__ unsigned long long g_trace[2][64][32];
@@ -374,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 
   if (threadIdx.x == 0) {
     const uint32_t two = rank == 0 ? 2u : 1u;
-    for (int i = 0; i < kSG; i++) { mbar_init(&S.g_full[i], MLPV_EXP == 11 ? 4 : 8); mbar_init(&S.g_empty[i], 1); }
+    for (int i = 0; i < kSG; i++) { mbar_init(&S.g_full[i], 8); mbar_init(&S.g_empty[i], 1); }
     for (int i = 0; i < kSW; i++) { mbar_init(&S.w_full[i], two); mbar_init(&S.w_empty[i], 1); }
     mbar_init(&S.acc1_full, 1); mbar_init(&S.acc2_full, 1); mbar_init(&S.acc3_full, 1);
     mbar_init(&S.acc2_free, 8);
@@ -416,7 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         for (int s = 0; s < nst; s++) {
           const uint32_t st = ws % kSW, ph = (ws / kSW) & 1u;
           mbar_wait_sleep(&S.w_empty[st], ph ^ 1u, 128);
-#if MLPV_EXP == 2 || MLPV_EXP == 6 || MLPV_EXP == 13 || !EXP_ON(EXPB_TMA)
+#if MLPV_EXP == 104
           if (t == t_begin) {
             mbar_expect_tx(&S.w_full[st], kTile);
             bulk_g2s(sW + st * kTile, src0 + (size_t)s * kTile, kTile, &S.w_full[st]);
@@ -514,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           uint32_t notready = 0, l3go = 0;
           if (el) {
             const bool r1 = mbar_test(&S.g_full[gslot], gph), r2 = mbar_test(&S.w_full[wslot], wph);
-            const bool r3 = l3_kb < kNkb2 && mbar_test(&S.h2_kb[MLPV_EXP == 37 ? 3 : (l3_kb & 3)], l3_tl & 1u);
+            const bool r3 = l3_kb < kNkb2 && mbar_test(&S.h2_kb[l3_kb & 3], l3_tl & 1u);
             mma2_f16_ss_lo(R1, alo, blo, id1, kb ? 1u : 0u);
             TRI(tl, kb, 2);
             if (pend_g >= 0) mma2_commit(&S.g_empty[pend_g], 0x3);
@@ -917,7 +914,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           if (i < 7) {
             const int gn = h ? 8 + i : i + 1;
             tmem_ld16(R2 + loff + 16u * gn, vbuf[(i + 1) & 1]);
-            if (MLPV_EXP == 33) tmem_ld_wait();
           }
           TRP(tl, i, 0);
           if (c1path && statrow) {
@@ -961,7 +957,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           TRP(tl, i, 2);
           if (g < 15) {
             tmem_st16(R2 + loff + 16u * g, hl);
-            if (MLPV_EXP == 33) tmem_st_wait();
           } else {
             *reinterpret_cast<uint4*>(sT + none16_off(r, 0)) = make_uint4(hl[0], hl[1], hl[2], hl[3]);
             *reinterpret_cast<uint4*>(sT + none16_off(r, 8)) = make_uint4(hl[4], hl[5], hl[6], hl[7]);
