@@ -654,10 +654,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpi));
     // ------------------------------------------------------------------ epilogue team (E1, E2, E3)
-    // Eight warps, two per TMEM lane quadrant: warp half h takes neuron groups [8h, 8h + 8) of every
-    // layer (16-column groups).  The team runs E1(t) -> E2(t) -> E1(t+1) ..., which is the order in
-    // which the accumulators become ready (E2(t) overlaps the layer-1 MMAs of tile t+1).  Per-row
-    // partial results of the two halves meet in shared memory.
+    // Eight warps, two per TMEM lane quadrant (halves h = 0, 1; same rows, different neurons).  Half
+    // 0 runs E1(t) -> E2(t) -> E1(t+1), half 1 E1(t) -> E2(t) -> E3(t) -> E1(t+1): the order in which
+    // the accumulators become ready (E2(t) overlaps the layer-1 MMAs of tile t+1).  Per-row partial
+    // results of the two halves meet in shared memory.
     const int q = warp & 3, h = (warp - kWE) >> 2;
     const int r = 32 * q + lane;                           // row = TMEM lane
     const int et = threadIdx.x - 32 * kWE;                 // 0..255
