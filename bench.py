@@ -142,10 +142,15 @@ def cpu_baseline(cfg, budget_s=12.0):
     cores = os.cpu_count() or 1
     os.environ["OMP_NUM_THREADS"] = str(cores)
     nb = min(16, cfg.n_base)
-    probe = cfg.subset(n_base=nb, begin=0, end=min(cfg.space, 8))
-    t0 = time.perf_counter()
-    O.check(probe, nthreads=cores)
-    dt = max(time.perf_counter() - t0, 1e-3)
+    m = 64                                       # calibrate on probes of at least ~1 s, then size the
+    while True:                                  # timed sample to ~budget_s of oracle work
+        probe = cfg.subset(n_base=nb, begin=0, end=min(cfg.space, m))
+        t0 = time.perf_counter()
+        O.check(probe, nthreads=cores)
+        dt = max(time.perf_counter() - t0, 1e-3)
+        if dt >= 1.0 or m >= cfg.space:
+            break
+        m *= 4
     rate = nb * (probe.pert.index_end - probe.pert.index_begin) / dt
     m = int(max(8, min(cfg.space, budget_s * rate / nb)))
     s = cfg.subset(n_base=nb, begin=0, end=m)
@@ -285,6 +290,7 @@ def main():
         d2h = sum(v.numel() * v.element_size() for v in host_out.values())
         e2e_ms, e2e_cand = 0.0, 0
         for k in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+            flush.fill_(k & 0xFF)               # the same L2 flush as the device-timed steps
             torch.cuda.synchronize()
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
