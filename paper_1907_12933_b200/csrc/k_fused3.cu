@@ -545,11 +545,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         // layer 2: D = R2 <- bias (ones x [b_hi | b_lo]) + H1 (fp16 hi | lo, TMEM) x W2 half tiles
         mbar_wait_sleep(&S.acc2_free, (tl & 1u) ^ 1u, 64);
         TR(tl, 4);
+        fence_after();                                      // the bias needs only R2, not H1
+        if (el) mma2_f16_ss(R2, sdesc_none(smem_u32(sOnes), 128, 256), sdesc_none(smem_u32(sB2), 128, 256), id2, 0u);
         mbar_wait_sleep(&S.h1_kb[0], tl & 1u, 32);
         TR(tl, 3);
         mbar_wait(&S.w_full[wslot], wph);
-        fence_after();
-        if (el) mma2_f16_ss(R2, sdesc_none(smem_u32(sOnes), 128, 256), sdesc_none(smem_u32(sB2), 128, 256), id2, 0u);
         for (int kb = 0; kb < kNkb2; kb++) {
           fence_after();
           const uint32_t bb = smem_u32(sW + wslot * kTile);

@@ -143,12 +143,24 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
 #pragma unroll
       for (int ww = 0; ww < 4; ww++) {
         uint32_t o[4];
+        // the 8 base pixels of this word: one 16-byte broadcast load when they are all in range
+        uint32_t xv[4] = {0, 0, 0, 0};
+        const int pw = p0 + 8 * ww;
+        if (pw + 8 <= n0 && ((n0 & 7) == 0)) {
+          const uint4 x8 = __ldg(reinterpret_cast<const uint4*>(x + pw));
+          xv[0] = x8.x; xv[1] = x8.y; xv[2] = x8.z; xv[3] = x8.w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int p = pw + 2 * k;
+            if (p + 1 < n0) xv[k] = (uint32_t)__ldg(x + p) | ((uint32_t)__ldg(x + p + 1) << 16);
+            else if (p < n0) xv[k] = (uint32_t)__ldg(x + p);
+          }
+        }
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           const int p = p0 + 8 * ww + 2 * k;               // pixels p, p+1
-          uint32_t x2 = 0;
-          if (p + 1 < n0) x2 = __ldg(reinterpret_cast<const uint32_t*>(x + p));
-          else if (p < n0) x2 = (uint32_t)__ldg(x + p);
+          const uint32_t x2 = xv[k];
           uint32_t y = lattice_pair_bf16((ws[ww] >> (8 * k)) & 0xFFu, x2, step2, org2);
           if (p >= n0) y = 0;
           else if (p + 1 >= n0) y &= 0xFFFFu;
@@ -173,6 +185,17 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
 #pragma unroll
         for (int ww2 = 0; ww2 < 2; ww2++) {
           const int ww = 2 * half + ww2;
+          // the 8 base pixels of this word: one 8-byte broadcast load when they are all in range
+          const int pw = p0 + 8 * ww;
+          uint8_t xb[8];
+          if (pw + 8 <= n0 && ((n0 & 7) == 0)) {
+            const uint2 x8 = __ldg(reinterpret_cast<const uint2*>(x + pw));
+#pragma unroll
+            for (int n = 0; n < 4; n++) { xb[n] = (uint8_t)(x8.x >> (8 * n)); xb[4 + n] = (uint8_t)(x8.y >> (8 * n)); }
+          } else {
+#pragma unroll
+            for (int n = 0; n < 8; n++) xb[n] = pw + n < n0 ? __ldg(x + pw + n) : (uint8_t)0;
+          }
 #pragma unroll
           for (int h4 = 0; h4 < 2; h4++) {
             uint32_t packed = 0;
@@ -183,7 +206,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
               int y = 0;
               if (p < n0) {
                 const int l = (int)((ws[ww] >> (4 * nb)) & 15u);
-                y = max(0, min(255, (int)__ldg(x + p) + l * s + og));
+                y = max(0, min(255, (int)xb[nb] + l * s + og));
               }
               packed |= (uint32_t)y << (8 * n);
             }
