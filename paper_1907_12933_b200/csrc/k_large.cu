@@ -256,8 +256,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           const LayerDesc& ld = a.lay[l];
           const uint32_t wbytes = (uint32_t)ld.nc * 128u;
           if (l >= 2) { mbar_wait(&h_ready[l - 1], hph[l - 1]); hph[l - 1] ^= 1u; }
-          for (int ch = 0; ch < ld.nchunks; ch++)
-            for (int kb = 0; kb < ld.nkb; kb++) {
+          // layer 1 with an even chunk count runs the chunks in pairs on one generated A stage:
+          // W stages in the order (pair, kb, chunk of the pair)
+          const bool paired = l == 1 && (ld.nchunks & 1) == 0;
+          for (int i = 0; i < ld.nchunks * ld.nkb; i++) {
+            const int ch = paired ? 2 * (i / (2 * ld.nkb)) + (i & 1) : i / ld.nkb;
+            const int kb = paired ? (i / 2) % ld.nkb : i % ld.nkb;
+            {
               const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
               mbar_wait(&pempty[st], ph ^ 1u);
               mbar_expect_tx(&pfull[st], wbytes + (l >= 2 ? kABytes : 0u));
@@ -265,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               if (l >= 2) bulk_g2s(sPA + st * kABytes, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
               ps++;
             }
+          }
         }
       }
     }
@@ -277,6 +283,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
           const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, l == 1 ? 1 : 0, l == 1 ? 1 : 0);
+          if (l == 1 && (ld.nchunks & 1) == 0) {
+            // chunk pairs: both accumulators, one generated A stage per K block (half the Philox work)
+            for (int cp = 0; cp < ld.nchunks / 2; cp++) {
+#pragma unroll
+              for (int c = 0; c < 2; c++) mbar_wait(&acc_empty[(cseq + c) & 1u], (((cseq + c) >> 1) & 1u) ^ 1u);
+              fence_after();
+              for (int kb = 0; kb < ld.nkb; kb++) {
+                const uint32_t gst = gs % kSG;
+                mbar_wait(&gfull[gst], (gs / kSG) & 1u);
+#pragma unroll 1
+                for (int c = 0; c < 2; c++) {
+                  const uint32_t pst = ps % kSP;
+                  mbar_wait(&pfull[pst], (ps / kSP) & 1u);
+                  fence_after();
+                  const uint32_t d = tbase + ((cseq + c) & 1u) * 256u;
+                  const uint32_t abase = smem_u32(sG + gst * kABytes), bbase = smem_u32(sPW + pst * kWBytes);
+#pragma unroll
+                  for (int kk = 0; kk < 4; kk++) {
+                    const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
+                    const uint32_t acc = (kb | kk) ? 1u : 0u;
+                    if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
+                  }
+                  mma_commit(&pempty[pst]);
+                  ps++;
+                }
+                mma_commit(&gempty[gst]);
+                gs++;
+              }
+              mma_commit(&acc_full[cseq & 1u]);
+              mma_commit(&acc_full[(cseq + 1) & 1u]);
+              cseq += 2;
+            }
+            continue;
+          }
           for (int ch = 0; ch < ld.nchunks; ch++) {
             const uint32_t buf = cseq & 1u, aph = (cseq >> 1) & 1u;
             mbar_wait(&acc_empty[buf], aph ^ 1u);
@@ -313,7 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
     const LayerDesc& l1 = a.lay[1];
     for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info(a, t);
-      for (int ch = 0; ch < l1.nchunks; ch++)
+      const int passes = (l1.nchunks & 1) == 0 ? l1.nchunks / 2 : l1.nchunks;   // chunk pairs share A
+      for (int ch = 0; ch < passes; ch++)
         for (int kb = 0; kb < l1.nkb; kb++) {
           const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
           mbar_wait(&gempty[st], ph ^ 1u);
