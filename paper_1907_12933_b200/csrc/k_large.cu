@@ -416,6 +416,85 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
             tmem_ld_wait();
             uint32_t hw[16];                         // fp16 hi pairs (float) or u8 quads (int8)
             uint32_t lw[16];
+            if (fl) {
+              // float path, 32 neurons at once (the per-neuron form below stays for int8):
+              // bias / base potentials by vector loads, predicates as 32-bit words
+              const int nin = min(32, ld.n - j0);       // neurons of this chunk that exist
+              const uint32_t inmask = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
+              float u[32], ubv[32];
+              // (the bias rows are 16-byte aligned; a base-trace row is when its offset is)
+              if (nin == 32 && ((reinterpret_cast<uintptr_t>(ub_f + j0) | reinterpret_cast<uintptr_t>(bias_f + j0)) & 15u) == 0) {
+#pragma unroll
+                for (int q4 = 0; q4 < 8; q4++) {
+                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_f + j0) + q4);
+                  const float4 t4 = __ldg(reinterpret_cast<const float4*>(ub_f + j0) + q4);
+                  u[4 * q4] = __uint_as_float(v[4 * q4]) + b4.x;
+                  u[4 * q4 + 1] = __uint_as_float(v[4 * q4 + 1]) + b4.y;
+                  u[4 * q4 + 2] = __uint_as_float(v[4 * q4 + 2]) + b4.z;
+                  u[4 * q4 + 3] = __uint_as_float(v[4 * q4 + 3]) + b4.w;
+                  ubv[4 * q4] = t4.x; ubv[4 * q4 + 1] = t4.y; ubv[4 * q4 + 2] = t4.z; ubv[4 * q4 + 3] = t4.w;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                  const bool in = i < nin;
+                  u[i] = in ? __uint_as_float(v[i]) + __ldg(bias_f + j0 + i) : 0.f;
+                  ubv[i] = in ? __ldg(ub_f + j0 + i) : 0.f;
+                }
+              }
+              // sign words (reading C2: sign(u) = 1 iff u >= 0, so -0.0 counts as >= 0: + 0.0f)
+              uint32_t nu = 0, nb = 0, ng = 0;
+#pragma unroll
+              for (int i = 31; i >= 0; i--) {
+                nu = __funnelshift_l(__float_as_uint(u[i] + 0.0f), nu, 1);
+                nb = __funnelshift_l(__float_as_uint(ubv[i] + 0.0f), nb, 1);
+              }
+              const uint32_t scw = (nu ^ nb) & inmask;
+              nsc += __popc(scw);
+              if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
+              float dt[32];
+#pragma unroll
+              for (int i = 0; i < 32; i++) {
+                const bool in = i < nin;
+                const float d = fabsf(u[i] - ubv[i]);
+                if (in) {
+                  linf_f = fmaxf(linf_f, d);
+                  minab = fminf(minab, fminf(fabsf(u[i]), fabsf(ubv[i])));
+                }
+                dt[i] = d - tg_f;                      // value change <=> sign bit clear
+              }
+              if (pair_on) {
+#pragma unroll
+                for (int i = 31; i >= 0; i--) {
+                  ng = __funnelshift_l(__float_as_uint(dt[i]), ng, 1);
+                  if (i < nin) vcamb = fminf(vcamb, fabsf(dt[i]));
+                }
+                const uint32_t vcw = ~ng & ~scw & inmask;
+                pend[j0 >> 5] |= scw;
+                pend[16 + (j0 >> 5)] |= vcw;
+              }
+              if (eval && valid) {
+#pragma unroll
+                for (int i = 0; i < 32; i++)
+                  if (i < nin) static_cast<float*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j0 + i] = u[i];
+              }
+              if (l == L && j0 == 0) {
+#pragma unroll
+                for (int i = 0; i < MLPV_MAX_CLASSES; i++) if (i < nin) lg_f[i] = u[i];
+              }
+              if (l < L) {
+                // h = hi + lo, two fp16 (RN), reading C19
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                  const float h0 = fmaxf(u[2 * i], 0.f), h1 = fmaxf(u[2 * i + 1], 0.f);
+                  const __half2 hi2 = __floats2half2_rn(h0, h1);
+                  const float2 hf = __half22float2(hi2);
+                  const __half2 lo2 = __floats2half2_rn(h0 - hf.x, h1 - hf.y);
+                  hw[i] = *reinterpret_cast<const uint32_t*>(&hi2);
+                  lw[i] = *reinterpret_cast<const uint32_t*>(&lo2);
+                }
+              }
+            } else
 #pragma unroll
             for (int i = 0; i < 32; i++) {
               const int j = j0 + i;
