@@ -422,17 +422,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               const int nin = min(32, ld.n - j0);       // neurons of this chunk that exist
               const uint32_t inmask = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
               float u[32], ubv[32];
-              // (the bias rows are 16-byte aligned; a base-trace row is when its offset is)
-              if (nin == 32 && ((reinterpret_cast<uintptr_t>(ub_f + j0) | reinterpret_cast<uintptr_t>(bias_f + j0)) & 15u) == 0) {
+              // (the bias rows are 16-byte aligned; a base-trace row is 16- or 8-byte aligned
+              // depending on its base index and the trace length)
+              const uintptr_t ua = reinterpret_cast<uintptr_t>(ub_f + j0);
+              if (nin == 32 && ((reinterpret_cast<uintptr_t>(bias_f + j0) | (ua & 7u)) & 15u) == 0) {
 #pragma unroll
                 for (int q4 = 0; q4 < 8; q4++) {
                   const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_f + j0) + q4);
-                  const float4 t4 = __ldg(reinterpret_cast<const float4*>(ub_f + j0) + q4);
                   u[4 * q4] = __uint_as_float(v[4 * q4]) + b4.x;
                   u[4 * q4 + 1] = __uint_as_float(v[4 * q4 + 1]) + b4.y;
                   u[4 * q4 + 2] = __uint_as_float(v[4 * q4 + 2]) + b4.z;
                   u[4 * q4 + 3] = __uint_as_float(v[4 * q4 + 3]) + b4.w;
-                  ubv[4 * q4] = t4.x; ubv[4 * q4 + 1] = t4.y; ubv[4 * q4 + 2] = t4.z; ubv[4 * q4 + 3] = t4.w;
+                }
+                if ((ua & 15u) == 0) {
+#pragma unroll
+                  for (int q4 = 0; q4 < 8; q4++) {
+                    const float4 t4 = __ldg(reinterpret_cast<const float4*>(ub_f + j0) + q4);
+                    ubv[4 * q4] = t4.x; ubv[4 * q4 + 1] = t4.y; ubv[4 * q4 + 2] = t4.z; ubv[4 * q4 + 3] = t4.w;
+                  }
+                } else {
+#pragma unroll
+                  for (int q2 = 0; q2 < 16; q2++) {
+                    const float2 t2 = __ldg(reinterpret_cast<const float2*>(ub_f + j0) + q2);
+                    ubv[2 * q2] = t2.x; ubv[2 * q2 + 1] = t2.y;
+                  }
                 }
               } else {
 #pragma unroll
