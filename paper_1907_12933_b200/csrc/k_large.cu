@@ -507,57 +507,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
                   lw[i] = *reinterpret_cast<const uint32_t*>(&lo2);
                 }
               }
-            } else
+            } else {
+              // int8 path, 32 neurons at once: exact int32 potentials (reading C18)
+              const int nin = min(32, ld.n - j0);
+              const uint32_t inmask = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
+              int32_t u[32], ubv[32];
+              const uintptr_t ua = reinterpret_cast<uintptr_t>(ub_i + j0), ba = reinterpret_cast<uintptr_t>(bias_i + j0);
+              if (nin == 32 && ((ua | ba) & 15u) == 0) {
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-              const int j = j0 + i;
-              const bool in = j < ld.n;
-              if (fl) {
-                const float u = in ? __uint_as_float(v[i]) + __ldg(bias_f + j) : 0.f;
-                if (in) {
-                  const float ub = __ldg(ub_f + j);
-                  if (eval && valid) static_cast<float*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j] = u;
-                  const bool sc = (u >= 0.f) != (ub >= 0.f);
-                  if (sc) { if (istar < 0) istar = j; nsc++; }
-                  const float d = fabsf(u - ub);
-                  linf_f = fmaxf(linf_f, d);
-                  minab = fminf(minab, fminf(fabsf(u), fabsf(ub)));
-                  if (pair_on) {
-                    const bool vc = !sc && d >= tg_f;
-                    if (sc) pend[j >> 5] |= 1u << (j & 31);
-                    if (vc) pend[16 + (j >> 5)] |= 1u << (j & 31);
-                    vcamb = fminf(vcamb, fabsf(d - tg_f));
-                  }
-                  if (l == L && j < MLPV_MAX_CLASSES) lg_f[j] = u;
-                }
-                if (l < L) {
-                  const float h = fmaxf(u, 0.f);
-                  const __half hi = __float2half_rn(h);
-                  const __half lo = __float2half_rn(h - __half2float(hi));
-                  const uint32_t hb = (uint32_t)__half_as_ushort(hi), lb = (uint32_t)__half_as_ushort(lo);
-                  if (i & 1) { hw[i >> 1] |= hb << 16; lw[i >> 1] |= lb << 16; }
-                  else { hw[i >> 1] = hb; lw[i >> 1] = lb; }
+                for (int q4 = 0; q4 < 8; q4++) {
+                  const int4 b4 = __ldg(reinterpret_cast<const int4*>(bias_i + j0) + q4);
+                  const int4 t4 = __ldg(reinterpret_cast<const int4*>(ub_i + j0) + q4);
+                  u[4 * q4] = (int32_t)v[4 * q4] + b4.x;
+                  u[4 * q4 + 1] = (int32_t)v[4 * q4 + 1] + b4.y;
+                  u[4 * q4 + 2] = (int32_t)v[4 * q4 + 2] + b4.z;
+                  u[4 * q4 + 3] = (int32_t)v[4 * q4 + 3] + b4.w;
+                  ubv[4 * q4] = t4.x; ubv[4 * q4 + 1] = t4.y; ubv[4 * q4 + 2] = t4.z; ubv[4 * q4 + 3] = t4.w;
                 }
               } else {
-                const int32_t u = in ? (int32_t)v[i] + __ldg(bias_i + j) : 0;
-                if (in) {
-                  const int32_t ub = __ldg(ub_i + j);
-                  if (eval && valid) static_cast<int32_t*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j] = u;
-                  const bool sc = (u >= 0) != (ub >= 0);
-                  if (sc) { if (istar < 0) istar = j; nsc++; }
-                  const int32_t d = abs(u - ub);
-                  linf_i = max(linf_i, d);
-                  if (pair_on) {
-                    const bool vc = !sc && d >= tg_i;
-                    if (sc) pend[j >> 5] |= 1u << (j & 31);
-                    if (vc) pend[16 + (j >> 5)] |= 1u << (j & 31);
-                  }
-                  if (l == L && j < MLPV_MAX_CLASSES) lg_i[j] = u;
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                  const bool in = i < nin;
+                  u[i] = in ? (int32_t)v[i] + __ldg(bias_i + j0 + i) : 0;
+                  ubv[i] = in ? __ldg(ub_i + j0 + i) : 0;
                 }
-                if (l < L) {
-                  const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
-                  const uint32_t y = in ? (uint32_t)max(0, min(255, (u + rr) >> sh)) : 0u;
-                  if ((i & 3) == 0) hw[i >> 2] = y; else hw[i >> 2] |= y << (8 * (i & 3));
+              }
+              uint32_t nu = 0, nb = 0, ng = 0;
+#pragma unroll
+              for (int i = 31; i >= 0; i--) {
+                nu = __funnelshift_l((uint32_t)u[i], nu, 1);
+                nb = __funnelshift_l((uint32_t)ubv[i], nb, 1);
+              }
+              const uint32_t scw = (nu ^ nb) & inmask;
+              nsc += __popc(scw);
+              if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
+              int32_t dt[32];
+#pragma unroll
+              for (int i = 0; i < 32; i++) {
+                const int32_t d = abs(u[i] - ubv[i]);
+                if (i < nin) linf_i = max(linf_i, d);
+                dt[i] = d - tg_i;                      // value change <=> d - tg >= 0
+              }
+              if (pair_on) {
+#pragma unroll
+                for (int i = 31; i >= 0; i--) ng = __funnelshift_l((uint32_t)dt[i], ng, 1);
+                const uint32_t vcw = ~ng & ~scw & inmask;
+                pend[j0 >> 5] |= scw;
+                pend[16 + (j0 >> 5)] |= vcw;
+              }
+              if (eval && valid) {
+#pragma unroll
+                for (int i = 0; i < 32; i++)
+                  if (i < nin) static_cast<int32_t*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j0 + i] = u[i];
+              }
+              if (l == L && j0 == 0) {
+#pragma unroll
+                for (int i = 0; i < MLPV_MAX_CLASSES; i++) if (i < nin) lg_i[i] = u[i];
+              }
+              if (l < L) {
+                const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                  uint32_t w4 = 0;
+#pragma unroll
+                  for (int k = 0; k < 4; k++) {
+                    const int i = 4 * q + k;
+                    const uint32_t y = i < nin ? (uint32_t)max(0, min(255, (u[i] + rr) >> sh)) : 0u;
+                    w4 |= y << (8 * k);
+                  }
+                  hw[q] = w4;
                 }
               }
             }
