@@ -36,7 +36,9 @@ constexpr int kSG = 3;                    // generator ring stages
 constexpr int kSP = 3;                    // producer ring stages
 constexpr uint32_t kABytes = 128u * 128u; // A tile: 128 rows x 128 B
 constexpr uint32_t kWBytes = 256u * 128u; // W tile: up to 256 rows x 128 B
-constexpr int kThreads = 320;
+constexpr int kThreads = 512;                // 4 warpgroups: control, 2 x generator, epilogue
+constexpr int kRegLaunchL = 128, kRegCtlL = 80, kRegEpiL = 248;   // setmaxnreg budget: 3 x 80 + 248 <= 4 x 128
+static_assert(3 * kRegCtlL + kRegEpiL <= 4 * kRegLaunchL, "setmaxnreg budget");
 constexpr uint32_t kTmemCols = 512;       // two 256-column accumulator buffers
 constexpr int kPendWords = 32;            // per candidate: 16 sc + 16 vc words (upper width <= 512)
 constexpr size_t kSmemBytes = 1024 + kSG * kABytes + kSP * (kABytes + kWBytes) + (size_t)kM * kPendWords * 4;
@@ -247,127 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
   const uint32_t tbase = s_tbase;
   uint8_t* scratch = a.scratch + (size_t)blockIdx.x * a.scratch_per_cta;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------------- producer
-    if (lane == 0) {
-      uint32_t ps = 0, hph[kMaxL + 1] = {0};
-      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-        for (int l = 1; l <= L; l++) {
-          const LayerDesc& ld = a.lay[l];
-          const uint32_t wbytes = (uint32_t)ld.nc * 128u;
-          if (l >= 2) { mbar_wait(&h_ready[l - 1], hph[l - 1]); hph[l - 1] ^= 1u; }
-          // layer 1 with an even chunk count runs the chunks in pairs on one generated A stage:
-          // W stages in the order (pair, kb, chunk of the pair)
-          const bool paired = l == 1 && (ld.nchunks & 1) == 0;
-          for (int i = 0; i < ld.nchunks * ld.nkb; i++) {
-            const int ch = paired ? 2 * (i / (2 * ld.nkb)) + (i & 1) : i / ld.nkb;
-            const int kb = paired ? (i / 2) % ld.nkb : i % ld.nkb;
-            {
-              const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
-              mbar_wait(&pempty[st], ph ^ 1u);
-              mbar_expect_tx(&pfull[st], wbytes + (l >= 2 ? kABytes : 0u));
-              bulk_g2s(sPW + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wbytes, &pfull[st]);
-              if (l >= 2) bulk_g2s(sPA + st * kABytes, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
-              ps++;
-            }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      uint32_t gs = 0, ps = 0, cseq = 0;
-      const bool i8 = a.net.numeric == MLPV_NUM_INT8;
-      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-        for (int l = 1; l <= L; l++) {
-          const LayerDesc& ld = a.lay[l];
-          const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, l == 1 ? 1 : 0, l == 1 ? 1 : 0);
-          if (l == 1 && (ld.nchunks & 1) == 0) {
-            // chunk pairs: both accumulators, one generated A stage per K block (half the Philox work)
-            for (int cp = 0; cp < ld.nchunks / 2; cp++) {
-#pragma unroll
-              for (int c = 0; c < 2; c++) mbar_wait(&acc_empty[(cseq + c) & 1u], (((cseq + c) >> 1) & 1u) ^ 1u);
-              fence_after();
-              for (int kb = 0; kb < ld.nkb; kb++) {
-                const uint32_t gst = gs % kSG;
-                mbar_wait(&gfull[gst], (gs / kSG) & 1u);
-#pragma unroll 1
-                for (int c = 0; c < 2; c++) {
-                  const uint32_t pst = ps % kSP;
-                  mbar_wait(&pfull[pst], (ps / kSP) & 1u);
-                  fence_after();
-                  const uint32_t d = tbase + ((cseq + c) & 1u) * 256u;
-                  const uint32_t abase = smem_u32(sG + gst * kABytes), bbase = smem_u32(sPW + pst * kWBytes);
-#pragma unroll
-                  for (int kk = 0; kk < 4; kk++) {
-                    const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
-                    const uint32_t acc = (kb | kk) ? 1u : 0u;
-                    if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
-                  }
-                  mma_commit(&pempty[pst]);
-                  ps++;
-                }
-                mma_commit(&gempty[gst]);
-                gs++;
-              }
-              mma_commit(&acc_full[cseq & 1u]);
-              mma_commit(&acc_full[(cseq + 1) & 1u]);
-              cseq += 2;
-            }
-            continue;
-          }
-          for (int ch = 0; ch < ld.nchunks; ch++) {
-            const uint32_t buf = cseq & 1u, aph = (cseq >> 1) & 1u;
-            mbar_wait(&acc_empty[buf], aph ^ 1u);
-            fence_after();
-            const uint32_t d = tbase + buf * 256u;
-            for (int kb = 0; kb < ld.nkb; kb++) {
-              const uint32_t pst = ps % kSP;
-              mbar_wait(&pfull[pst], (ps / kSP) & 1u);
-              uint32_t gst = 0;
-              if (l == 1) { gst = gs % kSG; mbar_wait(&gfull[gst], (gs / kSG) & 1u); }
-              fence_after();
-              const uint32_t abase = smem_u32(l == 1 ? sG + gst * kABytes : sPA + pst * kABytes);
-              const uint32_t bbase = smem_u32(sPW + pst * kWBytes);
-#pragma unroll
-              for (int kk = 0; kk < 4; kk++) {
-                const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
-                const uint32_t acc = (kb | kk) ? 1u : 0u;
-                if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
-              }
-              mma_commit(&pempty[pst]);
-              if (l == 1) { mma_commit(&gempty[gst]); gs++; }
-              ps++;
-            }
-            mma_commit(&acc_full[buf]);
-            cseq++;
-          }
-        }
-      }
-    }
-  } else if (warp < 6) {
-    // ------------------------------------------------------------------- generator
-    const int r = threadIdx.x - 64;
-    uint32_t gs = 0;
-    const LayerDesc& l1 = a.lay[1];
-    for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-      const TileInfo ti = tile_info(a, t);
-      const int passes = (l1.nchunks & 1) == 0 ? l1.nchunks / 2 : l1.nchunks;   // chunk pairs share A
-      for (int ch = 0; ch < passes; ch++)
-        for (int kb = 0; kb < l1.nkb; kb++) {
-          const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
-          mbar_wait(&gempty[st], ph ^ 1u);
-          gen_block(a, ti, r, kb, sG + st * kABytes);
-          fence_proxy_async();
-          named_bar(1, 128);
-          if (r == 0) mbar_arrive(&gfull[st]);
-          gs++;
-        }
-    }
-  } else {
+  if ((warp >> 2) == 3) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpiL));
     // ------------------------------------------------------------------- epilogue
-    const int e = threadIdx.x - 192;
+    const int e = threadIdx.x - 384;
     const int quad = warp & 3;
     const int r = 32 * quad + lane;                  // candidate row = TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
@@ -710,6 +595,130 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
       }
       (void)cidx;
     }
+    } else {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtlL));
+  if (warp == 0) {
+    // ------------------------------------------------------------------- producer
+    if (lane == 0) {
+      uint32_t ps = 0, hph[kMaxL + 1] = {0};
+      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        for (int l = 1; l <= L; l++) {
+          const LayerDesc& ld = a.lay[l];
+          const uint32_t wbytes = (uint32_t)ld.nc * 128u;
+          if (l >= 2) { mbar_wait(&h_ready[l - 1], hph[l - 1]); hph[l - 1] ^= 1u; }
+          // layer 1 with an even chunk count runs the chunks in pairs on one generated A stage:
+          // W stages in the order (pair, kb, chunk of the pair)
+          const bool paired = l == 1 && (ld.nchunks & 1) == 0;
+          for (int i = 0; i < ld.nchunks * ld.nkb; i++) {
+            const int ch = paired ? 2 * (i / (2 * ld.nkb)) + (i & 1) : i / ld.nkb;
+            const int kb = paired ? (i / 2) % ld.nkb : i % ld.nkb;
+            {
+              const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
+              mbar_wait(&pempty[st], ph ^ 1u);
+              mbar_expect_tx(&pfull[st], wbytes + (l >= 2 ? kABytes : 0u));
+              bulk_g2s(sPW + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wbytes, &pfull[st]);
+              if (l >= 2) bulk_g2s(sPA + st * kABytes, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
+              ps++;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      uint32_t gs = 0, ps = 0, cseq = 0;
+      const bool i8 = a.net.numeric == MLPV_NUM_INT8;
+      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        for (int l = 1; l <= L; l++) {
+          const LayerDesc& ld = a.lay[l];
+          const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, l == 1 ? 1 : 0, l == 1 ? 1 : 0);
+          if (l == 1 && (ld.nchunks & 1) == 0) {
+            // chunk pairs: both accumulators, one generated A stage per K block (half the Philox work)
+            for (int cp = 0; cp < ld.nchunks / 2; cp++) {
+#pragma unroll
+              for (int c = 0; c < 2; c++) mbar_wait(&acc_empty[(cseq + c) & 1u], (((cseq + c) >> 1) & 1u) ^ 1u);
+              fence_after();
+              for (int kb = 0; kb < ld.nkb; kb++) {
+                const uint32_t gst = gs % kSG;
+                mbar_wait(&gfull[gst], (gs / kSG) & 1u);
+#pragma unroll 1
+                for (int c = 0; c < 2; c++) {
+                  const uint32_t pst = ps % kSP;
+                  mbar_wait(&pfull[pst], (ps / kSP) & 1u);
+                  fence_after();
+                  const uint32_t d = tbase + ((cseq + c) & 1u) * 256u;
+                  const uint32_t abase = smem_u32(sG + gst * kABytes), bbase = smem_u32(sPW + pst * kWBytes);
+#pragma unroll
+                  for (int kk = 0; kk < 4; kk++) {
+                    const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
+                    const uint32_t acc = (kb | kk) ? 1u : 0u;
+                    if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
+                  }
+                  mma_commit(&pempty[pst]);
+                  ps++;
+                }
+                mma_commit(&gempty[gst]);
+                gs++;
+              }
+              mma_commit(&acc_full[cseq & 1u]);
+              mma_commit(&acc_full[(cseq + 1) & 1u]);
+              cseq += 2;
+            }
+            continue;
+          }
+          for (int ch = 0; ch < ld.nchunks; ch++) {
+            const uint32_t buf = cseq & 1u, aph = (cseq >> 1) & 1u;
+            mbar_wait(&acc_empty[buf], aph ^ 1u);
+            fence_after();
+            const uint32_t d = tbase + buf * 256u;
+            for (int kb = 0; kb < ld.nkb; kb++) {
+              const uint32_t pst = ps % kSP;
+              mbar_wait(&pfull[pst], (ps / kSP) & 1u);
+              uint32_t gst = 0;
+              if (l == 1) { gst = gs % kSG; mbar_wait(&gfull[gst], (gs / kSG) & 1u); }
+              fence_after();
+              const uint32_t abase = smem_u32(l == 1 ? sG + gst * kABytes : sPA + pst * kABytes);
+              const uint32_t bbase = smem_u32(sPW + pst * kWBytes);
+#pragma unroll
+              for (int kk = 0; kk < 4; kk++) {
+                const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
+                const uint32_t acc = (kb | kk) ? 1u : 0u;
+                if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
+              }
+              mma_commit(&pempty[pst]);
+              if (l == 1) { mma_commit(&gempty[gst]); gs++; }
+              ps++;
+            }
+            mma_commit(&acc_full[buf]);
+            cseq++;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------- generator
+    // two groups (warpgroups 1 and 2) take the ring stages in turn
+    const int ggrp = (warp >> 2) - 1;
+    const int r = threadIdx.x - 128 * (warp >> 2);
+    uint32_t gs = 0;
+    const LayerDesc& l1 = a.lay[1];
+    for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+      const TileInfo ti = tile_info(a, t);
+      const int passes = (l1.nchunks & 1) == 0 ? l1.nchunks / 2 : l1.nchunks;   // chunk pairs share A
+      for (int ch = 0; ch < passes; ch++)
+        for (int kb = 0; kb < l1.nkb; kb++) {
+          if ((int)(gs & 1u) != ggrp) { gs++; continue; }
+          const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
+          mbar_wait(&gempty[st], ph ^ 1u);
+          gen_block(a, ti, r, kb, sG + st * kABytes);
+          fence_proxy_async();
+          named_bar(ggrp ? 3 : 1, 128);
+          if (r == 0) mbar_arrive(&gfull[st]);
+          gs++;
+        }
+    }
+  }
   }
   fence_before();
   __syncthreads();
