@@ -33,6 +33,46 @@ __device__ __forceinline__ int32_t wload_i(const void* W, int numeric, size_t i)
   if (numeric == MLPV_NUM_Q4_12) return static_cast<const int16_t*>(W)[i];
   return static_cast<const int8_t*>(W)[i];
 }
+// lane's partial dot product of weight row `row` (fan-in `fan`) with the activations in shared
+// memory: 8 bf16 / 16 int8 weights per 16-byte load when the row allows it, element-wise otherwise
+__device__ __forceinline__ float row_dot_f(const void* W, int numeric, int row, int fan, const float* h, int lane) {
+  float acc = 0.f;
+  if (numeric == MLPV_NUM_BF16 && (fan & 7) == 0) {
+    const uint4* wr = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(W) + (size_t)row * fan);
+    for (int q = lane; q < (fan >> 3); q += 32) {
+      const uint4 w8 = __ldg(wr + q);
+      const float4 h0 = reinterpret_cast<const float4*>(h)[2 * q], h1 = reinterpret_cast<const float4*>(h)[2 * q + 1];
+      acc = fmaf(__uint_as_float(w8.x << 16), h0.x, acc);
+      acc = fmaf(__uint_as_float(w8.x & 0xFFFF0000u), h0.y, acc);
+      acc = fmaf(__uint_as_float(w8.y << 16), h0.z, acc);
+      acc = fmaf(__uint_as_float(w8.y & 0xFFFF0000u), h0.w, acc);
+      acc = fmaf(__uint_as_float(w8.z << 16), h1.x, acc);
+      acc = fmaf(__uint_as_float(w8.z & 0xFFFF0000u), h1.y, acc);
+      acc = fmaf(__uint_as_float(w8.w << 16), h1.z, acc);
+      acc = fmaf(__uint_as_float(w8.w & 0xFFFF0000u), h1.w, acc);
+    }
+    return acc;
+  }
+  for (int j = lane; j < fan; j += 32) acc = fmaf(wload_f(W, numeric, (size_t)row * fan + j), h[j], acc);
+  return acc;
+}
+__device__ __forceinline__ int32_t row_dot_i(const void* W, int numeric, int row, int fan, const int32_t* h, int lane) {
+  int32_t acc = 0;
+  if (numeric == MLPV_NUM_INT8 && (fan & 15) == 0) {
+    const uint4* wr = reinterpret_cast<const uint4*>(static_cast<const int8_t*>(W) + (size_t)row * fan);
+    for (int q = lane; q < (fan >> 4); q += 32) {
+      const uint4 w16 = __ldg(wr + q);
+      const uint32_t ws[4] = {w16.x, w16.y, w16.z, w16.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc += (int32_t)(int8_t)(ws[k] >> (8 * b)) * h[16 * q + 4 * k + b];
+    }
+    return acc;
+  }
+  for (int j = lane; j < fan; j += 32) acc += wload_i(W, numeric, (size_t)row * fan + j) * h[j];
+  return acc;
+}
 __device__ __forceinline__ float in_f(const void* x, int numeric, size_t i) {
   if (numeric == MLPV_NUM_FP32) return static_cast<const float*>(x)[i];
   return __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(x)[i]) << 16);
@@ -111,8 +151,7 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
     const int nl = net.sizes[l], fan = net.sizes[l - 1];
     for (int i = wid; i < nl; i += nw) {
       if (fixed) {
-        int32_t acc = 0;
-        for (int j = lane; j < fan; j += 32) acc += wload_i(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hi[j];
+        int32_t acc = row_dot_i(net.W[l - 1], net.numeric, i, fan, hi, lane);
         acc = __reduce_add_sync(0xffffffffu, acc);
         if (lane == 0) {
           acc += static_cast<const int32_t*>(net.b[l - 1])[i];
@@ -120,8 +159,7 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
           if (l < net.L) hin[i] = act_fixed(net.numeric, net.act, acc, net.shift[l - 1], net.knots);
         }
       } else {
-        float acc = 0.f;
-        for (int j = lane; j < fan; j += 32) acc = fmaf(wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j), hf[j], acc);
+        float acc = row_dot_f(net.W[l - 1], net.numeric, i, fan, hf, lane);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
