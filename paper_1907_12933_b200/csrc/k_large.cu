@@ -68,6 +68,8 @@ struct LargeArgs {
   int eval_base;
   void* eval_out;
   int pair_of_lower[kMaxL + 1];    // pair index whose lower layer is k, or -1
+  int soff[kMaxL + 2];             // staged bias / base potentials: layer l at [soff[l], soff[l+1]) (x4 aligned)
+  int staged;                      // 1: biases and the tile's base potentials live in shared memory
 };
 
 struct TileInfo {
@@ -243,6 +245,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
   }
   if (warp == 1) { tmem_alloc(&s_tbase, kTmemCols); tmem_relinquish(); }
   for (int i = threadIdx.x; i < kM * kPendWords; i += blockDim.x) s_pend[i] = 0;
+  // biases of every layer (32-bit float or int) once; the base potentials per tile (epilogue)
+  uint32_t* s_bias = s_pend + kM * kPendWords;
+  uint32_t* s_ub = s_bias + a.soff[a.net.L + 1];
+  if (a.staged)
+    for (int l = 1; l <= L; l++)
+      for (int j = threadIdx.x; j < a.net.sizes[l]; j += blockDim.x)
+        s_bias[a.soff[l] + j] = static_cast<const uint32_t*>(a.net.b[l - 1])[j];
   fence_before();
   __syncthreads();
   fence_after();
@@ -265,6 +274,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
       const TileInfo ti = tile_info(a, t);
       const bool valid = r < ti.nvalid;
       const uint64_t cidx = row_index(a, ti, r);
+      if (a.staged) {                              // this tile's base potentials (the previous tile's
+        const uint32_t* tr = static_cast<const uint32_t*>(a.ws.trace) + (size_t)ti.b * T;   // reads ended
+        for (int l = 1; l <= L; l++)                                                         // at its last
+          for (int j = e; j < a.net.sizes[l]; j += 128) s_ub[a.soff[l] + j] = tr[a.net.loff[l] + j];   // barrier)
+        named_bar(2, 128);
+      }
       // per-layer summaries of the previous layer (lower layer of the pair being finished)
       int p_nsc = 0, p_istar = -1;
       bool p_cond = false, p_amb = false;
@@ -282,10 +297,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         int nsc = 0, istar = -1;
         float linf_f = 0.f, minab = 3.0e38f, vcamb = 3.0e38f;
         int32_t linf_i = 0;
-        const float* bias_f = static_cast<const float*>(a.net.b[l - 1]);
-        const int32_t* bias_i = static_cast<const int32_t*>(a.net.b[l - 1]);
-        const float* ub_f = static_cast<const float*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
-        const int32_t* ub_i = static_cast<const int32_t*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
+        const float* bias_f = a.staged ? reinterpret_cast<const float*>(s_bias + a.soff[l]) : static_cast<const float*>(a.net.b[l - 1]);
+        const int32_t* bias_i = a.staged ? reinterpret_cast<const int32_t*>(s_bias + a.soff[l]) : static_cast<const int32_t*>(a.net.b[l - 1]);
+        const float* ub_f = a.staged ? reinterpret_cast<const float*>(s_ub + a.soff[l])
+                                     : static_cast<const float*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
+        const int32_t* ub_i = a.staged ? reinterpret_cast<const int32_t*>(s_ub + a.soff[l])
+                                       : static_cast<const int32_t*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
         uint8_t* hdst = scratch + a.h_off[l];
         const int sh = a.net.shift[l - 1];
         for (int ch = 0; ch < ld.nchunks; ch++) {
@@ -313,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               if (nin == 32 && ((reinterpret_cast<uintptr_t>(bias_f + j0) | (ua & 7u)) & 15u) == 0) {
 #pragma unroll
                 for (int q4 = 0; q4 < 8; q4++) {
-                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias_f + j0) + q4);
+                  const float4 b4 = reinterpret_cast<const float4*>(bias_f + j0)[q4];
                   u[4 * q4] = __uint_as_float(v[4 * q4]) + b4.x;
                   u[4 * q4 + 1] = __uint_as_float(v[4 * q4 + 1]) + b4.y;
                   u[4 * q4 + 2] = __uint_as_float(v[4 * q4 + 2]) + b4.z;
@@ -322,13 +339,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
                 if ((ua & 15u) == 0) {
 #pragma unroll
                   for (int q4 = 0; q4 < 8; q4++) {
-                    const float4 t4 = __ldg(reinterpret_cast<const float4*>(ub_f + j0) + q4);
+                    const float4 t4 = reinterpret_cast<const float4*>(ub_f + j0)[q4];
                     ubv[4 * q4] = t4.x; ubv[4 * q4 + 1] = t4.y; ubv[4 * q4 + 2] = t4.z; ubv[4 * q4 + 3] = t4.w;
                   }
                 } else {
 #pragma unroll
                   for (int q2 = 0; q2 < 16; q2++) {
-                    const float2 t2 = __ldg(reinterpret_cast<const float2*>(ub_f + j0) + q2);
+                    const float2 t2 = reinterpret_cast<const float2*>(ub_f + j0)[q2];
                     ubv[2 * q2] = t2.x; ubv[2 * q2 + 1] = t2.y;
                   }
                 }
@@ -336,8 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                   const bool in = i < nin;
-                  u[i] = in ? __uint_as_float(v[i]) + __ldg(bias_f + j0 + i) : 0.f;
-                  ubv[i] = in ? __ldg(ub_f + j0 + i) : 0.f;
+                  u[i] = in ? __uint_as_float(v[i]) + bias_f[j0 + i] : 0.f;
+                  ubv[i] = in ? ub_f[j0 + i] : 0.f;
                 }
               }
               // sign words (reading C2: sign(u) = 1 iff u >= 0, so -0.0 counts as >= 0: + 0.0f)
@@ -401,8 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               if (nin == 32 && ((ua | ba) & 15u) == 0) {
 #pragma unroll
                 for (int q4 = 0; q4 < 8; q4++) {
-                  const int4 b4 = __ldg(reinterpret_cast<const int4*>(bias_i + j0) + q4);
-                  const int4 t4 = __ldg(reinterpret_cast<const int4*>(ub_i + j0) + q4);
+                  const int4 b4 = reinterpret_cast<const int4*>(bias_i + j0)[q4];
+                  const int4 t4 = reinterpret_cast<const int4*>(ub_i + j0)[q4];
                   u[4 * q4] = (int32_t)v[4 * q4] + b4.x;
                   u[4 * q4 + 1] = (int32_t)v[4 * q4 + 1] + b4.y;
                   u[4 * q4 + 2] = (int32_t)v[4 * q4 + 2] + b4.z;
@@ -413,8 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                   const bool in = i < nin;
-                  u[i] = in ? (int32_t)v[i] + __ldg(bias_i + j0 + i) : 0;
-                  ubv[i] = in ? __ldg(ub_i + j0 + i) : 0;
+                  u[i] = in ? (int32_t)v[i] + bias_i[j0 + i] : 0;
+                  ubv[i] = in ? ub_i[j0 + i] : 0;
                 }
               }
               uint32_t nu = 0, nb = 0, ng = 0;
@@ -898,9 +915,14 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* b
     g_scratch_size = need;
   }
   a.scratch = g_scratch;
-  cudaError_t e = cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  a.soff[1] = 0;
+  for (int l = 1; l <= net.L; l++) a.soff[l + 1] = a.soff[l] + ((net.sizes[l] + 3) & ~3);
+  const size_t stage_bytes = (size_t)2 * a.soff[net.L + 1] * 4;
+  a.staged = kSmemBytes + stage_bytes <= (size_t)227 * 1024 ? 1 : 0;
+  const size_t smem = kSmemBytes + (a.staged ? stage_bytes : 0);
+  cudaError_t e = cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_large<<<grid, kThreads, kSmemBytes, st>>>(a);
+  k_large<<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
