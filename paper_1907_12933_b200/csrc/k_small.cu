@@ -243,6 +243,8 @@ struct SmallArgs {
   int eval_base;
   void* eval_out;             // [eval_n x T]
   int tbl_in_smem;            // delta table of the block's base staged in smem
+  int ds;                     // row stride of the delta table as read: n1 (global) or n1 | 1 (smem:
+                              // an odd stride puts the rows the lanes of a warp read in different banks)
 };
 
 __device__ __forceinline__ uint32_t dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, int32_t c) {
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
   int16_t* s_knots = reinterpret_cast<int16_t*>(take(net.knots ? 129 * 2 : 0));
   uint32_t* s_cov = reinterpret_cast<uint32_t*>(take(eval ? 0 : 4 * (size_t)a.cov.n_words * (FL ? 2 : 1)));
   const size_t per_base = (size_t)a.ws.S * q * n1;
-  P* s_delta = reinterpret_cast<P*>(take(a.tbl_in_smem ? sizeof(P) * per_base : 0));
+  P* s_delta = reinterpret_cast<P*>(take(a.tbl_in_smem ? sizeof(P) * (per_base / n1) * a.ds : 0));
   __shared__ unsigned long long s_cnt[3];
   __shared__ unsigned long long s_cex[2];
 
@@ -462,7 +464,8 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
     if (net.knots) for (int t = threadIdx.x; t < 129; t += blockDim.x) s_knots[t] = net.knots[t];
     if (!eval) for (int t = threadIdx.x; t < (int)a.cov.n_words * (FL ? 2 : 1); t += blockDim.x) s_cov[t] = 0;
     if (a.tbl_in_smem)
-      for (size_t t = threadIdx.x; t < per_base; t += blockDim.x) s_delta[t] = static_cast<const P*>(a.ws.delta)[(size_t)b * per_base + t];
+      for (size_t t = threadIdx.x; t < per_base; t += blockDim.x)
+        s_delta[(t / n1) * a.ds + t % n1] = static_cast<const P*>(a.ws.delta)[(size_t)b * per_base + t];
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
     if (threadIdx.x < 2) s_cex[threadIdx.x] = kNone;
   }
@@ -504,24 +507,47 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
         const int li = rem / q, lj = rem % q;
         int pi, pj;
         unrank_pair(pr, n0, pi, pj);
-        const P* d0 = delta + ((size_t)pi * q + li) * n1;
-        const P* d1 = delta + ((size_t)pj * q + lj) * n1;
+        const P* d0 = delta + ((size_t)pi * q + li) * a.ds;
+        const P* d1 = delta + ((size_t)pj * q + lj) * a.ds;
 #pragma unroll
         for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i] + d1[i];
       } else {
         const int pi = (int)(c / q), li = (int)(c % q);
-        const P* d0 = delta + ((size_t)pi * q + li) * n1;
+        const P* d0 = delta + ((size_t)pi * q + li) * a.ds;
 #pragma unroll
         for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i];
       }
     } else {
-      uint64_t cc = c;
-      for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
-        const int d = (int)(cc % (uint64_t)q);
-        cc /= (uint64_t)q;
-        const P* dk = delta + ((size_t)k * q + d) * n1;
+      // mixed-radix digits, least significant first: shifts for a power-of-two q, 32-bit
+      // division when the index fits, 64-bit otherwise (warp-uniform choice)
+      const int qb = __ffs(q) - 1;
+      if ((q & (q - 1)) == 0) {
+        uint64_t cc = c;
+        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
+          const int d = (int)(cc & (uint64_t)(q - 1));
+          cc >>= qb;
+          const P* dk = delta + ((size_t)k * q + d) * a.ds;
 #pragma unroll
-        for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+        }
+      } else if (c < (1ull << 32)) {
+        uint32_t cc = (uint32_t)c;
+        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
+          const int d = (int)(cc % (uint32_t)q);
+          cc /= (uint32_t)q;
+          const P* dk = delta + ((size_t)k * q + d) * a.ds;
+#pragma unroll
+          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+        }
+      } else {
+        uint64_t cc = c;
+        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
+          const int d = (int)(cc % (uint64_t)q);
+          cc /= (uint64_t)q;
+          const P* dk = delta + ((size_t)k * q + d) * a.ds;
+#pragma unroll
+          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+        }
       }
     }
     // ---- a5/a6: hidden activations and dense layers
@@ -647,8 +673,10 @@ static cudaError_t run_small(SmallArgs& a, int num_sms, cudaStream_t st) {
   if (net.knots) smem += al(129 * 2);
   const bool eval = a.eval_idx != nullptr;
   if (!eval) smem += al(4 * (size_t)a.cov.n_words * (NUM == MLPV_NUM_FP32 ? 2 : 1));
-  const size_t tbl = sizeof(P) * (size_t)a.ws.S * a.pert.n_levels * n1;
+  const int n1s = n1 | 1;
+  const size_t tbl = sizeof(P) * (size_t)a.ws.S * a.pert.n_levels * n1s;
   a.tbl_in_smem = (smem + al(tbl) <= 160 * 1024) ? 1 : 0;
+  a.ds = a.tbl_in_smem ? n1s : n1;
   if (a.tbl_in_smem) smem += al(tbl);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
   auto kern = k_small<NUM, L, M1, M2, M3>;
