@@ -139,8 +139,21 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
     const int n1 = net.sizes[1];
     for (int i = wid; i < n1; i += nw) {
       double acc = 0.0;
-      for (int j = lane; j < n0; j += 32)
-        acc += (double)wload_f(net.W[0], net.numeric, (size_t)i * n0 + j) * ((double)hf[j] + pert.origin_d);
+      if (net.numeric == MLPV_NUM_BF16 && (n0 & 7) == 0) {          // 8 bf16 weights per 16-byte load
+        const uint4* wr = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(net.W[0]) + (size_t)i * n0);
+        for (int qq = lane; qq < (n0 >> 3); qq += 32) {
+          const uint4 w8 = __ldg(wr + qq);
+          const uint32_t ws[4] = {w8.x, w8.y, w8.z, w8.w};
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            acc += (double)__uint_as_float(ws[k] << 16) * ((double)hf[8 * qq + 2 * k] + pert.origin_d);
+            acc += (double)__uint_as_float(ws[k] & 0xFFFF0000u) * ((double)hf[8 * qq + 2 * k + 1] + pert.origin_d);
+          }
+        }
+      } else {
+        for (int j = lane; j < n0; j += 32)
+          acc += (double)wload_f(net.W[0], net.numeric, (size_t)i * n0 + j) * ((double)hf[j] + pert.origin_d);
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) ws.base1[(size_t)b * n1 + i] = (float)(acc + (double)static_cast<const float*>(net.b[0])[i]);
