@@ -137,11 +137,15 @@ typedef struct {
  *   TARGET_NEVER       violated iff class(x') == target.
  *   THRESHOLD_LITERAL  violated iff y_D < V and y_i > V for some i != D (l_image_misclassified,
  *                      existential reading), D = target, or the base class if target < 0;
- *                      V in real units. */
+ *                      V in real units.
+ *   THRESHOLD_LITERAL_ALL  the universal reading of the same literal (SURVEY
+ *                      NEXT-4): violated iff y_D < V and y_i > V for every i != D.
+ * Float numerics flag a candidate for the literal forms when some |y_i - V| < near_tie. */
 typedef enum {
     MLPV_PROP_ARGMAX_UNCHANGED = 0,
     MLPV_PROP_TARGET_NEVER = 1,
-    MLPV_PROP_THRESHOLD_LITERAL = 2
+    MLPV_PROP_THRESHOLD_LITERAL = 2,
+    MLPV_PROP_THRESHOLD_LITERAL_ALL = 3
 } mlpv_prop_kind;
 
 typedef struct { mlpv_prop_kind kind; int32_t target; double V; } mlpv_property;

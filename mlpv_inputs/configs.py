@@ -19,7 +19,7 @@ import numpy as np
 NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8 = 0, 1, 2, 3
 ACT_SIGMOID, ACT_PL_SIGMOID, ACT_RELU = 0, 1, 2
 PERT_TUPLE_REPLACE, PERT_SUBSET_OFFSET, PERT_SUBSET_REPLACE, PERT_PHILOX_LATTICE, PERT_PHILOX_BOX = 0, 1, 2, 3, 4
-PROP_ARGMAX_UNCHANGED, PROP_TARGET_NEVER, PROP_THRESHOLD_LITERAL = 0, 1, 2
+PROP_ARGMAX_UNCHANGED, PROP_TARGET_NEVER, PROP_THRESHOLD_LITERAL, PROP_THRESHOLD_LITERAL_ALL = 0, 1, 2, 3
 
 CONFIG_IDS = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5_bf16", "cfg5_int8"]
 

@@ -36,7 +36,7 @@
 enum { O_FP32 = 0, O_BF16 = 1, O_Q412 = 2, O_INT8 = 3 };
 enum { O_SIGMOID = 0, O_PLSIG = 1, O_RELU = 2 };
 enum { O_TUPLE = 0, O_SUB_OFF = 1, O_SUB_REP = 2, O_PHILOX = 3, O_BOX = 4 };
-enum { O_UNCHANGED = 0, O_TARGET = 1, O_LITERAL = 2 };
+enum { O_UNCHANGED = 0, O_TARGET = 1, O_LITERAL = 2, O_LITERAL_ALL = 3 };
 
 typedef struct {
     int32_t L;
@@ -472,16 +472,18 @@ static int property_eval(const oprop *pr, const double *y, int n, int base_cls, 
                          int float_path, double near_tie, int *flag) {
     int cls = argmax_of(y, n);
     *flag = 0;
-    if (pr->kind == O_LITERAL) {
+    if (pr->kind == O_LITERAL || pr->kind == O_LITERAL_ALL) {
         /* l_image_misclassified <=> (n_D < V) and (n_i > V) for some i != D (PAPER.md:487-489,
-         * existential reading C12); D = target, or the base class if target < 0 */
+         * existential reading C12) or, O_LITERAL_ALL, for every i != D (the universal reading,
+         * SURVEY NEXT-4); D = target, or the base class if target < 0 */
         int D = pr->target >= 0 ? pr->target : base_cls;
-        int any = 0;
+        int any = 0, all = 1;
         for (int i = 0; i < n; i++) {
             if (i != D && y[i] > V) any = 1;
+            if (i != D && !(y[i] > V)) all = 0;
             if (float_path && fabs(y[i] - V) < near_tie) *flag = 1;
         }
-        return (y[D] < V) && any;
+        return (y[D] < V) && (pr->kind == O_LITERAL_ALL ? all : any);
     }
     if (float_path) {
         double top1 = y[cls], top2 = -INFINITY;

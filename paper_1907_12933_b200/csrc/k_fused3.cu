@@ -1087,18 +1087,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 #pragma unroll
         for (int i = 1; i < 16; i++) if (i < n3 && y[i] > top1) { top1 = y[i]; cls = i; }
         bool viol = false, flag = false;
-        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
           const int D = a.prop.target >= 0 ? a.prop.target : bcls;
-          bool any = false;
+          bool any = false, all = true;
           float yD = 0.f;
 #pragma unroll
           for (int i = 0; i < 16; i++)
             if (i < n3) {
               if (i == D) yD = y[i];
               if (i != D && y[i] > a.prop.V_f) any = true;
+              if (i != D && !(y[i] > a.prop.V_f)) all = false;
               if (fabsf(y[i] - a.prop.V_f) < a.cov.near_tie) flag = true;
             }
-          viol = yD < a.prop.V_f && any;
+          viol = yD < a.prop.V_f && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? all : any);
         } else {
           float top2 = -3.0e38f;
 #pragma unroll

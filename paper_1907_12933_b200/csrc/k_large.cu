@@ -555,18 +555,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         float top1 = lg_f[0];
 #pragma unroll
         for (int i = 1; i < MLPV_MAX_CLASSES; i++) if (i < nL && lg_f[i] > top1) { top1 = lg_f[i]; cls = i; }
-        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
           const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
-          bool any = false;
+          bool any = false, all = true;
           float yD = 0.f;
 #pragma unroll
           for (int i = 0; i < MLPV_MAX_CLASSES; i++)
             if (i < nL) {
               if (i == D) yD = lg_f[i];
               if (i != D && lg_f[i] > a.prop.V_f) any = true;
+              if (i != D && !(lg_f[i] > a.prop.V_f)) all = false;
               if (fabsf(lg_f[i] - a.prop.V_f) < a.cov.near_tie) flag = true;
             }
-          viol = yD < a.prop.V_f && any;
+          viol = yD < a.prop.V_f && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? all : any);
         } else {
           float top2 = -3.0e38f;
 #pragma unroll
@@ -578,18 +579,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         int32_t top1 = lg_i[0];
 #pragma unroll
         for (int i = 1; i < MLPV_MAX_CLASSES; i++) if (i < nL && lg_i[i] > top1) { top1 = lg_i[i]; cls = i; }
-        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
           const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
           const int32_t V = (int32_t)a.prop.V_i;
-          bool any = false;
+          bool any = false, all = true;
           int32_t yD = 0;
 #pragma unroll
           for (int i = 0; i < MLPV_MAX_CLASSES; i++)
             if (i < nL) {
               if (i == D) yD = lg_i[i];
               if (i != D && lg_i[i] > V) any = true;
+              if (i != D && !(lg_i[i] > V)) all = false;
             }
-          viol = yD < V && any;
+          viol = yD < V && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? all : any);
         } else {
           viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != base_cls;
         }

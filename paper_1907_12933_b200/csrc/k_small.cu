@@ -594,20 +594,21 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
 #pragma unroll
     for (int i = 1; i < MY; i++) if (i < nL && Y[i] > top1) { top1 = Y[i]; cls = i; }
     bool viol, flag = false;
-    if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL) {
+    if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
       const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
       const P V = FL ? (P)a.prop.V_f : (P)a.prop.V_i;
-      bool any = false;
+      bool any = false, all = true;
       P yD = Y[0];
 #pragma unroll
       for (int i = 0; i < MY; i++) {
         if (i < nL) {
           if (i == D) yD = Y[i];
           if (i != D && Y[i] > V) any = true;
+          if (i != D && !(Y[i] > V)) all = false;
           if (FL && fabsf((float)(Y[i] - V)) < a.cov.near_tie) flag = true;
         }
       }
-      viol = (yD < V) && any;
+      viol = (yD < V) && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? all : any);
     } else {
       if constexpr (FL) {
         float top2 = -3.0e38f;

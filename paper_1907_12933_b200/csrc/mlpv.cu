@@ -366,9 +366,9 @@ static mlpv_status build_prop(mlpv_ctx* h, const mlpv_property* pr, DevProp* d) 
   memset(d, 0, sizeof *d);
   if (!pr) return fail(h, MLPV_E_INVALID, "property is NULL");
   const int nL = h->net.sizes[h->net.L];
-  if (pr->kind < 0 || pr->kind > 2) return fail(h, MLPV_E_INVALID, "prop.kind = %d", (int)pr->kind);
+  if (pr->kind < 0 || pr->kind > 3) return fail(h, MLPV_E_INVALID, "prop.kind = %d", (int)pr->kind);
   if (pr->kind == MLPV_PROP_TARGET_NEVER && (pr->target < 0 || pr->target >= nL)) return fail(h, MLPV_E_INVALID, "prop.target = %d (n_L = %d)", pr->target, nL);
-  if (pr->kind == MLPV_PROP_THRESHOLD_LITERAL && pr->target >= nL) return fail(h, MLPV_E_INVALID, "prop.target = %d (n_L = %d)", pr->target, nL);
+  if ((pr->kind == MLPV_PROP_THRESHOLD_LITERAL || pr->kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) && pr->target >= nL) return fail(h, MLPV_E_INVALID, "prop.target = %d (n_L = %d)", pr->target, nL);
   if (!std::isfinite(pr->V)) return fail(h, MLPV_E_INVALID, "prop.V is not finite");
   d->kind = pr->kind;
   d->target = pr->target;

@@ -580,3 +580,36 @@ def test_check_invariants(oracle_mod):
             # and nothing below it is a violation
             lo = O.check(cfg.subset(n_base=1, base_start=bi, begin=0, end=int(full.first_cex[bi])))
             assert int(lo.violated[0]) == 0
+
+
+def _literal_cfg(numeric, prop_kind):
+    """2-2-3 ReLU net: identity hidden layer, logits y0 = 0.45 (bias), y1 = h0, y2 = h1; base (0, 0)
+    -> class 0; both pixels replaced by l/4, l = 0..4 (25 candidates, c = 5 l0 + l1)."""
+    if numeric == M.NUM_Q4_12:
+        W = [np.array([[4096, 0], [0, 4096]], np.int16), np.array([[0, 0], [4096, 0], [0, 4096]], np.int16)]
+        b = [np.zeros(2, np.int32), np.array([int(0.45 * 4096) << 12, 0, 0], np.int32)]
+        net = Net([2, 2, 3], M.ACT_RELU, M.NUM_Q4_12, W, b, acc_scale=[2.0 ** -24] * 2)
+        base, levels, V = np.zeros((1, 2), np.int16), np.array([1024 * l for l in range(5)], np.int16), 0.5
+    else:
+        W = [np.eye(2, dtype=np.float32), np.array([[0, 0], [1, 0], [0, 1]], np.float32)]
+        b = [np.zeros(2, np.float32), np.array([0.45, 0, 0], np.float32)]
+        net = Net([2, 2, 3], M.ACT_RELU, M.NUM_FP32, W, b, acc_scale=[1.0, 1.0])
+        base, levels, V = np.zeros((1, 2), np.float32), np.array([l / 4 for l in range(5)], np.float32), 0.5
+    pert = Pert(M.PERT_TUPLE_REPLACE, tuple=2, levels=levels)
+    pert.index_end = pert.space_size(2)
+    return Config("lit", "literal net", net, base, pert, Prop(prop_kind, 0, V), CovSpec([1]))
+
+
+def test_literal_readings(oracle_mod):
+    """l_image_misclassified with D = 0, V = 0.5 and y_D = 0.45 < V always:
+    existential reading (C12) violated iff l0 > 2 or l1 > 2 -> 25 - 9 = 16, first c = 3;
+    universal reading (NEXT-4) iff l0 > 2 and l1 > 2 -> 4, first c = 18.  Float: the 9
+    candidates with a logit exactly at V (l = 2) are flagged; Q4.12: exact, nothing flagged."""
+    O = oracle_mod
+    for numeric in (M.NUM_FP32, M.NUM_Q4_12):
+        r_any = O.check(_literal_cfg(numeric, M.PROP_THRESHOLD_LITERAL))
+        r_all = O.check(_literal_cfg(numeric, M.PROP_THRESHOLD_LITERAL_ALL))
+        assert int(r_any.violated[0]) == 16 and int(r_any.first_cex[0]) == 3
+        assert int(r_all.violated[0]) == 4 and int(r_all.first_cex[0]) == 18
+        nflag = 9 if numeric == M.NUM_FP32 else 0
+        assert int(r_any.flagged[0]) == nflag and int(r_all.flagged[0]) == nflag

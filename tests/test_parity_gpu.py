@@ -152,7 +152,8 @@ def test_other_properties(P, oracle_mod):
     cfg = _stress_cfg2()
     chk = P.Checker(cfg.net)
     for prop in (Prop(M.PROP_TARGET_NEVER, 1, 0.0), Prop(M.PROP_THRESHOLD_LITERAL, -1, 0.25),
-                 Prop(M.PROP_THRESHOLD_LITERAL, 2, -0.5)):
+                 Prop(M.PROP_THRESHOLD_LITERAL, 2, -0.5), Prop(M.PROP_THRESHOLD_LITERAL_ALL, -1, 0.25),
+                 Prop(M.PROP_THRESHOLD_LITERAL_ALL, 1, -0.5)):
         s = cfg.subset(begin=0, end=50_000)
         s.prop = prop
         assert_fixed_parity(run_gpu(chk, s), oracle_mod.check(s))
@@ -199,3 +200,15 @@ def test_invalid_range_rejected(P):
     with pytest.raises(P.MlpvError) as e:
         run_gpu(chk, bad)
     assert e.value.status == 1 and "index range" in str(e.value)
+
+
+def test_literal_readings_gpu(P, oracle_mod):
+    """The closed-form literal net (tests/test_oracle_pins.py): 16 / 4 violations, first 3 / 18."""
+    from tests.test_oracle_pins import _literal_cfg
+    for numeric in (M.NUM_FP32, M.NUM_Q4_12):
+        for kind, nv, first in ((M.PROP_THRESHOLD_LITERAL, 16, 3), (M.PROP_THRESHOLD_LITERAL_ALL, 4, 18)):
+            cfg = _literal_cfg(numeric, kind)
+            g = run_gpu(P.Checker(cfg.net), cfg)
+            assert int(g["violated"][0]) == nv and int(g["first_cex"][0]) == first
+            o = oracle_mod.check(cfg)
+            (assert_float_parity if numeric == M.NUM_FP32 else assert_fixed_parity)(g, o)

@@ -133,7 +133,8 @@ def test_fused3_shapes(P, oracle_mod, n0, n3):
 
 def test_fused3_properties(P, oracle_mod):
     for prop in (M.Prop(M.PROP_TARGET_NEVER, 3, 0.0), M.Prop(M.PROP_THRESHOLD_LITERAL, -1, 0.2),
-                 M.Prop(M.PROP_THRESHOLD_LITERAL, 1, -0.1)):
+                 M.Prop(M.PROP_THRESHOLD_LITERAL, 1, -0.1), M.Prop(M.PROP_THRESHOLD_LITERAL_ALL, -1, -0.3),
+                 M.Prop(M.PROP_THRESHOLD_LITERAL_ALL, 2, 0.1)):
         cfg = _box_cfg(eps=0.2, n_base=3, seed=11, prop=prop)
         chk = P.Checker(cfg.net)
         s = cfg.subset(begin=0, end=900)
@@ -167,3 +168,12 @@ def test_cfg4_bench_launch(P, oracle_mod):
         yb = oracle_mod.forward(cfg.net, cfg.bases[b])[-1]
         top = np.sort(y)[::-1]
         assert int(np.argmax(y)) != int(np.argmax(yb)) or top[0] - top[1] < 1e-5, (b, c)
+
+
+def test_cfg5_literal_all(P, oracle_mod):
+    """The universal literal on the generic tcgen05 path (both numerics)."""
+    for name, chk_par in (("cfg5_bf16", assert_float_parity), ("cfg5_int8", assert_fixed_parity)):
+        cfg = M.make_config(name)
+        s = cfg.subset(n_base=2, begin=0, end=260)
+        s.prop = M.Prop(M.PROP_THRESHOLD_LITERAL_ALL, -1, 0.0)
+        chk_par(run_gpu(_checker(P, name), s), oracle_mod.check(s))
