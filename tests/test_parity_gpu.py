@@ -212,3 +212,24 @@ def test_literal_readings_gpu(P, oracle_mod):
             assert int(g["violated"][0]) == nv and int(g["first_cex"][0]) == first
             o = oracle_mod.check(cfg)
             (assert_float_parity if numeric == M.NUM_FP32 else assert_fixed_parity)(g, o)
+
+
+def test_lut_revalidation(P, oracle_mod):
+    """NEXT-4: the first counterexamples of the stress Q4.12 net re-evaluated under the real-valued
+    network it approximates (exact sigmoid, FP32 path) agree with the oracle's double forward of
+    that network (class, and the violation unless the margin is a near-tie)."""
+    from paper_1907_12933_b200.revalidate import exact_net, revalidate
+    cfg = _stress_cfg2()
+    g = run_gpu(P.Checker(cfg.net), cfg)
+    recs = revalidate(cfg.net, cfg.bases, cfg.pert, cfg.prop, g["first_cex"])
+    assert len(recs) == int(np.count_nonzero(g["first_cex"] != UMAX)) and len(recs) > 0
+    en = exact_net(cfg.net)
+    for r in recs:
+        img = oracle_mod.decode(cfg.net.numeric, cfg.pert, cfg.bases[r["base"]], r["base"], r["index"]).astype(np.float64) / 4096
+        yo = oracle_mod.forward(en, img.astype(np.float32))[-1]
+        yb = oracle_mod.forward(en, (cfg.bases[r["base"]].astype(np.float64) / 4096).astype(np.float32))[-1]
+        assert np.allclose(r["logits"], yo, rtol=1e-5, atol=1e-6)
+        if r["margin"] > 1e-5:
+            assert r["class"] == int(np.argmax(yo))
+            assert r["violated_exact"] == (int(np.argmax(yo)) != int(np.argmax(yb)))
+    print("LUT artefacts:", sum(not r["violated_exact"] for r in recs), "of", len(recs))
