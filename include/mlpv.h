@@ -129,6 +129,14 @@ typedef struct {
     uint64_t n_samples;
     double lattice_step, lattice_origin;
     uint64_t index_begin, index_end;
+    /* Restriction R of checkNN (reading C27): > 0 keeps only the
+     * candidates I with delta(I^d, I) <= restrict_l2, the L2 distance to the base image in real
+     * pixel units (FP32 / BF16 values, Q4.12 raw / 4096, INT8 raw / 255); the others are skipped
+     * (not checked, no verdict, no coverage), so outside = range length - checked.  Fixed point:
+     * sum of squared raw differences (int64) <= floor(restrict_l2^2 * S^2) in double, S = 4096 /
+     * 255.  Float: sum over pixels, in pixel order, of (x' - x)^2 in double <= restrict_l2^2.
+     * Subset and tuple spaces only (MLPV_E_UNSUPPORTED for the Philox spaces).  0 = no restriction. */
+    double restrict_l2;
 } mlpv_pert;
 
 /* Safety property (reading C12).  Class = argmax of the logits, lowest index

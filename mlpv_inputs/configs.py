@@ -80,6 +80,7 @@ class Pert:
     lattice_origin: float = 0.0
     index_begin: int = 0
     index_end: int = 0
+    restrict_l2: float = 0.0                     # restriction R (reading C27): 0 = none
 
     def space_size(self, n0: int) -> int:
         if self.kind == PERT_TUPLE_REPLACE:

@@ -58,6 +58,7 @@ typedef struct {
     uint64_t seed, n_samples;
     double step, origin;
     uint64_t begin, end;
+    double restrict_l2;       /* restriction R: > 0 keeps delta(I^d, I) <= restrict_l2 */
 } opert;
 
 typedef struct { int32_t kind, target; double V; } oprop;
@@ -494,6 +495,27 @@ static int property_eval(const oprop *pr, const double *y, int n, int base_cls, 
     return cls != base_cls;                   /* safety assert Y^d = N(I) */
 }
 
+/* restriction R of checkNN (reading C27): delta(I^d, I) <= b with delta the L2
+ * distance in real pixel units, by the definition: fixed point exactly in integers against
+ * floor(b^2 S^2); float as the plain sum over all pixels of the squared differences in double */
+static int within_restriction(int numeric, const void *base, const void *img, int n0, double b) {
+    if (is_fixed(numeric)) {
+        double S = numeric == O_Q412 ? 4096.0 : 255.0;
+        int64_t thr = (int64_t)floor(b * b * S * S), s2 = 0;
+        for (int p = 0; p < n0; p++) {
+            int64_t d = (int64_t)in_get(numeric, img, p) - (int64_t)in_get(numeric, base, p);
+            s2 += d * d;
+        }
+        return s2 <= thr;
+    }
+    double s2 = 0.0;
+    for (int p = 0; p < n0; p++) {
+        double d = in_get(numeric, img, p) - in_get(numeric, base, p);
+        s2 += d * d;
+    }
+    return s2 <= b * b;
+}
+
 /* ------------------------------------------------------------------ the check */
 
 static double rne(double v) { return nearbyint(v); }
@@ -545,6 +567,8 @@ int orc_check(const onet *n, const void *bases, int n_base, const opert *p, cons
                 uint64_t c = (uint64_t)ci;
                 if (ximg) orc_decode_box(n->numeric, p, base, n0, b, c, ximg);
                 else orc_decode(n->numeric, p, base, n0, b, c, img);
+                if (p->restrict_l2 > 0 && !within_restriction(n->numeric, base, img, n0, p->restrict_l2))
+                    continue;
                 if (forward_d(&dn, img, ximg, tc, h, hn)) lbad = 1;
                 int flag;
                 int v = property_eval(pr, tc + T - nL, nL, base_cls, V, fl, cov->near_tie, &flag);

@@ -45,7 +45,8 @@ class _Pert(C.Structure):
     _fields_ = [("kind", C.c_int32), ("tuple", C.c_int32), ("n_pixels", C.c_int32),
                 ("pixels", C.POINTER(C.c_int32)), ("n_levels", C.c_int32), ("levels", C.c_void_p),
                 ("seed", C.c_uint64), ("n_samples", C.c_uint64), ("step", C.c_double),
-                ("origin", C.c_double), ("begin", C.c_uint64), ("end", C.c_uint64)]
+                ("origin", C.c_double), ("begin", C.c_uint64), ("end", C.c_uint64),
+                ("restrict_l2", C.c_double)]
 
 
 class _Prop(C.Structure):
@@ -136,7 +137,7 @@ def _mk_pert(pert, keep: _Keep) -> _Pert:
                  _p(pix, C.c_int32), 0 if pert.levels is None else len(pert.levels),
                  lv.ctypes.data, C.c_uint64(pert.seed), C.c_uint64(pert.n_samples),
                  pert.lattice_step, pert.lattice_origin, C.c_uint64(pert.index_begin),
-                 C.c_uint64(pert.index_end))
+                 C.c_uint64(pert.index_end), float(getattr(pert, "restrict_l2", 0.0)))
 
 
 # ----------------------------------------------------------------------------- primitives

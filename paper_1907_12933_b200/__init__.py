@@ -46,7 +46,8 @@ class _Pert(C.Structure):
     _fields_ = [("kind", C.c_int), ("tuple", C.c_int32), ("n_pixels", C.c_int32),
                 ("pixels", C.POINTER(C.c_int32)), ("n_levels", C.c_int32), ("levels", C.c_void_p),
                 ("seed", C.c_uint64), ("n_samples", C.c_uint64), ("lattice_step", C.c_double),
-                ("lattice_origin", C.c_double), ("index_begin", C.c_uint64), ("index_end", C.c_uint64)]
+                ("lattice_origin", C.c_double), ("index_begin", C.c_uint64), ("index_end", C.c_uint64),
+                ("restrict_l2", C.c_double)]
 
 
 class _Prop(C.Structure):
@@ -124,7 +125,7 @@ def _mk_pert(pert, keep: _Keep) -> _Pert:
     return _Pert(pert.kind, pert.tuple, 0 if pert.pixels is None else len(pert.pixels), _ptr(pix, C.c_int32),
                  nl, lvp, C.c_uint64(int(pert.seed)), C.c_uint64(int(pert.n_samples)),
                  float(pert.lattice_step), float(pert.lattice_origin), C.c_uint64(int(pert.index_begin)),
-                 C.c_uint64(int(pert.index_end)))
+                 C.c_uint64(int(pert.index_end)), float(getattr(pert, "restrict_l2", 0.0)))
 
 
 def _mk_cov(cov, keep: _Keep, tau=None) -> _Cov:

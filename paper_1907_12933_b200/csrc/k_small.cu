@@ -258,7 +258,13 @@ struct SmallArgs {
   int tbl_in_smem;            // delta table of the block's base staged in smem
   int ds;                     // row stride of the delta table as read: n1 (global) or n1 | 1 (smem:
                               // an odd stride puts the rows the lanes of a warp read in different banks)
+  const void* bases;          // [n_base x n_0] base images (restriction R)
 };
+
+// Restriction R of checkNN (reading C27): delta(I^d, I) <= b over the changed
+// pixels (the others contribute 0): fixed point exactly in int64 against floor(b^2 S^2), float
+// in double in ascending pixel order (the order of the oracle's plain sum), no contraction.
+__device__ __forceinline__ double sq_rn(double d) { return __dmul_rn(d, d); }
 
 __device__ __forceinline__ uint32_t dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, int32_t c) {
   int32_t d;
@@ -563,6 +569,59 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
         }
       }
     }
+    if (a.pert.restrict_on && !eval) {
+      const char* xb = static_cast<const char*>(a.bases);
+      const size_t bo = (size_t)b * n0;
+      bool inside;
+      if (a.pert.kind == MLPV_PERT_TUPLE_REPLACE) {
+        int pi = 0, pj = 0, li = 0, lj = 0;
+        if (a.pert.tuple == 2) {
+          const uint32_t rem = (uint32_t)(c % a.pert.q2);
+          li = rem / q; lj = rem % q;
+          unrank_pair((uint32_t)(c / a.pert.q2), n0, pi, pj);
+        } else {
+          pi = (int)(c / q); li = (int)(c % q);
+        }
+        if constexpr (FL) {
+          double s2 = sq_rn((double)lvl_f(a.pert.levels, NUM, li) - (double)in_f(xb, NUM, bo + pi));
+          if (a.pert.tuple == 2) s2 = __dadd_rn(s2, sq_rn((double)lvl_f(a.pert.levels, NUM, lj) - (double)in_f(xb, NUM, bo + pj)));
+          inside = s2 <= a.pert.r2_f;
+        } else {
+          const long long d0 = (long long)lvl_i(a.pert.levels, li) - in_i(xb, NUM, bo + pi);
+          long long s2 = d0 * d0;
+          if (a.pert.tuple == 2) {
+            const long long d1 = (long long)lvl_i(a.pert.levels, lj) - in_i(xb, NUM, bo + pj);
+            s2 += d1 * d1;
+          }
+          inside = s2 <= a.pert.r2_raw;
+        }
+      } else {
+        int dig[16];
+        uint64_t cc = c;
+        for (int k = a.pert.n_pixels - 1; k >= 0; k--) { dig[k] = (int)(cc % (uint64_t)q); cc /= (uint64_t)q; }
+        if constexpr (FL) {
+          double s2 = 0.0;
+          for (int k = 0; k < a.pert.n_pixels; k++) {
+            const int p = a.pert.pixels[k];
+            s2 = __dadd_rn(s2, sq_rn((double)lvl_f(a.pert.levels, NUM, dig[k]) - (double)in_f(xb, NUM, bo + p)));
+          }
+          inside = s2 <= a.pert.r2_f;
+        } else {
+          long long s2 = 0;
+          const int hi = NUM == MLPV_NUM_Q4_12 ? 4096 : 255;
+          for (int k = 0; k < a.pert.n_pixels; k++) {
+            const int p = a.pert.pixels[k];
+            const int32_t xp = in_i(xb, NUM, bo + p);
+            const int32_t xn = a.pert.kind == MLPV_PERT_SUBSET_OFFSET ? max(0, min(hi, xp + lvl_i(a.pert.levels, dig[k])))
+                                                                      : lvl_i(a.pert.levels, dig[k]);
+            const long long d = (long long)xn - xp;
+            s2 += d * d;
+          }
+          inside = s2 <= a.pert.r2_raw;
+        }
+      }
+      if (!inside) continue;                           // outside R: no verdict, no coverage
+    }
     // ---- a5/a6: hidden activations and dense layers
     {
       float h1f[M1]; int32_t h1i[M1]; uint32_t h1p[(M1 + 3) / 4];
@@ -717,9 +776,9 @@ cudaError_t launch_small(const DevNet& net, const void* bases, int n_base, const
                          const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
                          int num_sms, cudaStream_t st, bool* supported) {
-  (void)bases;
   SmallArgs a{};
   a.net = net; a.pert = pert; a.prop = prop; a.cov = cov; a.res = res; a.ws = ws; a.n_base = n_base;
+  a.bases = bases;
   a.eval_idx = eval_idx; a.eval_n = eval_n; a.eval_base = eval_base; a.eval_out = eval_out;
   *supported = true;
   const int L = net.L, n1 = net.sizes[1], n2 = net.sizes[2], n3 = L >= 3 ? net.sizes[3] : 0;

@@ -330,6 +330,20 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
     default:
       return fail(h, MLPV_E_INVALID, "pert.kind = %d", (int)p->kind);
   }
+  if (!std::isfinite(p->restrict_l2) || p->restrict_l2 < 0)
+    return fail(h, MLPV_E_INVALID, "pert.restrict_l2 = %g (finite, >= 0)", p->restrict_l2);
+  if (p->restrict_l2 > 0) {
+    if (p->kind == MLPV_PERT_PHILOX_LATTICE || p->kind == MLPV_PERT_PHILOX_BOX)
+      return fail(h, MLPV_E_UNSUPPORTED, "pert.restrict_l2 is built for the subset and tuple spaces");
+    dp->restrict_on = 1;
+    const double b = p->restrict_l2;
+    if (is_fixed(num)) {
+      const double S = num == MLPV_NUM_Q4_12 ? 4096.0 : 255.0;
+      dp->r2_raw = (long long)std::floor(b * b * S * S);
+    } else {
+      dp->r2_f = b * b;
+    }
+  }
   if (p->kind != MLPV_PERT_PHILOX_LATTICE && p->kind != MLPV_PERT_PHILOX_BOX) {
     if (p->n_levels < 1 || p->n_levels > 256) return fail(h, MLPV_E_INVALID, "pert.n_levels = %d (1..256)", p->n_levels);
     if (!p->levels) return fail(h, MLPV_E_INVALID, "pert.levels is NULL");
@@ -459,6 +473,7 @@ static mlpv_status run_kernel(mlpv_ctx* h, const void* bases, int n_base, const 
                      h->num_sms, st, &supported, &why);
     if (!supported) return fail(h, MLPV_E_UNSUPPORTED, "large-net kernel: %s", why.c_str());
   } else {
+    dp.levels = plan.levels_dev;
     e = launch_small(h->net, bases, n_base, dp, dprop, dc, dr, plan.ws, eval_idx, eval_n, eval_base, eval_out,
                      h->num_sms, st, &supported);
     if (!supported) return fail(h, MLPV_E_UNSUPPORTED, "no small-net kernel for this shape / numeric (L=%d, widths %d,%d,%d)",

@@ -52,6 +52,11 @@ struct DevPert {
   double step_d, origin_d;    // PHILOX_BOX
   int step_i, origin_i;       // PHILOX (INT8)
   uint64_t q2;                // TUPLE: q^2
+  // restriction R (reading C27): keep delta(I^d, I) <= b; subset / tuple spaces (k_small)
+  int restrict_on;
+  double r2_f;                // float: b^2
+  long long r2_raw;           // fixed: floor(b^2 S^2), S = 4096 (Q4.12) / 255 (INT8)
+  const void* levels;         // device copy of the levels (set by the plan; k_small's filter)
 };
 
 struct DevResult {

@@ -613,3 +613,42 @@ def test_literal_readings(oracle_mod):
         assert int(r_all.violated[0]) == 4 and int(r_all.first_cex[0]) == 18
         nflag = 9 if numeric == M.NUM_FP32 else 0
         assert int(r_any.flagged[0]) == nflag and int(r_all.flagged[0]) == nflag
+
+
+def _restrict_cfg(b):
+    """Binary 5x5 images: base all 0, six pixels each replaced by 0 or 1 (Q4.12 raw 0 / 4096), so the
+    candidate with k ones lies at L2 distance sqrt(k) from the base (delta(A, O) =
+    sqrt(6) = 2.449 for images differing in 6 pixels)."""
+    cfg = M.make_config("cfg2").subset(n_base=1)
+    cfg.bases = np.zeros((1, 25), np.int16)
+    cfg.pert = Pert(M.PERT_SUBSET_REPLACE, pixels=np.array([0, 3, 7, 12, 18, 24], np.int32),
+                    levels=np.array([0, 4096], np.int16), index_begin=0, index_end=64, restrict_l2=b)
+    return cfg
+
+
+def test_restriction_distances(oracle_mod):
+    """Restriction R (reading C27): checked = #{k <= b^2} candidates; b = 2 -> C(6,0..4) = 57,
+    b = 2.449 (< sqrt 6) -> 63, b = 2.4495 (> sqrt 6) -> 64, b = 0.99 -> only the base; b = 0 means
+    no restriction.  The double sqrt(6) squares to 5.999999999999999 < 6, so floor(b^2 4096^2) is
+    one below 6 * 4096^2 and the k = 6 candidate stays outside."""
+    O = oracle_mod
+    for b, n in ((2.0, 57), (2.449, 63), (math.sqrt(6.0), 63), (2.4495, 64), (3.0, 64), (0.99, 1), (0.0, 64)):
+        assert int(O.check(_restrict_cfg(b)).checked[0]) == n, b
+
+
+def test_restriction_monotone(oracle_mod):
+    """Violations, checked counts and coverage grow with the bound."""
+    O = oracle_mod
+    cfg = _stress_cfg2()
+    cfg = cfg.subset(n_base=2, begin=0, end=60_000)
+    prev = None
+    for b in (0.05, 0.1, 0.2, 0.3, 0.45, 0.7):
+        c = cfg.subset(n_base=2, begin=0, end=60_000)
+        c.pert = c.pert.with_range(0, 60_000)
+        c.pert.restrict_l2 = b
+        r = O.check(c)
+        if prev is not None:
+            assert np.all(r.checked >= prev.checked) and np.all(r.violated >= prev.violated)
+            assert not np.any(prev.cov_all & ~r.cov_all)
+        prev = r
+    assert int(prev.violated.sum()) > 0

@@ -233,3 +233,40 @@ def test_lut_revalidation(P, oracle_mod):
             assert r["class"] == int(np.argmax(yo))
             assert r["violated_exact"] == (int(np.argmax(yo)) != int(np.argmax(yb)))
     print("LUT artefacts:", sum(not r["violated_exact"] for r in recs), "of", len(recs))
+
+
+def test_restriction_gpu(P, oracle_mod):
+    """Restriction R (reading C27) on every subset / tuple path against the oracle:
+    the binary-image pin (57 / 63 / 64 of 64), Q4.12 subset offsets, fp32 pairs, int8 subset."""
+    from tests.test_oracle_pins import _restrict_cfg
+    for b, n in ((2.0, 57), (2.449, 63), (2.4495, 64)):
+        cfg = _restrict_cfg(b)
+        g = run_gpu(P.Checker(cfg.net), cfg)
+        assert int(g["checked"][0]) == n
+        assert_fixed_parity(g, oracle_mod.check(cfg))
+    cfg = _stress_cfg2()
+    chk = P.Checker(cfg.net)
+    for b in (0.1, 0.3):
+        s = cfg.subset(begin=0, end=120_000)
+        s.pert.restrict_l2 = b
+        g = run_gpu(chk, s)
+        assert np.all(g["checked"] < 120_000)
+        assert_fixed_parity(g, oracle_mod.check(s))
+    cfg = M.make_config("cfg1")
+    cfg.pert.restrict_l2 = 0.9
+    g = run_gpu(P.Checker(cfg.net), cfg)
+    assert 0 < int(g["checked"][0]) < 76_800
+    assert_float_parity(g, oracle_mod.check(cfg))
+    cfg = M.make_config("cfg3").subset(n_base=2, begin=0, end=200_000)
+    cfg.pert.restrict_l2 = 0.8
+    g = run_gpu(P.Checker(cfg.net), cfg)
+    assert np.all(g["checked"] < 200_000)
+    assert_fixed_parity(g, oracle_mod.check(cfg))
+
+
+def test_restriction_rejected_on_philox(P):
+    cfg = M.make_config("cfg4").subset(n_base=1, begin=0, end=10)
+    cfg.pert.restrict_l2 = 0.5
+    with pytest.raises(P.MlpvError) as e:
+        run_gpu(P.Checker(cfg.net), cfg)
+    assert e.value.status == 3
