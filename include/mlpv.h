@@ -233,6 +233,21 @@ mlpv_status mlpv_decode(mlpv_numeric numeric, const mlpv_pert *pert, const void 
 mlpv_status mlpv_merge(const mlpv_result *parts, int32_t n_parts, int32_t n_base, size_t n_words,
                        const mlpv_result *out, void *stream);
 
+/* Dataset-pair coverage (PAPER.md:364-392 Eqs. sscover..dvcover and the
+ * EG1 experiment): the four covers of every unordered pair {x_a, x_b}, a < b, of
+ * an image set, OR-ed over all n_images (n_images - 1) / 2 pairs, in the word layout of
+ * mlpv_coverage_layout (the same bit of a pair is set iff some pair of images covers it; x_a
+ * takes the role the base has in mlpv_check, the covers being symmetric in the two images).
+ * images: device [n_images x n_0] in the input element type.  cov_all / cov_certain: device
+ * [n_words], overwritten (n_images = 1: all zero).  Float numerics: cov_certain holds the bits of
+ * pairs none of whose predicates lies within tau of its boundary (reading C20; cov.tau NULL:
+ * tau_l = 1e-6 + 1e-5 max over the images of max |u_l|); fixed point: cov_certain = cov_all.
+ * The covered-neuron literal l_covered_neuron follows from mlpv_neuron_coverage on cov_all.
+ * Uses the handle's workspace (4 (T + 1) n_images bytes); enqueued on `stream`, no sync.
+ * Errors: MLPV_E_INVALID (NULL / n_images < 1 / bad spec), MLPV_E_OOM, MLPV_E_CUDA. */
+mlpv_status mlpv_pair_coverage(mlpv_t h, const void *images, int32_t n_images, const mlpv_coverage_spec *cov,
+                               uint32_t *cov_all, uint32_t *cov_certain, void *stream);
+
 /* Neuron coverage (reading C9): covered[4 * T] bytes (device; method-major,
  * T = n_1 + .. + n_L, 1 = covered) and counts[4] (device uint32: covered neurons per method) from
  * the pair words.  A neuron is covered iff it is an endpoint of a covered pair; a VS / VV column j

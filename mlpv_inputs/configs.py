@@ -294,3 +294,46 @@ def make_config(name: str) -> Config:
                     "cfg5_bf16": lambda: _cfg5("bf16"), "cfg5_int8": lambda: _cfg5("int8")}
         _CACHE[name] = builders[name]()
     return copy.copy(_CACHE[name])
+
+
+# ------------------------------------------------------------ dataset-pair workload (NEXT-3)
+def vowel_net(numeric: int = NUM_Q4_12, seed: int = 0) -> Net:
+    """A random-init 25-5-4-5 sigmoid net, the architecture of the paper's vocalic classifier
+    (Table II's 14 neurons).  Q4.12: PL-sigmoid table (readings
+    C16/C17), W in Q4.12, b in Q8.24; FP32: the exact logistic sigmoid on W / 4096, b * 2^-24."""
+    rng = np.random.default_rng([12933, 77, seed])
+    sizes = [25, 5, 4, 5]
+    W, b = [], []
+    for l in range(1, 4):
+        w = rng.normal(0.0, np.sqrt(4.0 / sizes[l - 1]), (sizes[l], sizes[l - 1]))
+        W.append(np.clip(np.rint(w * 4096), -32768, 32767).astype(np.int16))
+        b.append((np.rint(rng.normal(0.0, 0.5, sizes[l]) * 4096).astype(np.int64) << 12).astype(np.int32))
+    if numeric == NUM_Q4_12:
+        return Net(sizes, ACT_PL_SIGMOID, NUM_Q4_12, W, b, sigmoid_knots=pl_sigmoid_knots(),
+                   acc_scale=[2.0 ** -24] * 3)
+    assert numeric == NUM_FP32
+    return Net(sizes, ACT_SIGMOID, NUM_FP32, [(w.astype(np.float64) / 4096).astype(np.float32) for w in W],
+               [(v.astype(np.float64) * 2.0 ** -24).astype(np.float32) for v in b], acc_scale=[1.0] * 3)
+
+
+def pair_images(net: Net, n: int, seed: int = 0) -> np.ndarray:
+    """n seeded images for the dataset-pair workload, in the net's input element type.
+    n_0 = 25: 5x5 glyph-like stand-ins for the vocalic images and their noisy variants
+    (Fig. 4): pixels on with p = 0.4 at U[0.7, 1) plus N(0, 0.05) noise, clipped
+    to [0, 1].  n_0 = 784: smooth_blobs (28x28).  Otherwise U[0, 1) pixels."""
+    rng = np.random.default_rng([12933, 303, seed])
+    n0 = net.sizes[0]
+    if n0 == 25:
+        x = (rng.random((n, 25)) < 0.4) * rng.uniform(0.7, 1.0, (n, 25)) + rng.normal(0.0, 0.05, (n, 25))
+        x = np.clip(x, 0.0, 1.0)
+    elif n0 == 784:
+        x = smooth_blobs(rng, n).astype(np.float64)
+    else:
+        x = rng.random((n, n0))
+    if net.numeric == NUM_FP32:
+        return x.astype(np.float32)
+    if net.numeric == NUM_BF16:
+        return f32_to_bf16_bits(x.astype(np.float32))
+    if net.numeric == NUM_Q4_12:
+        return np.rint(x * 4096.0).astype(np.int16)
+    return np.rint(x * 255.0).astype(np.uint8)

@@ -459,6 +459,14 @@ void orc_cover(const int32_t *sizes, int L, const double *t1, const double *t2, 
     cover_eval(sizes, L, t1, t2, n_pairs, lower, dg, dh, NULL, words, NULL);
 }
 
+/* Same, with the ambiguity widths tau (reading C20): certain[p] = no predicate of pair p within
+ * tau of its boundary.  Used by the dataset-pair workload. */
+void orc_cover_tau(const int32_t *sizes, int L, const double *t1, const double *t2, int n_pairs,
+                   const int32_t *lower, const double *dg, const double *dh, const double *tau,
+                   uint32_t *words, int *certain) {
+    cover_eval(sizes, L, t1, t2, n_pairs, lower, dg, dh, tau, words, certain);
+}
+
 /* ------------------------------------------------------------------ property (§III.C) */
 
 /* argmax with lowest index on ties (reading C12) */

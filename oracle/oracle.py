@@ -93,6 +93,10 @@ def lib():
         _lib.orc_cover.argtypes = [C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int32),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_uint32)]
+        _lib.orc_cover_tau.argtypes = [C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_uint32), C.POINTER(C.c_int)]
         _lib.orc_check.restype = C.c_int
         _lib.orc_check.argtypes = [C.POINTER(_Net), C.c_void_p, C.c_int, C.POINTER(_Pert),
                                    C.POINTER(_Prop), C.POINTER(_Cov), C.POINTER(_Res), C.c_int]
@@ -225,6 +229,53 @@ def cover_traces(sizes, t1: List[np.ndarray], t2: List[np.ndarray], pairs, dg, d
                     len(pairs), _p(lo, C.c_int32), _p(g, C.c_double), _p(h, C.c_double),
                     _p(w, C.c_uint32))
     return w[:n]
+
+
+def pair_coverage(net, images, pairs, d_value: float, d_distance: float,
+                  tau: Optional[np.ndarray] = None):
+    """Dataset-pair coverage: the four covers
+    of every unordered pair {x_a, x_b}, a < b, of `images`, OR-ed over all pairs, in the layout of
+    `coverage_layout`.  Thresholds in potential units as in the check (fixed point: d / scale,
+    RNE).  Float numerics also return the words of pairs none of whose predicates lies within
+    tau of its boundary (reading C20; tau defaults to C20's widths over the image set); fixed
+    point returns the same words twice.  Returns (cov_all, cov_certain)."""
+    sizes = list(net.sizes)
+    L = net.L
+    fl = net.numeric in (0, 1)                         # FP32, BF16
+    traces = [forward(net, np.asarray(x)) for x in images]
+    if fl:
+        dg = [float(d_value)] * L
+        dh = [float(d_distance)] * L
+        if tau is None:
+            tau = [1e-6 + 1e-5 * max(float(np.max(np.abs(t[l]))) for t in traces) for l in range(L)]
+    else:
+        dg = [float(np.rint(d_value / net.acc_scale[l])) for l in range(L)]
+        dh = [float(np.rint(d_distance / net.acc_scale[l])) for l in range(L)]
+    n, offs = coverage_layout(sizes, pairs)
+    ends = [int(offs[p, 0]) + 2 * sizes[k] * ((sizes[k + 1] + 31) // 32) + 2 * ((sizes[k + 1] + 31) // 32)
+            for p, k in enumerate(pairs)]
+    s = np.ascontiguousarray(sizes, dtype=np.int32)
+    lo = np.ascontiguousarray(pairs, dtype=np.int32)
+    g = np.ascontiguousarray(dg, dtype=np.float64)
+    h = np.ascontiguousarray(dh, dtype=np.float64)
+    tu = np.ascontiguousarray(tau if fl else [0.0] * L, dtype=np.float64)
+    flat = [np.ascontiguousarray(np.concatenate(t), dtype=np.float64) for t in traces]
+    cov_all = np.zeros(max(n, 1), np.uint32)
+    cov_cert = np.zeros(max(n, 1), np.uint32)
+    w = np.zeros(max(n, 1), np.uint32)
+    cert = np.zeros(max(len(pairs), 1), np.int32)
+    for a in range(len(images)):
+        for b in range(a + 1, len(images)):
+            w[:] = 0
+            lib().orc_cover_tau(_p(s, C.c_int32), L, _p(flat[a], C.c_double), _p(flat[b], C.c_double),
+                                len(pairs), _p(lo, C.c_int32), _p(g, C.c_double), _p(h, C.c_double),
+                                _p(tu, C.c_double) if fl else None, _p(w, C.c_uint32), _p(cert, C.c_int))
+            cov_all |= w
+            for p in range(len(pairs)):
+                if not fl or cert[p]:
+                    o = int(offs[p, 0])
+                    cov_cert[o:ends[p]] |= w[o:ends[p]]
+    return cov_all[:n], cov_cert[:n]
 
 
 @dataclass

@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("MLPV_LIB") or os.path.join(HERE, "libmlpv.so")   # ML
 NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8 = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_UNSUPPORTED", 4: "E_OVERFLOW", 5: "E_OOM", 6: "E_CUDA"}
 EXPORTS = ["mlpv_create", "mlpv_destroy", "mlpv_last_error", "mlpv_coverage_layout", "mlpv_space_size",
-           "mlpv_check", "mlpv_eval", "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_profile",
+           "mlpv_check", "mlpv_eval", "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_pair_coverage",
+           "mlpv_profile",
            "mlpv_version"]
 
 
@@ -89,6 +90,8 @@ def lib() -> C.CDLL:
         L.mlpv_decode.argtypes = [C.c_int, C.POINTER(_Pert), C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p]
         L.mlpv_merge.argtypes = [C.POINTER(_Res), C.c_int32, C.c_int32, C.c_size_t, C.POINTER(_Res), C.c_void_p]
         L.mlpv_neuron_coverage.argtypes = [C.c_void_p, C.POINTER(_Cov), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.mlpv_pair_coverage.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(_Cov), C.c_void_p,
+                                         C.c_void_p, C.c_void_p]
         L.mlpv_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
         L.mlpv_version.restype = C.c_char_p
         for f in ("mlpv_create", "mlpv_coverage_layout", "mlpv_space_size", "mlpv_check", "mlpv_eval",
@@ -279,6 +282,20 @@ class Checker:
         e = C.c_void_p(ev_end.cuda_event) if ev_end is not None else None
         _ck(lib().mlpv_profile(self._h, b, e, C.byref(n)), self._h)
         return int(n.value)
+
+    def pair_coverage(self, images, cov, tau=None, stream=None):
+        """Dataset-pair coverage (mlpv_pair_coverage): images = CUDA tensor [n, n_0] in the input
+        element type.  Returns (cov_all, cov_certain), CUDA int32 tensors of n_words words."""
+        import torch
+        nw, _ = self.coverage_layout(cov)
+        cov_all = torch.empty(max(nw, 1), dtype=torch.int32, device=images.device)
+        cov_cert = torch.empty(max(nw, 1), dtype=torch.int32, device=images.device)
+        keep = _Keep()
+        c = _mk_cov(cov, keep, tau)
+        _ck(lib().mlpv_pair_coverage(self._h, C.c_void_p(images.data_ptr()), int(images.shape[0]), C.byref(c),
+                                     C.c_void_p(cov_all.data_ptr()), C.c_void_p(cov_cert.data_ptr()),
+                                     _stream_ptr(stream)), self._h)
+        return cov_all[:nw], cov_cert[:nw]
 
     def neuron_coverage(self, cov, words, stream=None):
         import torch

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "mlpv_internal.cuh"
 
@@ -130,6 +131,108 @@ cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* 
   k_tau_max<<<grid, 256, 0, st>>>(net, static_cast<const float*>(trace), n_base, per_blk,
                                   reinterpret_cast<unsigned*>(tau_out));
   k_tau_final<<<1, 32, 0, st>>>(net.L, tau_out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ dataset-pair coverage (NEXT-3)
+// The four covers of every unordered pair {x_a, x_b}, a < b, of an image set,
+// OR-ed over all pairs (the set-level literals of PAPER.md:364-392 / 584-589).  Block a takes the
+// pairs (a, b > a), one thread per b; words are OR-ed into a block copy in smem when it fits,
+// then flushed.  Same predicates as the check's epilogue (k_small cover_pair) with x_a in the
+// role of the base; fixed-point distances in int64 (exact).  Float: the pair's bits also go to
+// the certain set unless a predicate it used lies within tau of its boundary (reading C20).
+template <typename P, typename D>
+__global__ void __launch_bounds__(128) k_pair_cov(DevNet net, DevCov cov, const P* trace, int n,
+                                                  uint32_t* g_all, uint32_t* g_cert, int in_smem) {
+  extern __shared__ uint32_t s_w[];
+  constexpr bool FL = std::is_same<P, float>::value;
+  const int a = blockIdx.x;
+  uint32_t* wa = in_smem ? s_w : g_all;
+  uint32_t* wc = in_smem ? s_w + cov.n_words : g_cert;
+  if (in_smem) {
+    for (uint32_t w = threadIdx.x; w < 2 * cov.n_words; w += blockDim.x) s_w[w] = 0;
+    __syncthreads();
+  }
+  const int T = net.trace_len;
+  const P* ta = trace + (size_t)a * T;
+  for (int b = a + 1 + threadIdx.x; b < n; b += blockDim.x) {
+    const P* tb = trace + (size_t)b * T;
+    for (int p = 0; p < cov.n_pairs; p++) {
+      const int k = cov.lower[p], nk = net.sizes[k], nu = net.sizes[k + 1];
+      const P* la = ta + net.loff[k];
+      const P* lb = tb + net.loff[k];
+      const P* ua = ta + net.loff[k + 1];
+      const P* ub = tb + net.loff[k + 1];
+      D th, tg;
+      float tl = 0.f, tu = 0.f;
+      if constexpr (FL) {
+        th = cov.th_f[k - 1]; tg = cov.tg_f[k];
+        tl = cov.tau_dev ? cov.tau_dev[k - 1] : cov.tau[k - 1];
+        tu = cov.tau_dev ? cov.tau_dev[k] : cov.tau[k];
+      } else {
+        th = cov.th_i[k - 1]; tg = cov.tg_i[k];
+      }
+      int nsc = 0, istar = -1;
+      D linf = D(0);
+      bool amb = false;
+      for (int i = 0; i < nk; i++) {
+        const P x = la[i], y = lb[i];
+        if ((x >= P(0)) != (y >= P(0))) { if (istar < 0) istar = i; nsc++; }
+        D d = D(y) - D(x);
+        d = d < D(0) ? -d : d;
+        linf = d > linf ? d : linf;
+        if (FL && (fabsf((float)x) < tl || fabsf((float)y) < tl)) amb = true;
+      }
+      if (!(nsc == 1 || (nsc == 0 && linf >= th))) continue;
+      if (FL && nsc == 0 && fabsf((float)(linf - th)) < tl) amb = true;
+      if (FL && !amb) {
+        for (int j = 0; j < nu && !amb; j++) {
+          const P x = ua[j], y = ub[j];
+          const float d = fabsf((float)y - (float)x);
+          if (fabsf((float)x) < tu || fabsf((float)y) < tu || fabsf(d - (float)tg) < tu) amb = true;
+        }
+      }
+      const int wpr = (nu + 31) >> 5;
+      const uint32_t o_sc = nsc == 1 ? cov.off[p][0] + istar * wpr : cov.off[p][2];
+      const uint32_t o_vc = nsc == 1 ? cov.off[p][1] + istar * wpr : cov.off[p][3];
+      for (int w = 0; w < wpr; w++) {
+        uint32_t scw = 0, vcw = 0;
+        for (int jj = 0; jj < 32 && 32 * w + jj < nu; jj++) {
+          const P x = ua[32 * w + jj], y = ub[32 * w + jj];
+          const bool sc = (x >= P(0)) != (y >= P(0));
+          D d = D(y) - D(x);
+          d = d < D(0) ? -d : d;
+          scw |= (uint32_t)sc << jj;
+          vcw |= (uint32_t)(!sc && d >= tg) << jj;
+        }
+        if (scw) { atomicOr(&wa[o_sc + w], scw); if (!amb) atomicOr(&wc[o_sc + w], scw); }
+        if (vcw) { atomicOr(&wa[o_vc + w], vcw); if (!amb) atomicOr(&wc[o_vc + w], vcw); }
+      }
+    }
+  }
+  if (in_smem) {
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < cov.n_words; w += blockDim.x) {
+      if (s_w[w]) atomicOr(&g_all[w], s_w[w]);
+      if (s_w[cov.n_words + w]) atomicOr(&g_cert[w], s_w[cov.n_words + w]);
+    }
+  }
+}
+
+cudaError_t launch_pair_cov(const DevNet& net, const DevCov& cov, const void* trace, int n,
+                            uint32_t* cov_all, uint32_t* cov_cert, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(cov_all, 0, 4ull * cov.n_words, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cov_cert, 0, 4ull * cov.n_words, st);
+  if (e != cudaSuccess || n < 2 || cov.n_words == 0) return e;
+  const size_t smem = 8ull * cov.n_words;
+  const int in_smem = smem <= 48 * 1024;
+  const unsigned grid = (unsigned)(n - 1);
+  if (net.numeric == MLPV_NUM_FP32 || net.numeric == MLPV_NUM_BF16)
+    k_pair_cov<float, float><<<grid, 128, in_smem ? smem : 0, st>>>(net, cov, static_cast<const float*>(trace), n,
+                                                                      cov_all, cov_cert, in_smem);
+  else
+    k_pair_cov<int32_t, long long><<<grid, 128, in_smem ? smem : 0, st>>>(net, cov, static_cast<const int32_t*>(trace),
+                                                                           n, cov_all, cov_cert, in_smem);
   return cudaGetLastError();
 }
 

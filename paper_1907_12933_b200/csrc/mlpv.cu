@@ -701,6 +701,43 @@ extern "C" mlpv_status mlpv_merge(const mlpv_result* parts, int32_t n_parts, int
   return MLPV_OK;
 }
 
+extern "C" mlpv_status mlpv_pair_coverage(mlpv_t h, const void* images, int32_t n_images, const mlpv_coverage_spec* cov,
+                                          uint32_t* cov_all, uint32_t* cov_certain, void* stream) {
+  if (!h) return fail(nullptr, MLPV_E_INVALID, "handle is NULL");
+  if (h->sticky != MLPV_OK) return fail(h, h->sticky, "handle has a sticky CUDA error: %s", h->err.c_str());
+  if (!images || n_images < 1) return fail(h, MLPV_E_INVALID, "images is NULL or n_images = %d", n_images);
+  DevCov dc;
+  mlpv_status s = build_cov(h, cov, &dc);
+  if (s != MLPV_OK) return s;
+  if (dc.n_words > 0 && (!cov_all || !cov_certain)) return fail(h, MLPV_E_INVALID, "cov_all / cov_certain is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(h, cudaSetDevice(h->device), "cudaSetDevice");
+  const DevNet& n = h->net;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_cls = al(4ull * n_images * n.trace_len), o_tau = o_cls + al(4ull * n_images);
+  if ((s = ensure_ws(h, o_tau + al(4 * kMaxL))) != MLPV_OK) return s;
+  char* w = static_cast<char*>(h->ws);
+  BaseWS ws{};
+  ws.trace = w;
+  ws.cls = reinterpret_cast<int32_t*>(w + o_cls);
+  DevPert dp;
+  memset(&dp, 0, sizeof dp);
+  dp.kind = MLPV_PERT_SUBSET_REPLACE;            // no delta table / box base (ws.delta, ws.base1 NULL)
+  CUDA_TRY(h, launch_base_prologue(n, images, n_images, dp, nullptr, ws, st), "image traces");
+  h->launches++;
+  const bool fl = !is_fixed(n.numeric);
+  if (fl && !cov->tau && dc.n_words > 0) {
+    float* tau_dev = reinterpret_cast<float*>(w + o_tau);
+    CUDA_TRY(h, launch_tau(n, ws.trace, n_images, tau_dev, st), "tau");
+    h->launches++;
+    dc.tau_dev = tau_dev;
+  }
+  if (dc.n_words == 0) return MLPV_OK;
+  CUDA_TRY(h, launch_pair_cov(n, dc, ws.trace, n_images, cov_all, cov_certain, st), "pair coverage");
+  h->launches++;
+  return MLPV_OK;
+}
+
 extern "C" mlpv_status mlpv_neuron_coverage(mlpv_t h, const mlpv_coverage_spec* cov, const uint32_t* words,
                                             uint8_t* covered, uint32_t* counts, void* stream) {
   if (!h) return fail(nullptr, MLPV_E_INVALID, "handle is NULL");

@@ -88,5 +88,7 @@ cudaError_t launch_merge(const MergeParts& parts, int n_parts, int n_base, size_
 cudaError_t launch_neuron_cov(const DevNet& net, const DevCov& cov, const uint32_t* words,
                               uint8_t* covered, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* tau_out, cudaStream_t st);
+cudaError_t launch_pair_cov(const DevNet& net, const DevCov& cov, const void* trace, int n,
+                            uint32_t* cov_all, uint32_t* cov_cert, cudaStream_t st);
 
 }  // namespace mlpv

@@ -652,3 +652,73 @@ def test_restriction_monotone(oracle_mod):
             assert not np.any(prev.cov_all & ~r.cov_all)
         prev = r
     assert int(prev.violated.sum()) > 0
+
+
+# ------------------------------------------------ dataset-pair coverage (NEXT-3)
+def _pc_pairs(numeric):
+    net = M.vowel_net(numeric)
+    return net, M.pair_images(net, 7, seed=1)
+
+
+@pytest.mark.parametrize("numeric", [M.NUM_Q4_12, M.NUM_FP32])
+def test_pair_coverage_is_or_over_unordered_pairs(oracle_mod, numeric):
+    """The set-level covers of Eqs. sscover..dvcover are the OR of the two-image covers over all
+    unordered pairs (the covers are symmetric in x1, x2): an explicit double loop over
+    cover_traces, with thresholds converted to trace units here (d / 2^-24 for Q4.12)."""
+    O = oracle_mod
+    net, imgs = _pc_pairs(numeric)
+    pairs, d = [1, 2], 0.08
+    scale = 1.0 if numeric == M.NUM_FP32 else 2.0 ** 24
+    tr = [O.forward(net, x) for x in imgs]
+    want = None
+    for a in range(len(imgs)):
+        for b in range(len(imgs)):
+            if a == b:
+                continue                            # ordered pairs: symmetry must make b<a redundant
+            w = O.cover_traces(net.sizes, tr[a], tr[b], pairs, [d * scale] * 3, [d * scale] * 3)
+            want = w if want is None else want | w
+    got, cert = O.pair_coverage(net, imgs, pairs, d, d)
+    assert np.array_equal(got, want)
+    assert got.any()
+    assert not np.any(cert & ~got)
+    if numeric == M.NUM_Q4_12:
+        assert np.array_equal(cert, got)           # fixed point: exact, nothing ambiguous
+
+
+def test_pair_coverage_set_invariants(oracle_mod):
+    """Order of the images is irrelevant; adding an image only adds covered pairs; one image
+    covers nothing."""
+    O = oracle_mod
+    net, imgs = _pc_pairs(M.NUM_Q4_12)
+    full, _ = O.pair_coverage(net, imgs, [1, 2], 0.1, 0.1)
+    perm, _ = O.pair_coverage(net, imgs[::-1].copy(), [1, 2], 0.1, 0.1)
+    assert np.array_equal(full, perm)
+    part, _ = O.pair_coverage(net, imgs[:4], [1, 2], 0.1, 0.1)
+    assert not np.any(part & ~full) and part.sum() <= full.sum()
+    one, _ = O.pair_coverage(net, imgs[:1], [1, 2], 0.1, 0.1)
+    assert not one.any()
+
+
+def test_pair_coverage_duplicates_closed_form(oracle_mod):
+    """Two copies of one image: no sign change anywhere, all distances 0.  With d_h = d_g = 0 the
+    DS premise holds and every upper neuron is value-changed by 0 >= 0, so
+    exactly the DV columns are full and SS / SV / DS are empty; with d > 0 nothing is covered."""
+    O = oracle_mod
+    net, imgs = _pc_pairs(M.NUM_Q4_12)
+    two = np.stack([imgs[2], imgs[2]])
+    w0, _ = O.pair_coverage(net, two, [1, 2], 0.0, 0.0)
+    sets = _pairs_of(O, net.sizes, [1, 2], w0)
+    assert sets == {("VV", k, None, j) for k in (1, 2) for j in range(net.sizes[k + 1])}
+    w1, _ = O.pair_coverage(net, two, [1, 2], 0.01, 0.01)
+    assert not w1.any()
+
+
+def test_pair_coverage_certainty_widths(oracle_mod):
+    """Float certainty (reading C20): tau = 0 makes every pair certain; a tau above every |u|
+    makes none certain."""
+    O = oracle_mod
+    net, imgs = _pc_pairs(M.NUM_FP32)
+    a0, c0 = O.pair_coverage(net, imgs, [1, 2], 0.08, 0.08, tau=[0.0] * 3)
+    assert np.array_equal(a0, c0)
+    a1, c1 = O.pair_coverage(net, imgs, [1, 2], 0.08, 0.08, tau=[1e9] * 3)
+    assert np.array_equal(a0, a1) and not c1.any()
