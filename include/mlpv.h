@@ -214,6 +214,39 @@ mlpv_status mlpv_check(mlpv_t h, const void *base_inputs, int32_t n_base, const 
                        const mlpv_property *prop, const mlpv_coverage_spec *cov,
                        const mlpv_result *res, void *stream);
 
+/* Incremental bounds: the GPU analog of the two-step incremental BMC loop
+ * (§II.B; SPEC.md incremental_verify).  Iteration i = 1, 2, .. checks the ball
+ * delta(I^d, I) <= b_i (the restriction R of mlpv_pert.restrict_l2) and stops at the first
+ * iteration with a counterexample (step one: violation) or when b_i = gamma (step two: the ball
+ * is complete, the verdict is "safe over the grid").  Schedule (reading C28):
+ *   Delta = gamma / max_bound,  b_i = (i g >= max_bound) ? gamma : (i g) * Delta   (double),
+ *   i = 1 .. n_steps = ceil(max_bound / g);  g = granularity (the paper's increment, default 1;
+ *   g > 1 may miss the nearest counterexample: PAPER.md:170-173). */
+typedef struct {
+    double gamma;          /* radius of the outer ball, finite > 0 (real pixel units as restrict_l2) */
+    int32_t max_bound;     /* >= 1 */
+    int32_t granularity;   /* >= 1 */
+} mlpv_incremental;
+
+/* n_steps of the schedule (0 if inc is NULL or invalid). */
+int32_t mlpv_incremental_steps(const mlpv_incremental *inc);
+/* b_i of the schedule, 1 <= i <= n_steps (the exact double both the library and a caller's loop
+ * use); 0.0 if inc is NULL or invalid. */
+double mlpv_incremental_bound(const mlpv_incremental *inc, int32_t i);
+
+/* The incremental loop, per base input, in ONE enumeration of the gamma ball: step[b] (device
+ * int32 [n_base]) = the first iteration i whose ball holds a violating candidate (0: none, i.e.
+ * safe after n_steps iterations), first_cex[b] = the lowest index among the violating candidates
+ * inside b_step -- what the loop reports at that iteration.  step_unflagged / first_cex_unflagged:
+ * the same over unflagged violations (float numerics, reading C20).  The other result fields are
+ * those of mlpv_check with restrict_l2 = gamma (pert->restrict_l2 is ignored).  Subset / tuple
+ * spaces with index_end <= 2^48 and n_steps <= 2048; MLPV_E_UNSUPPORTED otherwise.  Errors as
+ * mlpv_check, plus MLPV_E_INVALID for a NULL / invalid inc or NULL step arrays. */
+mlpv_status mlpv_check_incremental(mlpv_t h, const void *base_inputs, int32_t n_base, const mlpv_pert *pert,
+                                   const mlpv_property *prop, const mlpv_coverage_spec *cov,
+                                   const mlpv_incremental *inc, const mlpv_result *res, int32_t *step,
+                                   int32_t *step_unflagged, void *stream);
+
 /* Parity hook: potentials of every layer (layers 1..L concatenated, T = n_1 + .. + n_L values per
  * candidate) for candidates `indices` (device [n]) of base `base_id` of base_inputs (device
  * [n_base x n_0]), computed by the same kernels and arithmetic as mlpv_check.  out: device

@@ -16,5 +16,5 @@ from .configs import (  # noqa: F401
     PERT_TUPLE_REPLACE, PERT_SUBSET_OFFSET, PERT_SUBSET_REPLACE, PERT_PHILOX_LATTICE, PERT_PHILOX_BOX,
     PROP_ARGMAX_UNCHANGED, PROP_TARGET_NEVER, PROP_THRESHOLD_LITERAL, PROP_THRESHOLD_LITERAL_ALL,
     Config, Net, Pert, Prop, CovSpec, make_config, CONFIG_IDS,
-    f32_to_bf16_bits, bf16_bits_to_f32, vowel_net, pair_images,
+    f32_to_bf16_bits, bf16_bits_to_f32, vowel_net, pair_images, gamma_config,
 )

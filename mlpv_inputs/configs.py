@@ -301,7 +301,10 @@ def vowel_net(numeric: int = NUM_Q4_12, seed: int = 0) -> Net:
     """A random-init 25-5-4-5 sigmoid net, the architecture of the paper's vocalic classifier
     (Table II's 14 neurons).  Q4.12: PL-sigmoid table (readings
     C16/C17), W in Q4.12, b in Q8.24; FP32: the exact logistic sigmoid on W / 4096, b * 2^-24."""
-    rng = np.random.default_rng([12933, 77, seed])
+    return _vowel_net(np.random.default_rng([12933, 77, seed]), numeric)
+
+
+def _vowel_net(rng: np.random.Generator, numeric: int) -> Net:
     sizes = [25, 5, 4, 5]
     W, b = [], []
     for l in range(1, 4):
@@ -337,3 +340,16 @@ def pair_images(net: Net, n: int, seed: int = 0) -> np.ndarray:
     if net.numeric == NUM_Q4_12:
         return np.rint(x * 4096.0).astype(np.int16)
     return np.rint(x * 255.0).astype(np.uint8)
+
+
+def gamma_config(n_base: int = 50) -> Config:
+    """Table III-style workload (NEXT-1 / NEXT-2): vowel_net(Q4.12), n_base 5x5
+    binary images (pixels on with p = 0.4), a SUBSET_REPLACE space over 8 pixels x levels
+    {0, 0.5, 1} (6,561 candidates per base), property "class unchanged"."""
+    rng = np.random.default_rng([12933, 77, 0])
+    net = _vowel_net(rng, NUM_Q4_12)
+    bases = (rng.random((n_base, 25)) < 0.4).astype(np.int16) * 4096
+    pixels = np.sort(rng.choice(25, 8, replace=False)).astype(np.int32)
+    pert = Pert(PERT_SUBSET_REPLACE, pixels=pixels, levels=np.array([0, 2048, 4096], np.int16),
+                index_begin=0, index_end=3 ** 8)
+    return Config("gamma", "25-5-4-5 PL-sigmoid Q4.12", net, bases, pert, Prop(), CovSpec([1, 2]))

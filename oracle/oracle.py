@@ -231,6 +231,46 @@ def cover_traces(sizes, t1: List[np.ndarray], t2: List[np.ndarray], pairs, dg, d
     return w[:n]
 
 
+def incremental_schedule(gamma: float, max_bound: int, granularity: int = 1) -> List[float]:
+    """Reading C28 (SPEC.md incremental_verify): Delta = gamma / max_bound,
+    b_i = gamma once i*g >= max_bound, else (i*g) * Delta; i = 1 .. ceil(max_bound / g)."""
+    n = -(-max_bound // granularity)
+    delta = gamma / max_bound
+    return [gamma if i * granularity >= max_bound else float(i * granularity) * delta for i in range(1, n + 1)]
+
+
+def incremental_verify(cfg, gamma: float, max_bound: int, granularity: int = 1, nthreads: int = 0):
+    """The two-step incremental loop of PAPER.md:152-168, per base input, literally: iteration i
+    checks the ball delta <= b_i (restriction R, reading C27) -- step one, a violation ends the
+    base's loop with that iteration and the ball's first counterexample -- and b_i = gamma ends
+    it as complete (step two).  Returns step (1-based, 0 = none), first_cex, and the same over
+    unflagged violations, plus the bounds and the iterations run."""
+    import copy
+    bounds = incremental_schedule(gamma, max_bound, granularity)
+    n = cfg.n_base
+    none = np.uint64(0xFFFFFFFFFFFFFFFF)
+    step = np.zeros(n, np.int32)
+    step_u = np.zeros(n, np.int32)
+    first = np.full(n, none, np.uint64)
+    first_u = np.full(n, none, np.uint64)
+    it = 0
+    for i, b in enumerate(bounds, 1):
+        it = i
+        c = copy.copy(cfg)
+        c.pert = copy.copy(cfg.pert)
+        c.pert.restrict_l2 = b
+        r = check(c, nthreads)
+        for j in range(n):
+            if step[j] == 0 and r.first_cex[j] != none:
+                step[j], first[j] = i, r.first_cex[j]
+            if step_u[j] == 0 and r.first_cex_unflagged[j] != none:
+                step_u[j], first_u[j] = i, r.first_cex_unflagged[j]
+        if np.all(step_u > 0):
+            break                                   # every base input decided
+    return {"step": step, "first_cex": first, "step_unflagged": step_u, "first_cex_unflagged": first_u,
+            "bounds": bounds, "iterations": it}
+
+
 def pair_coverage(net, images, pairs, d_value: float, d_distance: float,
                   tau: Optional[np.ndarray] = None):
     """Dataset-pair coverage: the four covers

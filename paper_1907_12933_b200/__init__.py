@@ -23,8 +23,8 @@ NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8 = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_UNSUPPORTED", 4: "E_OVERFLOW", 5: "E_OOM", 6: "E_CUDA"}
 EXPORTS = ["mlpv_create", "mlpv_destroy", "mlpv_last_error", "mlpv_coverage_layout", "mlpv_space_size",
            "mlpv_check", "mlpv_eval", "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_pair_coverage",
-           "mlpv_profile",
-           "mlpv_version"]
+           "mlpv_check_incremental", "mlpv_incremental_steps", "mlpv_incremental_bound",
+           "mlpv_profile", "mlpv_version"]
 
 
 class MlpvError(RuntimeError):
@@ -60,6 +60,10 @@ class _Cov(C.Structure):
                 ("d_distance", C.c_double), ("near_tie", C.c_double), ("tau", C.POINTER(C.c_double))]
 
 
+class _Inc(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("max_bound", C.c_int32), ("granularity", C.c_int32)]
+
+
 class _Res(C.Structure):
     _fields_ = [("checked", C.c_void_p), ("violated", C.c_void_p), ("flagged", C.c_void_p),
                 ("first_cex", C.c_void_p), ("first_cex_unflagged", C.c_void_p),
@@ -92,6 +96,13 @@ def lib() -> C.CDLL:
         L.mlpv_neuron_coverage.argtypes = [C.c_void_p, C.POINTER(_Cov), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.mlpv_pair_coverage.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(_Cov), C.c_void_p,
                                          C.c_void_p, C.c_void_p]
+        L.mlpv_check_incremental.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(_Pert), C.POINTER(_Prop),
+                                             C.POINTER(_Cov), C.POINTER(_Inc), C.POINTER(_Res), C.c_void_p,
+                                             C.c_void_p, C.c_void_p]
+        L.mlpv_incremental_steps.restype = C.c_int32
+        L.mlpv_incremental_steps.argtypes = [C.POINTER(_Inc)]
+        L.mlpv_incremental_bound.restype = C.c_double
+        L.mlpv_incremental_bound.argtypes = [C.POINTER(_Inc), C.c_int32]
         L.mlpv_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
         L.mlpv_version.restype = C.c_char_p
         for f in ("mlpv_create", "mlpv_coverage_layout", "mlpv_space_size", "mlpv_check", "mlpv_eval",
@@ -260,6 +271,31 @@ class Checker:
         r["n_words"] = nw
         return r
 
+    def check_incremental(self, bases, pert, prop, cov, gamma: float, max_bound: int, granularity: int = 1,
+                          tau=None, stream=None) -> Dict:
+        """mlpv_check_incremental: the check's result dict plus "step" / "step_unflagged" (CUDA
+        int32 [n_base]; 1-based iteration of the incremental loop, 0 = none in the gamma ball)."""
+        import torch
+        n_base = int(bases.shape[0])
+        nw, _ = self.coverage_layout(cov)
+        r = alloc_result(n_base, nw, bases.device)
+        r["step"] = torch.empty(n_base, dtype=torch.int32, device=bases.device)
+        r["step_unflagged"] = torch.empty(n_base, dtype=torch.int32, device=bases.device)
+        keep = _Keep()
+        p = _mk_pert(pert, keep)
+        pr = _Prop(prop.kind, prop.target, float(prop.V))
+        c = _mk_cov(cov, keep, tau)
+        inc = _Inc(float(gamma), int(max_bound), int(granularity))
+        rs = _res_struct(r)
+        if nw == 0:
+            rs.cov_all = None
+            rs.cov_certain = None
+        _ck(lib().mlpv_check_incremental(self._h, C.c_void_p(bases.data_ptr()), n_base, C.byref(p), C.byref(pr),
+                                         C.byref(c), C.byref(inc), C.byref(rs), C.c_void_p(r["step"].data_ptr()),
+                                         C.c_void_p(r["step_unflagged"].data_ptr()), _stream_ptr(stream)), self._h)
+        r["n_words"] = nw
+        return r
+
     def eval(self, bases, base_id: int, pert, indices, stream=None):
         """Potentials of every layer for candidates `indices` (CUDA int64 tensor) of base base_id."""
         import torch
@@ -308,6 +344,13 @@ class Checker:
                                        C.c_void_p(covered.data_ptr()), C.c_void_p(counts.data_ptr()),
                                        _stream_ptr(stream)), self._h)
         return covered.view(4, T), counts
+
+
+def incremental_schedule(gamma: float, max_bound: int, granularity: int = 1):
+    """The bounds b_1 .. b_n of the incremental loop as the library computes them (reading C28)."""
+    inc = _Inc(float(gamma), int(max_bound), int(granularity))
+    n = lib().mlpv_incremental_steps(C.byref(inc))
+    return [lib().mlpv_incremental_bound(C.byref(inc), i) for i in range(1, n + 1)]
 
 
 def version() -> str:

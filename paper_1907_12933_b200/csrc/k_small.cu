@@ -569,6 +569,8 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
         }
       }
     }
+    double rs2_f = 0.0;                                // squared distance to the base (restriction /
+    long long rs2_i = 0;                               // incremental steps), float / fixed point
     if (a.pert.restrict_on && !eval) {
       const char* xb = static_cast<const char*>(a.bases);
       const size_t bo = (size_t)b * n0;
@@ -585,6 +587,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
         if constexpr (FL) {
           double s2 = sq_rn((double)lvl_f(a.pert.levels, NUM, li) - (double)in_f(xb, NUM, bo + pi));
           if (a.pert.tuple == 2) s2 = __dadd_rn(s2, sq_rn((double)lvl_f(a.pert.levels, NUM, lj) - (double)in_f(xb, NUM, bo + pj)));
+          rs2_f = s2;
           inside = s2 <= a.pert.r2_f;
         } else {
           const long long d0 = (long long)lvl_i(a.pert.levels, li) - in_i(xb, NUM, bo + pi);
@@ -593,6 +596,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
             const long long d1 = (long long)lvl_i(a.pert.levels, lj) - in_i(xb, NUM, bo + pj);
             s2 += d1 * d1;
           }
+          rs2_i = s2;
           inside = s2 <= a.pert.r2_raw;
         }
       } else {
@@ -605,6 +609,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
             const int p = a.pert.pixels[k];
             s2 = __dadd_rn(s2, sq_rn((double)lvl_f(a.pert.levels, NUM, dig[k]) - (double)in_f(xb, NUM, bo + p)));
           }
+          rs2_f = s2;
           inside = s2 <= a.pert.r2_f;
         } else {
           long long s2 = 0;
@@ -617,6 +622,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
             const long long d = (long long)xn - xp;
             s2 += d * d;
           }
+          rs2_i = s2;
           inside = s2 <= a.pert.r2_raw;
         }
       }
@@ -681,8 +687,15 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
     if (flag) my_f++;
     if (viol) {
       my_v++;
-      if (c < my_cex) my_cex = c;
-      if (!flag && c < my_cexu) my_cexu = c;
+      unsigned long long key = c;
+      if (a.pert.n_steps > 0) {                       // incremental bounds (NEXT-2): key = (step, index)
+        int st = 1;
+        if constexpr (FL) { while (st < a.pert.n_steps && rs2_f > a.pert.step_r2_f[st - 1]) st++; }
+        else { while (st < a.pert.n_steps && rs2_i > a.pert.step_r2_raw[st - 1]) st++; }
+        key |= (unsigned long long)st << kStepShift;
+      }
+      if (key < my_cex) my_cex = key;
+      if (!flag && key < my_cexu) my_cexu = key;
     }
     // ---- a8: coverage
     uint32_t* s_cert = FL ? s_cov + a.cov.n_words : s_cov;

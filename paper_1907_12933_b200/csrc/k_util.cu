@@ -134,6 +134,24 @@ cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* 
   return cudaGetLastError();
 }
 
+// Incremental bounds (NEXT-2): split the (step, index) keys of the check into step[b] (1-based,
+// 0 = no counterexample in the ball) and the index.
+__global__ void k_split_steps(DevResult r, int n_base, int32_t* step, int32_t* step_u) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_base) return;
+  const unsigned long long m = (1ull << kStepShift) - 1;
+  const unsigned long long k = r.first_cex[b], ku = r.first_cex_unflagged[b];
+  step[b] = k == kNone ? 0 : (int32_t)(k >> kStepShift);
+  step_u[b] = ku == kNone ? 0 : (int32_t)(ku >> kStepShift);
+  if (k != kNone) r.first_cex[b] = k & m;
+  if (ku != kNone) r.first_cex_unflagged[b] = ku & m;
+}
+
+cudaError_t launch_split_steps(const DevResult& r, int n_base, int32_t* step, int32_t* step_u, cudaStream_t st) {
+  k_split_steps<<<(n_base + 127) / 128, 128, 0, st>>>(r, n_base, step, step_u);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ dataset-pair coverage (NEXT-3)
 // The four covers of every unordered pair {x_a, x_b}, a < b, of an image set,
 // OR-ed over all pairs (the set-level literals of PAPER.md:364-392 / 584-589).  Block a takes the

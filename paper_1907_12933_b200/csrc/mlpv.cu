@@ -40,6 +40,7 @@ struct mlpv_ctx {
   std::vector<double> acc_scale;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;   // mlpv_profile
   uint64_t launches = 0;
+  void* steps_dev = nullptr;          // incremental bounds: [kMaxSteps] r2 values (NEXT-2)
 };
 
 static thread_local std::string g_err;
@@ -515,9 +516,43 @@ extern "C" mlpv_status mlpv_space_size(mlpv_t h, const mlpv_pert* pert, uint64_t
   return MLPV_OK;
 }
 
+static mlpv_status check_impl(mlpv_t h, const void* base_inputs, int32_t n_base, const mlpv_pert* pert,
+                              const mlpv_property* prop, const mlpv_coverage_spec* cov, const mlpv_result* res,
+                              void* stream, const mlpv_incremental* inc, int32_t* step, int32_t* step_u);
+
 extern "C" mlpv_status mlpv_check(mlpv_t h, const void* base_inputs, int32_t n_base, const mlpv_pert* pert,
                                   const mlpv_property* prop, const mlpv_coverage_spec* cov, const mlpv_result* res,
                                   void* stream) {
+  return check_impl(h, base_inputs, n_base, pert, prop, cov, res, stream, nullptr, nullptr, nullptr);
+}
+
+// Incremental bounds (reading C28): one enumeration of
+// the gamma ball whose first-counterexample keys carry the step of the smallest ball b_i holding
+// the candidate; the iteration-by-iteration loop of the paper reports the same (step, index).
+extern "C" mlpv_status mlpv_check_incremental(mlpv_t h, const void* base_inputs, int32_t n_base, const mlpv_pert* pert,
+                                              const mlpv_property* prop, const mlpv_coverage_spec* cov,
+                                              const mlpv_incremental* inc, const mlpv_result* res, int32_t* step,
+                                              int32_t* step_unflagged, void* stream) {
+  if (!h) return fail(nullptr, MLPV_E_INVALID, "handle is NULL");
+  if (!inc || !step || !step_unflagged) return fail(h, MLPV_E_INVALID, "inc / step / step_unflagged is NULL");
+  return check_impl(h, base_inputs, n_base, pert, prop, cov, res, stream, inc, step, step_unflagged);
+}
+
+extern "C" double mlpv_incremental_bound(const mlpv_incremental* inc, int32_t i) {
+  if (!inc || inc->max_bound < 1 || inc->granularity < 1) return 0.0;
+  const int64_t ig = (int64_t)i * inc->granularity;
+  if (ig >= inc->max_bound) return inc->gamma;
+  return (double)ig * (inc->gamma / (double)inc->max_bound);
+}
+
+extern "C" int32_t mlpv_incremental_steps(const mlpv_incremental* inc) {
+  if (!inc || inc->max_bound < 1 || inc->granularity < 1) return 0;
+  return (int32_t)((inc->max_bound + inc->granularity - 1) / inc->granularity);
+}
+
+static mlpv_status check_impl(mlpv_t h, const void* base_inputs, int32_t n_base, const mlpv_pert* pert,
+                              const mlpv_property* prop, const mlpv_coverage_spec* cov, const mlpv_result* res,
+                              void* stream, const mlpv_incremental* inc, int32_t* step, int32_t* step_u) {
   if (!h) return fail(nullptr, MLPV_E_INVALID, "handle is NULL");
   if (h->sticky != MLPV_OK) return fail(h, h->sticky, "handle has a sticky CUDA error: %s", h->err.c_str());
   if (!base_inputs || n_base < 1) return fail(h, MLPV_E_INVALID, "base_inputs is NULL or n_base = %d", n_base);
@@ -531,6 +566,39 @@ extern "C" mlpv_status mlpv_check(mlpv_t h, const void* base_inputs, int32_t n_b
   if (dc.n_words > 0 && (!res->cov_all || !res->cov_certain)) return fail(h, MLPV_E_INVALID, "coverage result buffers are NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUDA_TRY(h, cudaSetDevice(h->device), "cudaSetDevice");
+  mlpv_pert pinc;
+  if (inc) {
+    if (!(inc->gamma > 0) || !std::isfinite(inc->gamma)) return fail(h, MLPV_E_INVALID, "inc.gamma = %g (finite, > 0)", inc->gamma);
+    if (inc->max_bound < 1 || inc->granularity < 1) return fail(h, MLPV_E_INVALID, "inc.max_bound / granularity must be >= 1");
+    const int n_steps = mlpv_incremental_steps(inc);
+    if (n_steps > kMaxSteps) return fail(h, MLPV_E_INVALID, "inc: %d steps (max %d)", n_steps, kMaxSteps);
+    if (pert->kind == MLPV_PERT_PHILOX_LATTICE || pert->kind == MLPV_PERT_PHILOX_BOX)
+      return fail(h, MLPV_E_UNSUPPORTED, "incremental bounds are built for the subset and tuple spaces");
+    if (pert->index_end > (1ull << kStepShift)) return fail(h, MLPV_E_UNSUPPORTED, "incremental bounds need index_end <= 2^48");
+    pinc = *pert;
+    pinc.restrict_l2 = inc->gamma;               // the kernel enumerates the whole gamma ball once
+    pert = &pinc;
+    if ((s = build_pert(h, pert, &dp, true)) != MLPV_OK) return s;
+    if (!h->steps_dev) {
+      CUDA_TRY(h, cudaMalloc(&h->steps_dev, 8 * kMaxSteps), "steps buffer");
+      h->allocs.push_back(h->steps_dev);
+    }
+    std::vector<double> r2f(n_steps);
+    std::vector<long long> r2i(n_steps);
+    const bool fx = is_fixed(h->net.numeric);
+    const double S = h->net.numeric == MLPV_NUM_Q4_12 ? 4096.0 : 255.0;
+    for (int i = 1; i <= n_steps; i++) {
+      const double b = mlpv_incremental_bound(inc, i);
+      r2f[i - 1] = b * b;
+      r2i[i - 1] = (long long)std::floor(b * b * S * S);
+    }
+    // pageable source: cudaMemcpyAsync returns once the data is staged
+    CUDA_TRY(h, cudaMemcpyAsync(h->steps_dev, fx ? (const void*)r2i.data() : (const void*)r2f.data(), 8ull * n_steps,
+                                cudaMemcpyHostToDevice, st), "copy steps");
+    dp.n_steps = n_steps;
+    dp.step_r2_f = static_cast<const double*>(h->steps_dev);
+    dp.step_r2_raw = static_cast<const long long*>(h->steps_dev);
+  }
   DevResult dr{res->checked, res->violated, res->flagged, res->first_cex, res->first_cex_unflagged, res->cov_all, res->cov_certain};
   CUDA_TRY(h, launch_init_result(dr, n_base, dc.n_words, st), "init results");
   h->launches++;
@@ -538,8 +606,15 @@ extern "C" mlpv_status mlpv_check(mlpv_t h, const void* base_inputs, int32_t n_b
   const bool fl = !is_fixed(h->net.numeric);
   if ((s = prepare(h, base_inputs, n_base, pert, dp, &dc, &plan, st, fl)) != MLPV_OK) return s;
   dc.tau_dev = (fl && !cov->tau) ? plan.tau_dev : nullptr;
-  if (pert->index_begin == pert->index_end) return MLPV_OK;
-  return run_kernel(h, base_inputs, n_base, pert, dp, dprop, dc, dr, plan, nullptr, 0, 0, nullptr, st);
+  if (pert->index_begin != pert->index_end) {
+    if ((s = run_kernel(h, base_inputs, n_base, pert, dp, dprop, dc, dr, plan, nullptr, 0, 0, nullptr, st)) != MLPV_OK)
+      return s;
+  }
+  if (inc) {
+    CUDA_TRY(h, launch_split_steps(dr, n_base, step, step_u, st), "split steps");
+    h->launches++;
+  }
+  return MLPV_OK;
 }
 
 extern "C" mlpv_status mlpv_eval(mlpv_t h, const void* base_inputs, int32_t n_base, int32_t base_id,

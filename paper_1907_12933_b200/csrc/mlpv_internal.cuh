@@ -57,7 +57,14 @@ struct DevPert {
   double r2_f;                // float: b^2
   long long r2_raw;           // fixed: floor(b^2 S^2), S = 4096 (Q4.12) / 255 (INT8)
   const void* levels;         // device copy of the levels (set by the plan; k_small's filter)
+  // incremental bounds b_1 < .. < b_n (NEXT-2, reading C28): a violation's first_cex key is
+  // (step << kStepShift) | index, step = smallest i with distance^2 <= r2 of b_i
+  int n_steps;                // 0 = off
+  const double* step_r2_f;    // device [n_steps] b_i^2 (float numerics)
+  const long long* step_r2_raw;  // device [n_steps] floor(b_i^2 S^2) (fixed point)
 };
+constexpr int kStepShift = 48;   // candidate indices < 2^48 in incremental mode
+constexpr int kMaxSteps = 2048;
 
 struct DevResult {
   uint64_t *checked, *violated, *flagged, *first_cex, *first_cex_unflagged;
@@ -88,6 +95,7 @@ cudaError_t launch_merge(const MergeParts& parts, int n_parts, int n_base, size_
 cudaError_t launch_neuron_cov(const DevNet& net, const DevCov& cov, const uint32_t* words,
                               uint8_t* covered, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* tau_out, cudaStream_t st);
+cudaError_t launch_split_steps(const DevResult& r, int n_base, int32_t* step, int32_t* step_u, cudaStream_t st);
 cudaError_t launch_pair_cov(const DevNet& net, const DevCov& cov, const void* trace, int n,
                             uint32_t* cov_all, uint32_t* cov_cert, cudaStream_t st);
 

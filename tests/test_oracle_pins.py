@@ -722,3 +722,52 @@ def test_pair_coverage_certainty_widths(oracle_mod):
     assert np.array_equal(a0, c0)
     a1, c1 = O.pair_coverage(net, imgs, [1, 2], 0.08, 0.08, tau=[1e9] * 3)
     assert np.array_equal(a0, a1) and not c1.any()
+
+
+# ------------------------------------------ incremental bounds (NEXT-2, C28)
+def _flip_cfg(levels=(0.15, 0.275, 0.4, 0.525, 0.65)):
+    """SPEC.md's hand-built 2-pixel threshold net: class flips when pixel0 + pixel1 > 1.  2-2-2
+    ReLU, identity hidden layer, y0 = 1 - h0 - h1, y1 = 0; I^d = (0.4, 0.4) (class 0); both pixels
+    take the q = 5 levels of [I^d - r, I^d + r], r = 0.25 (c = 5 d0 + d1)."""
+    W = [np.eye(2, dtype=np.float32), np.array([[-1, -1], [0, 0]], np.float32)]
+    b = [np.zeros(2, np.float32), np.array([1, 0], np.float32)]
+    net = Net([2, 2, 2], M.ACT_RELU, M.NUM_FP32, W, b, acc_scale=[1.0, 1.0])
+    pert = Pert(M.PERT_SUBSET_REPLACE, pixels=np.array([0, 1], np.int32), levels=np.array(levels, np.float32))
+    pert.index_end = pert.space_size(2)
+    return Config("thr", "threshold net", net, np.array([[0.4, 0.4]], np.float32), pert, Prop(), CovSpec([]))
+
+
+def test_incremental_schedule_closed_form(oracle_mod):
+    """b_i = i g gamma / max_bound, the last one exactly gamma; ceil(max_bound / g) steps
+    (SPEC.md completeness_phase: first complete at the smallest i with b_i >= gamma)."""
+    O = oracle_mod
+    assert O.incremental_schedule(0.5, 10, 1)[-1] == 0.5 and len(O.incremental_schedule(0.5, 10, 1)) == 10
+    b = O.incremental_schedule(0.5, 10, 3)
+    assert len(b) == 4 and b[-1] == 0.5 and b[:3] == pytest.approx([0.15, 0.3, 0.45], abs=1e-15)
+    assert O.incremental_schedule(1.0, 1, 7) == [1.0]
+
+
+def test_incremental_threshold_net(oracle_mod):
+    """Nearest grid counterexamples (brute force over the 25 points): (0.525, 0.525) at
+    sqrt(2)/8 = 0.177 (c = 18), then (0.4, 0.65) / (0.65, 0.4) at 0.25 (c = 14 / 22).
+    gamma = 0.5, Delta = 0.05: g = 1 finds c = 18 at step 4 (b = 0.2, the smallest ball holding
+    0.177); g = 2 at step 2 (b = 0.2), the same; g = 3 at step 2 (b = 0.3), where c = 14 at
+    distance 0.25 is the lowest index -- not the nearest one.  gamma = 0.17:
+    none after all 10 steps.  q = 2, r = 0 (both levels = I^d): only I^d, none."""
+    O = oracle_mod
+    cfg = _flip_cfg()
+    # brute force of the nearest flipping grid point
+    lv = np.array(cfg.pert.levels, np.float64)
+    d = min(math.hypot(lv[i] - np.float32(0.4), lv[j] - np.float32(0.4)) for i in range(5) for j in range(5)
+            if np.float32(lv[i]) + np.float32(lv[j]) > 1)
+    assert d == pytest.approx(math.sqrt(2) / 8, abs=1e-6)
+    r = O.incremental_verify(cfg, 0.5, 10, 1)
+    assert (int(r["step"][0]), int(r["first_cex"][0]), r["iterations"]) == (4, 18, 4)
+    r = O.incremental_verify(cfg, 0.5, 10, 2)
+    assert (int(r["step"][0]), int(r["first_cex"][0])) == (2, 18)
+    r = O.incremental_verify(cfg, 0.5, 10, 3)
+    assert (int(r["step"][0]), int(r["first_cex"][0])) == (2, 14)
+    r = O.incremental_verify(cfg, 0.17, 10, 1)
+    assert int(r["step"][0]) == 0 and r["iterations"] == 10
+    r = O.incremental_verify(_flip_cfg((0.4, 0.4)), 0.5, 10, 1)
+    assert int(r["step"][0]) == 0

@@ -12,7 +12,6 @@ paper are not available, so the numbers are the method's behaviour on this net, 
 usage: python tools/gamma_sweep.py [--bases 50] [--gammas 0.5,1,1.5,2,2.5,3]
 """
 import argparse
-import math
 import os
 import sys
 import time
@@ -22,30 +21,18 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import mlpv_inputs as M                                             # noqa: E402
-from mlpv_inputs.configs import Config, CovSpec, Net, Pert, Prop, pl_sigmoid_knots    # noqa: E402
+from mlpv_inputs.configs import Config                              # noqa: E402
 
 
 def make(n_base: int) -> Config:
-    rng = np.random.default_rng([12933, 77, 0])
-    sizes = [25, 5, 4, 5]
-    W, b = [], []
-    for l in range(1, 4):
-        w = rng.normal(0.0, math.sqrt(4.0 / sizes[l - 1]), (sizes[l], sizes[l - 1]))
-        W.append(np.clip(np.rint(w * 4096), -32768, 32767).astype(np.int16))
-        b.append((np.rint(rng.normal(0.0, 0.5, sizes[l]) * 4096).astype(np.int64) << 12).astype(np.int32))
-    net = Net(sizes, M.ACT_PL_SIGMOID, M.NUM_Q4_12, W, b, sigmoid_knots=pl_sigmoid_knots(),
-              acc_scale=[2.0 ** -24] * 3)
-    bases = (rng.random((n_base, 25)) < 0.4).astype(np.int16) * 4096
-    pixels = np.sort(rng.choice(25, 8, replace=False)).astype(np.int32)
-    pert = Pert(M.PERT_SUBSET_REPLACE, pixels=pixels, levels=np.array([0, 2048, 4096], np.int16),
-                index_begin=0, index_end=3 ** 8)
-    return Config("gamma", "25-5-4-5 PL-sigmoid Q4.12", net, bases, pert, Prop(), CovSpec([1, 2]))
+    return M.gamma_config(n_base)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bases", type=int, default=50)
     ap.add_argument("--gammas", default="0.5,1,1.5,2,2.5,3")
+    ap.add_argument("--max-bound", type=int, default=12)
     args = ap.parse_args()
     import torch
     import paper_1907_12933_b200 as P
@@ -64,6 +51,21 @@ def main():
         first = int(r["first_cex"][hit].min()) if hit.any() else -1
         print(f"{g:6.2f} {int(r['checked'].sum()):10d} {int(r['violated'].sum()):11d} {int(hit.sum()):10d} "
               f"{first:10d} {dt:8.2f}")
+    # the incremental loop (NEXT-2) over the same gammas as one schedule: gamma_max, max_bound
+    gs = [float(x) for x in args.gammas.split(",")]
+    mb = args.max_bound
+    cfg.pert.restrict_l2 = 0.0
+    bases = torch.from_numpy(cfg.bases).cuda()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = chk.check_incremental(bases, cfg.pert, cfg.prop, cfg.cov, max(gs), mb, 1)
+    st = r["step"].cpu().numpy()
+    dt = (time.perf_counter() - t0) * 1e3
+    sched = P.incremental_schedule(max(gs), mb, 1)
+    print(f"incremental: gamma = {max(gs)}, {mb} steps, {dt:.2f} ms; bases violated at step i (b_i):")
+    for i, b in enumerate(sched, 1):
+        print(f"  step {i:3d}  b = {b:6.3f}  bases {int((st == i).sum()):4d}")
+    print(f"  safe over the grid: {int((st == 0).sum())}")
 
 
 if __name__ == "__main__":
