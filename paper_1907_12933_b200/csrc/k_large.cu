@@ -3,15 +3,15 @@
 // TMEM), fused epilogue with the coverage predicates and the safety property.
 //
 // One persistent CTA per SM; a tile is 128 consecutive candidate indices of one base input (one
-// candidate per TMEM lane).  Warp roles (320 threads):
-//   warp 0     producer: cp.async.bulk of pre-swizzled weight tiles (and, for layers >= 2, of the
-//              previous layer's activations from the CTA's L2-resident scratch) into a 3-stage ring
-//   warp 1     MMA issuer (one thread): tcgen05.mma kind::f16 (bf16 / f16) or kind::i8, owns TMEM
-//   warps 2-5  generator: Philox4x32-10 lattice candidates (reading C14/C15) written as SWIZZLE_128B
-//              K-major A tiles into a 3-stage ring
-//   warps 6-9  epilogue: tcgen05.ld of the accumulators (thread = candidate), bias, potentials,
-//              sign / value / distance predicates and pair coverage (rows a5, a8), hidden activation
-//              written back as the next layer's A operand, argmax / property / counts (a7, a9)
+// candidate per TMEM lane).  Warp roles (512 threads, 4 warpgroups; setmaxnreg 80 / 80 / 248 / 80):
+//   warps 0-7   generator, two groups taking the ring stages in turn: Philox4x32-10 lattice
+//               candidates (reading C14/C15) written as SWIZZLE_128B K-major A tiles (row a2)
+//   warps 8-11  epilogue: tcgen05.ld of the accumulators (thread = candidate), bias, potentials,
+//               sign / value / distance predicates and pair coverage (rows a5, a8), hidden activation
+//               written back as the next layer's A operand, argmax / property / counts (a7, a9)
+//   warp 14     producer: cp.async.bulk of pre-swizzled weight tiles (and, for layers >= 2, of the
+//               previous layer's activations from the CTA's L2-resident scratch)
+//   warp 15     MMA issuer (one thread): tcgen05.mma kind::f16 (bf16 / f16) or kind::i8, owns TMEM
 // Float path (BF16): layer 1 is bf16 x bf16 -> fp32 (exact operands); hidden activations are split
 // h = hi + lo into two fp16 values (|h - hi - lo| <= 2^-22 |h|) and layer l >= 2 contracts [hi | lo]
 // against [W_l | W_l] in fp16 (reading C19).  INT8 path: u8 x s8 -> s32, bit-exact.
@@ -28,15 +28,34 @@
 #include "mlpv_internal.cuh"
 #include "tc_ptx.cuh"
 
+#ifndef MLPV_EXP
+#define MLPV_EXP 0          // timing experiments only (results wrong by design); 0 = product
+#endif
+// MLPV_EXP = 201: the weight tiles are not streamed (128 B per stage); 202: the epilogue skips its
+// per-column work (barriers only); 203: the generators skip the candidate generation;
+// 204: all three
+
 namespace mlpv {
 using namespace tc;
 
+#ifdef MLPV_TRACE
+__device__ unsigned long long g_kltrace[32][24];       // block 0, first 32 tiles, clock64 stamps
+#define KT(tl, ev) do { if (blockIdx.x == 0 && (tl) < 32) g_kltrace[(tl)][(ev)] = clock64(); } while (0)
+#else
+#define KT(tl, ev) do { } while (0)
+#endif
+
 constexpr int kM = 128;                   // candidates per tile = TMEM lanes
 constexpr int kSG = 3;                    // generator ring stages
-constexpr int kSP = 3;                    // producer ring stages
+constexpr int kSP = 3;                    // producer ring stages, layers >= 2 (W tile + A tile)
+constexpr int kSPA = 4;                   // producer ring stages, layer 1 (W tile only; the same bytes)
 constexpr uint32_t kABytes = 128u * 128u; // A tile: 128 rows x 128 B
 constexpr uint32_t kWBytes = 256u * 128u; // W tile: up to 256 rows x 128 B
-constexpr int kThreads = 512;                // 4 warpgroups: control, 2 x generator, epilogue
+constexpr int kThreads = 512;                // 4 warpgroups: 2 x generator, epilogue, control
+// The SMSP arbiter favours the highest warp id: the MMA issuer and the weight producer get the top
+// ids (a low-id issuer lost issue slots to the generators: 260 cycles per 128-cycle MMA, trace),
+// then the epilogue, then the generators.
+constexpr int kWProd = 14, kWIss = 15;
 constexpr int kRegLaunchL = 128, kRegCtlL = 80, kRegEpiL = 248;   // setmaxnreg budget: 3 x 80 + 248 <= 4 x 128
 static_assert(3 * kRegCtlL + kRegEpiL <= 4 * kRegLaunchL, "setmaxnreg budget");
 constexpr uint32_t kTmemCols = 512;       // two 256-column accumulator buffers
@@ -231,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
   uint8_t* sPA = sG + kSG * kABytes;                         // [kSP][kABytes]
   uint8_t* sPW = sPA + kSP * kABytes;                        // [kSP][kWBytes]
   uint32_t* s_pend = reinterpret_cast<uint32_t*>(sPW + kSP * kWBytes);   // [kM][kPendWords]
-  __shared__ uint64_t gfull[kSG], gempty[kSG], pfull[kSP], pempty[kSP], acc_full[2], acc_empty[2], h_ready[kMaxL + 1];
+  __shared__ uint64_t gfull[kSG], gempty[kSG], pfull[kSP], pempty[kSP], pfullA[kSPA], pemptyA[kSPA], acc_full[2],
+      acc_empty[2], h_ready[kMaxL + 1];
   __shared__ uint32_t s_tbase;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -239,11 +259,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSG; i++) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
     for (int i = 0; i < kSP; i++) { mbar_init(&pfull[i], 1); mbar_init(&pempty[i], 1); }
+    for (int i = 0; i < kSPA; i++) { mbar_init(&pfullA[i], 1); mbar_init(&pemptyA[i], 1); }
     for (int i = 0; i < 2; i++) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 1); }
     for (int i = 0; i <= kMaxL; i++) mbar_init(&h_ready[i], 1);
     fence_mbar_init();
   }
-  if (warp == 1) { tmem_alloc(&s_tbase, kTmemCols); tmem_relinquish(); }
+  if (warp == kWIss) { tmem_alloc(&s_tbase, kTmemCols); tmem_relinquish(); }
   for (int i = threadIdx.x; i < kM * kPendWords; i += blockDim.x) s_pend[i] = 0;
   // biases of every layer (32-bit float or int) once; the base potentials per tile (epilogue)
   uint32_t* s_bias = s_pend + kM * kPendWords;
@@ -258,10 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
   const uint32_t tbase = s_tbase;
   uint8_t* scratch = a.scratch + (size_t)blockIdx.x * a.scratch_per_cta;
 
-  if ((warp >> 2) == 3) {
+  if ((warp >> 2) == 2) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpiL));
     // ------------------------------------------------------------------- epilogue
-    const int e = threadIdx.x - 384;
+    const int e = threadIdx.x - 256;
     const int quad = warp & 3;
     const int r = 32 * quad + lane;                  // candidate row = TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
@@ -272,6 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
     uint32_t* pend = s_pend + r * kPendWords;
     for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info(a, t);
+      const int etl = (int)((t - blockIdx.x) / gridDim.x);
+      (void)etl;
       const bool valid = r < ti.nvalid;
       const uint64_t cidx = row_index(a, ti, r);
       if (a.staged) {                              // this tile's base potentials (the previous tile's
@@ -309,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           const uint32_t buf = cseq & 1u, ph = (cseq >> 1) & 1u;
           mbar_wait(&acc_full[buf], ph);
           fence_after();
-          for (int pc = 0; pc < ld.nc; pc += 32) {
+          for (int pc = 0; pc < ((MLPV_EXP == 202 || MLPV_EXP == 204) ? 0 : ld.nc); pc += 32) {
             const int j0 = ch * ld.nc + pc;
             if (j0 >= ld.n && l == L) break;
             if (j0 >= ((ld.n + 63) & ~63) && l < L && fl) break;
@@ -504,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           fence_before();
           named_bar(2, 128);
           if (e == 0) mbar_arrive(&acc_empty[buf]);
+          if (e == 0) KT(etl, 11 + (l == 1 ? ch : (l == 2 ? 4 + ch : 6)));
           cseq++;
         }
         // ---- finish pair (l-1, l): coverage of this candidate (reading C3, C8; C20 for certainty)
@@ -543,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           __threadfence_block();
           named_bar(2, 128);
           if (e == 0) mbar_arrive(&h_ready[l]);
+          if (e == 0) KT(etl, 17 + l);
         }
       }
       if (eval) continue;
@@ -616,14 +641,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
     }
     } else {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtlL));
-  if (warp == 0) {
+  if (warp == kWProd) {
     // ------------------------------------------------------------------- producer
     if (lane == 0) {
-      uint32_t ps = 0, hph[kMaxL + 1] = {0};
+      // Layer 1 streams W tiles alone through kSPA slots of kWBytes laid over the whole
+      // [sPA, sPW) region; layers >= 2 stream (W, A) pairs through kSP slots (sPW, sPA).  The two
+      // layouts overlap, so a switch first drains the other layout's last stage (MMAs complete
+      // in order).
+      uint32_t ps = 0, psA = 0, hph[kMaxL + 1] = {0};
+      int lay_prev = -1;
       for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
           const uint32_t wbytes = (uint32_t)ld.nc * 128u;
+          const int lay = l == 1 ? 0 : 1;
+          if (lay != lay_prev) {
+            if (lay_prev == 0 && psA > 0) mbar_wait(&pemptyA[(psA - 1) % kSPA], ((psA - 1) / kSPA) & 1u);
+            if (lay_prev == 1 && ps > 0) mbar_wait(&pempty[(ps - 1) % kSP], ((ps - 1) / kSP) & 1u);
+            lay_prev = lay;
+          }
           if (l >= 2) { mbar_wait(&h_ready[l - 1], hph[l - 1]); hph[l - 1] ^= 1u; }
           // layer 1 with an even chunk count runs the chunks in pairs on one generated A stage:
           // W stages in the order (pair, kb, chunk of the pair)
@@ -631,11 +667,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           for (int i = 0; i < ld.nchunks * ld.nkb; i++) {
             const int ch = paired ? 2 * (i / (2 * ld.nkb)) + (i & 1) : i / ld.nkb;
             const int kb = paired ? (i / 2) % ld.nkb : i % ld.nkb;
-            {
+            const uint32_t wb = (MLPV_EXP == 201 || MLPV_EXP == 204) ? 128u : wbytes;
+            if (lay == 0) {
+              const uint32_t st = psA % kSPA, ph = (psA / kSPA) & 1u;
+              mbar_wait(&pemptyA[st], ph ^ 1u);
+              mbar_expect_tx(&pfullA[st], wb);
+              bulk_g2s(sPA + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wb, &pfullA[st]);
+              psA++;
+            } else {
               const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
               mbar_wait(&pempty[st], ph ^ 1u);
-              mbar_expect_tx(&pfull[st], wbytes + (l >= 2 ? kABytes : 0u));
-              bulk_g2s(sPW + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wbytes, &pfull[st]);
+              mbar_expect_tx(&pfull[st], wb + (l >= 2 ? kABytes : 0u));
+              bulk_g2s(sPW + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wb, &pfull[st]);
               if (l >= 2) bulk_g2s(sPA + st * kABytes, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
               ps++;
             }
@@ -643,12 +686,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kWIss) {
     // ------------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      uint32_t gs = 0, ps = 0, cseq = 0;
+    {
+      // the whole warp runs the loop (descriptors stay warp-uniform, in uniform registers); one
+      // elected lane issues the MMAs and commits.  A lane-0-only issuer spent ~900 cycles per
+      // 4-MMA stage moving per-lane operands into uniform registers (trace).
+      const bool el = elect_one();
+      uint32_t gs = 0, ps = 0, psA = 0, cseq = 0;
       const bool i8 = a.net.numeric == MLPV_NUM_INT8;
       for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        const int tl = (int)((t - blockIdx.x) / gridDim.x);
+        KT(tl, 0);
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
           const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, l == 1 ? 1 : 0, l == 1 ? 1 : 0);
@@ -657,31 +706,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
             for (int cp = 0; cp < ld.nchunks / 2; cp++) {
 #pragma unroll
               for (int c = 0; c < 2; c++) mbar_wait(&acc_empty[(cseq + c) & 1u], (((cseq + c) >> 1) & 1u) ^ 1u);
+              KT(tl, 1 + 2 * (cp & 1));
               fence_after();
+#ifdef MLPV_TRACE
+              long long wg = 0, wp = 0;
+#endif
               for (int kb = 0; kb < ld.nkb; kb++) {
                 const uint32_t gst = gs % kSG;
+#ifdef MLPV_TRACE
+                const long long tw0 = clock64();
+#endif
                 mbar_wait(&gfull[gst], (gs / kSG) & 1u);
+#ifdef MLPV_TRACE
+                wg += clock64() - tw0;
+#endif
 #pragma unroll 1
                 for (int c = 0; c < 2; c++) {
-                  const uint32_t pst = ps % kSP;
-                  mbar_wait(&pfull[pst], (ps / kSP) & 1u);
-                  fence_after();
-                  const uint32_t d = tbase + ((cseq + c) & 1u) * 256u;
-                  const uint32_t abase = smem_u32(sG + gst * kABytes), bbase = smem_u32(sPW + pst * kWBytes);
+                  const uint32_t pst = psA % kSPA;
+#ifdef MLPV_TRACE
+                  const long long tw1 = clock64();
+#endif
+                  mbar_wait(&pfullA[pst], (psA / kSPA) & 1u);
+#ifdef MLPV_TRACE
+                  wp += clock64() - tw1;
+#endif
+                  // (no tcgen05.fence::after_thread_sync per stage: the operands arrive through the
+                  // async proxy / proxy-fenced stores behind the mbarrier; a fence here stalled the
+                  // issue until the queued MMAs drained -- ~900 cycles per 4-MMA stage, trace)
+                  const uint32_t d = tbase + (MLPV_EXP == 205 ? 0u : ((cseq + c) & 1u) * 256u);
+                  const uint32_t abase = smem_u32(sG + gst * kABytes), bbase = smem_u32(sPA + pst * kWBytes);
 #pragma unroll
-                  for (int kk = 0; kk < 4; kk++) {
+                  for (int kk = 0; kk < (MLPV_EXP == 206 ? 2 : 4); kk++) {
                     const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
                     const uint32_t acc = (kb | kk) ? 1u : 0u;
-                    if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
+                    if (el) { if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc); }
                   }
-                  mma_commit(&pempty[pst]);
-                  ps++;
+                  if (el) mma_commit(&pemptyA[pst]);
+                  psA++;
                 }
-                mma_commit(&gempty[gst]);
+                if (el) mma_commit(&gempty[gst]);
                 gs++;
               }
-              mma_commit(&acc_full[cseq & 1u]);
-              mma_commit(&acc_full[(cseq + 1) & 1u]);
+              if (el) mma_commit(&acc_full[cseq & 1u]);
+              if (el) mma_commit(&acc_full[(cseq + 1) & 1u]);
+              KT(tl, 2 + 2 * (cp & 1));
+#ifdef MLPV_TRACE
+              if (blockIdx.x == 0 && tl < 32) { g_kltrace[tl][20 + 2 * (cp & 1)] = wg; g_kltrace[tl][21 + 2 * (cp & 1)] = wp; }
+#endif
               cseq += 2;
             }
             continue;
@@ -689,37 +760,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           for (int ch = 0; ch < ld.nchunks; ch++) {
             const uint32_t buf = cseq & 1u, aph = (cseq >> 1) & 1u;
             mbar_wait(&acc_empty[buf], aph ^ 1u);
+            if (ch == 0) KT(tl, 5 + 3 * (l - 2));
             fence_after();
             const uint32_t d = tbase + buf * 256u;
             for (int kb = 0; kb < ld.nkb; kb++) {
-              const uint32_t pst = ps % kSP;
-              mbar_wait(&pfull[pst], (ps / kSP) & 1u);
+              const uint32_t pst = l == 1 ? psA % kSPA : ps % kSP;
+              if (l == 1) mbar_wait(&pfullA[pst], (psA / kSPA) & 1u);
+              else mbar_wait(&pfull[pst], (ps / kSP) & 1u);
+              if (ch == 0 && kb == 0) KT(tl, 6 + 3 * (l - 2));
               uint32_t gst = 0;
               if (l == 1) { gst = gs % kSG; mbar_wait(&gfull[gst], (gs / kSG) & 1u); }
-              fence_after();
               const uint32_t abase = smem_u32(l == 1 ? sG + gst * kABytes : sPA + pst * kABytes);
-              const uint32_t bbase = smem_u32(sPW + pst * kWBytes);
+              const uint32_t bbase = smem_u32(l == 1 ? sPA + pst * kWBytes : sPW + pst * kWBytes);
 #pragma unroll
               for (int kk = 0; kk < 4; kk++) {
                 const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
                 const uint32_t acc = (kb | kk) ? 1u : 0u;
-                if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc);
+                if (el) { if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc); }
               }
-              mma_commit(&pempty[pst]);
-              if (l == 1) { mma_commit(&gempty[gst]); gs++; }
-              ps++;
+              if (l == 1) { if (el) mma_commit(&pemptyA[pst]); if (el) mma_commit(&gempty[gst]); gs++; psA++; }
+              else { if (el) mma_commit(&pempty[pst]); ps++; }
             }
-            mma_commit(&acc_full[buf]);
+            if (el) mma_commit(&acc_full[buf]);
+            if (ch == ld.nchunks - 1) KT(tl, 7 + 3 * (l - 2));
             cseq++;
           }
         }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ------------------------------------------------------------------- generator
     // two groups (warpgroups 1 and 2) take the ring stages in turn
-    const int ggrp = (warp >> 2) - 1;
-    const int r = threadIdx.x - 128 * (warp >> 2);
+    const int ggrp = warp >> 2;
+    const int r = threadIdx.x - 128 * ggrp;
     uint32_t gs = 0;
     const LayerDesc& l1 = a.lay[1];
     for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
@@ -729,8 +802,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         for (int kb = 0; kb < l1.nkb; kb++) {
           if ((int)(gs & 1u) != ggrp) { gs++; continue; }
           const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
-          mbar_wait(&gempty[st], ph ^ 1u);
-          gen_block(a, ti, r, kb, sG + st * kABytes);
+          // one poller warp per group (with a short sleep between polls), the others wait in a
+          // named barrier: spinning generators would take issue slots from the epilogue warps
+          if ((warp & 3) == 0) mbar_wait_sleep(&gempty[st], ph ^ 1u, 32);
+          named_bar(ggrp ? 5 : 4, 128);
+          if (MLPV_EXP != 203 && MLPV_EXP != 204) gen_block(a, ti, r, kb, sG + st * kABytes);
           fence_proxy_async();
           named_bar(ggrp ? 3 : 1, 128);
           if (r == 0) mbar_arrive(&gfull[st]);
@@ -742,8 +818,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 1) tmem_dealloc(tbase, kTmemCols);
+  if (warp == kWIss) tmem_dealloc(tbase, kTmemCols);
 }
+
+#ifdef MLPV_TRACE
+extern "C" int mlpv_kl_trace_read(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_kltrace, sizeof g_kltrace);
+}
+#endif
 
 // ----------------------------------------------------------------------------- host side
 struct LargeGeom {

@@ -277,17 +277,7 @@ void run(const char* name) {
 }
 
 int main() {
-  // run<0>("2CTA SS M256 N256 K16");
-  // run<14>("2CTA SS + 4 warps tcgen05.ld");
-  // run<18>("2CTA SS + 4 warps ld16/st8 in place");
-  // run<19>("2CTA SS + L3-like TS N=16 batches");
-  // run<7>("2CTA SS random bf16");
-  // run<20>("2CTA SS fp16 subnormal A x fp16 B");
-  run<13>("2CTA SS rings like k_fused3 (random)");
-  // run<24>("SS MMA + 8 epilogue-like warps");
-  // run<25>("8 epilogue-like warps alone");
-  run<26>("SS MMA + 8 epilogue-like warps, st waited");
-  run<27>("8 epilogue-like warps alone, st waited");
-  run<28>("SS MMA + 8 epilogue-like warps (st waited) + 12 philox/STS warps");
+  run<0>("2CTA SS M256 N256 K16");
+  run<3>("1CTA SS M128 N256 K16");
   return 0;
 }
