@@ -146,6 +146,37 @@ __device__ __forceinline__ uint32_t lattice_pair_bf16(uint32_t byte, uint32_t x2
   return bf2_u(__hmin2(y, one));
 }
 
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));   // sel nibble bit 3: sign-replicate
+  return d;
+}
+__device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// Eight u8 lattice pixels from one Philox word (nibble n -> pixel n): y = clamp(x + l*s + og, 0, 255),
+// two pixels per 32-bit word in 16-bit lanes biased by 256 (c2 = (256 + og) in both lanes; exact for
+// s >= 0, |og|, |s| <= 255: a lane stays in [1, 4591], no carry between lanes); the clamped lane is
+// 256 + y, whose low byte is y.
+__device__ __forceinline__ uint2 lattice8_u8(uint32_t w, uint2 x8, uint32_t s, uint32_t c2) {
+  const uint32_t t = w & 0x0F0F0F0Fu, u = (w >> 4) & 0x0F0F0F0Fu;   // even / odd pixels' levels
+  uint32_t y[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {                                     // pixels 2k, 2k+1
+    const uint32_t L = prmt(t, u, 0x8480u + 0x0101u * k);             // [l_2k, 0, l_2k+1, 0]
+    const uint32_t X = prmt(k < 2 ? x8.x : x8.y, 0u, (k & 1) ? 0x4342u : 0x4140u);   // [x_2k, 0, x_2k+1, 0]
+    y[k] = min_u16x2(max_u16x2(L * s + X + c2, 0x01000100u), 0x01FF01FFu);
+  }
+  return make_uint2(prmt(y[0], y[1], 0x6420u), prmt(y[2], y[3], 0x6420u));
+}
+
 // ----------------------------------------------------------------------------- generator
 __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot) {
   const int n0 = a.net.sizes[0];
@@ -183,8 +214,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           const int p = p0 + 8 * ww + 2 * k;               // pixels p, p+1
-          const uint32_t x2 = xv[k];
-          uint32_t y = lattice_pair_bf16((ws[ww] >> (8 * k)) & 0xFFu, x2, step2, org2);
+          uint32_t y = lattice_pair_bf16((ws[ww] >> (8 * k)) & 0xFFu, xv[k], step2, org2);
           if (p >= n0) y = 0;
           else if (p + 1 >= n0) y &= 0xFFFFu;
           o[k] = y;
@@ -202,6 +232,18 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
       uint4 w = make_uint4(0, 0, 0, 0);
       if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, k0, k1);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      if (p0 + 32 <= n0 && (n0 & 7) == 0 && s >= 0) {    // whole block in range: 16-bit-lane form
+        const uint32_t c2 = (uint32_t)(256 + og) * 0x00010001u;
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+          const uint2 xa = __ldg(reinterpret_cast<const uint2*>(x + p0 + 16 * half));
+          const uint2 xb2 = __ldg(reinterpret_cast<const uint2*>(x + p0 + 16 * half + 8));
+          const uint2 ya = lattice8_u8(ws[2 * half], xa, (uint32_t)s, c2);
+          const uint2 yb = lattice8_u8(ws[2 * half + 1], xb2, (uint32_t)s, c2);
+          *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (2 * q + half))) = make_uint4(ya.x, ya.y, yb.x, yb.y);
+        }
+        continue;
+      }
 #pragma unroll
       for (int half = 0; half < 2; half++) {
         uint32_t o[4];

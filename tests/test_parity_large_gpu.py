@@ -177,3 +177,30 @@ def test_cfg5_literal_all(P, oracle_mod):
         s = cfg.subset(n_base=2, begin=0, end=260)
         s.prop = M.Prop(M.PROP_THRESHOLD_LITERAL_ALL, -1, 0.0)
         chk_par(run_gpu(_checker(P, name), s), oracle_mod.check(s))
+
+
+@pytest.mark.parametrize("n0,step,origin", [(3072, -3.0, 20.0), (1000, 2.0, -15.0), (997, 1.0, -8.0),
+                                            (256, 17.0, -255.0)])
+def test_int8_lattice_generator_paths(P, oracle_mod, n0, step, origin):
+    """k_large's int8 lattice generator: the 16-bit-lane fast path (whole 32-pixel blocks, step >= 0)
+    and the per-pixel path (negative step, a ragged last block, n_0 not a multiple of 8), extreme
+    offsets that clamp at 0 and 255; bit-exact against the oracle."""
+    from mlpv_inputs.configs import _quant_int8
+    rng = np.random.default_rng([12933, 950, n0])
+    sizes = [n0, 256, 64, 10]
+    W = [rng.normal(0.0, np.sqrt(2.0 / sizes[l - 1]), (sizes[l], sizes[l - 1])).astype(np.float32) for l in range(1, 4)]
+    b = [rng.normal(0.0, np.sqrt(1.0 / sizes[l - 1]), sizes[l]).astype(np.float32) for l in range(1, 4)]
+    sh = [7, 6]
+    Wq, bq, acc = _quant_int8(W, b, sh)
+    net = M.Net(sizes, M.ACT_RELU, M.NUM_INT8, Wq, bq, requant_shift=sh, acc_scale=acc)
+    bases = np.rint(rng.random((3, n0)) * 255.0).astype(np.uint8)
+    bases[0, : n0 // 3] = 0
+    bases[1, : n0 // 3] = 255
+    pert = M.Pert(M.PERT_PHILOX_LATTICE, seed=int(rng.integers(2 ** 63)), n_samples=2 ** 20,
+                  lattice_step=step, lattice_origin=origin)
+    pert.index_end = 300
+    cfg = M.Config("i8gen", "int8 generator paths", net, bases, pert, M.Prop(), M.CovSpec([1, 2]))
+    chk = P.Checker(net)
+    assert_fixed_parity(run_gpu(chk, cfg), oracle_mod.check(cfg))
+    g, o = _eval(P, chk, cfg, 1, [0, 1, 299, 12345], oracle_mod)
+    assert np.array_equal(g.astype(np.int64), o.astype(np.int64))
