@@ -204,3 +204,35 @@ def test_int8_lattice_generator_paths(P, oracle_mod, n0, step, origin):
     assert_fixed_parity(run_gpu(chk, cfg), oracle_mod.check(cfg))
     g, o = _eval(P, chk, cfg, 1, [0, 1, 299, 12345], oracle_mod)
     assert np.array_equal(g.astype(np.int64), o.astype(np.int64))
+
+
+@pytest.mark.parametrize("name", ["cfg5_bf16", "cfg5_int8"])
+def test_cfg5_bench_launch(P, oracle_mod, name):
+    """The launch bench.py times for cfg5 (all 256 bases x a 1,024 (bf16) / 2,048 (int8) sample slice
+    of step 3).  Base 0 against the oracle on the same slice (int8 bit-exact, bf16 by the flag
+    rules of reading C20); every other base: every candidate counted and each first counterexample
+    re-evaluated by the oracle (decode + forward) to a changed class, or a near-tie for bf16."""
+    cfg = M.make_config(name)
+    chk = _checker(P, name)
+    S = 1024 if name == "cfg5_bf16" else 2048
+    lo, hi = 3 * S, 4 * S
+    g = run_gpu(chk, cfg.subset(begin=lo, end=hi))
+    assert np.all(g["checked"] == hi - lo)
+    fixed = name == "cfg5_int8"
+    tau = None if fixed else oracle_mod.default_tau(cfg)
+    o = oracle_mod.check(cfg.subset(n_base=1, base_start=0, begin=lo, end=hi), tau=tau)
+    if fixed:
+        assert int(g["violated"][0]) == int(o.violated[0]) and int(g["first_cex"][0]) == int(o.first_cex[0])
+        assert np.array_equal(g["cov_all"][:len(o.cov_all)] & o.cov_all, o.cov_all)
+    else:
+        vg, vo = int(g["violated"][0]), int(o.violated[0])
+        assert abs(vg - vo) <= min(int(g["flagged"][0]), int(o.flagged[0]))
+        assert int(g["first_cex"][0]) <= int(o.first_cex_unflagged[0])
+        assert int(o.first_cex[0]) <= int(g["first_cex_unflagged"][0])
+    for b in np.nonzero(g["first_cex"] != UMAX)[0][:12]:
+        c = int(g["first_cex"][b])
+        assert lo <= c < hi
+        y = oracle_mod.forward(cfg.net, oracle_mod.decode(cfg.net.numeric, cfg.pert, cfg.bases[b], int(b), c))[-1]
+        yb = oracle_mod.forward(cfg.net, cfg.bases[b])[-1]
+        top = np.sort(y)[::-1]
+        assert int(np.argmax(y)) != int(np.argmax(yb)) or (not fixed and top[0] - top[1] < 1e-5), (b, c)
