@@ -52,3 +52,39 @@ def reduce_results(res: Dict, n_base: int, n_words: int, group=None, stream=None
     import paper_1907_12933_b200 as P
     parts = allgather_results(res, n_base, n_words, group)
     return P.merge(parts, n_base, n_words, stream=stream)
+
+
+STEP_SHIFT = 48   # candidate indices < 2^48 in incremental mode (include/mlpv.h)
+
+
+def merge_incremental(parts: List[Dict], n_base: int) -> Dict:
+    """Incremental bounds across shards (SURVEY.md §8(f) NEXT-2 on several GPUs): the loop's answer for
+    a base input is the lexicographic minimum of the shards' (step, index) pairs, step 0 = none.
+    parts: per shard {"step", "first_cex", "step_unflagged", "first_cex_unflagged"} tensors."""
+    import torch
+    out = {}
+    for sk, ik in (("step", "first_cex"), ("step_unflagged", "first_cex_unflagged")):
+        keys = []
+        for p in parts:
+            st = p[sk][:n_base].to(torch.int64)
+            idx = p[ik][:n_base].to(torch.int64) & ((1 << STEP_SHIFT) - 1)
+            keys.append(torch.where(st > 0, (st << STEP_SHIFT) | idx, torch.full_like(st, 2 ** 63 - 1)))
+        k = torch.stack(keys).min(dim=0).values
+        hit = k != 2 ** 63 - 1
+        out[sk] = torch.where(hit, k >> STEP_SHIFT, torch.zeros_like(k)).to(torch.int32)
+        out[ik] = torch.where(hit, k & ((1 << STEP_SHIFT) - 1), torch.full_like(k, -1))   # -1 = UINT64_MAX
+    return out
+
+
+def allgather_incremental(res: Dict, n_base: int, group=None) -> Dict:
+    """All-gather of every rank's (step, index) pairs and their merge (merge_incremental)."""
+    import torch
+    import torch.distributed as dist
+    flat = torch.cat([res["step"][:n_base].to(torch.int64), res["first_cex"][:n_base].to(torch.int64),
+                      res["step_unflagged"][:n_base].to(torch.int64),
+                      res["first_cex_unflagged"][:n_base].to(torch.int64)]).contiguous()
+    bufs = [torch.empty_like(flat) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(bufs, flat, group=group)
+    parts = [{"step": b[:n_base], "first_cex": b[n_base:2 * n_base], "step_unflagged": b[2 * n_base:3 * n_base],
+              "first_cex_unflagged": b[3 * n_base:]} for b in bufs]
+    return merge_incremental(parts, n_base)

@@ -76,3 +76,39 @@ def test_gloo_world2_allgather_merge_equals_full_run():
         p.join(timeout=60)
     assert ok, viol
     assert sum(viol) > 0
+
+
+def _worker_inc(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import mlpv_inputs as M
+    from oracle import oracle as O
+    cfg = M.gamma_config(20)
+    b, e = PD.shard(0, cfg.pert.index_end, rank, world)
+    r = O.incremental_verify(cfg.subset(begin=b, end=e), 3.0, 12, 1)   # this rank's slice
+    res = {"step": torch.from_numpy(r["step"]), "first_cex": torch.from_numpy(r["first_cex"].view(np.int64)),
+           "step_unflagged": torch.from_numpy(r["step_unflagged"]),
+           "first_cex_unflagged": torch.from_numpy(r["first_cex_unflagged"].view(np.int64))}
+    merged = PD.allgather_incremental(res, cfg.n_base)
+    if rank == 0:
+        full = O.incremental_verify(cfg, 3.0, 12, 1)
+        ok = np.array_equal(merged["step"].numpy(), full["step"]) and \
+            np.array_equal(merged["first_cex"].numpy().view(np.uint64), full["first_cex"])
+        q.put((ok, int((full["step"] > 0).sum())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_incremental_merge_equals_full_loop():
+    """NEXT-2 sharded: each rank runs the incremental loop on half of every base's index range; the
+    lexicographic (step, index) minimum over ranks equals the loop over the whole range."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_inc, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok, n_hit = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+    assert ok and n_hit > 0
