@@ -533,15 +533,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               }
               if (l < L) {
                 const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
+                // y = clamp((u + rr) >> sh, 0, 255) (reading C18): cvt.pack.sat saturates two s32
+                // to u8 and packs them above c's low half, so two instructions pack four neurons
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
-                  uint32_t w4 = 0;
+                  int32_t t[4];
 #pragma unroll
-                  for (int k = 0; k < 4; k++) {
-                    const int i = 4 * q + k;
-                    const uint32_t y = i < nin ? (uint32_t)max(0, min(255, (u[i] + rr) >> sh)) : 0u;
-                    w4 |= y << (8 * k);
-                  }
+                  for (int k = 0; k < 4; k++) t[k] = 4 * q + k < nin ? (u[4 * q + k] + rr) >> sh : 0;
+                  uint32_t hi2, w4;
+                  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi2) : "r"(t[3]), "r"(t[2]));
+                  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(w4) : "r"(t[1]), "r"(t[0]), "r"(hi2));
                   hw[q] = w4;
                 }
               }
