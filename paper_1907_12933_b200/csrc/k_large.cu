@@ -33,7 +33,8 @@
 #endif
 // MLPV_EXP = 201: the weight tiles are not streamed (128 B per stage); 202: the epilogue skips its
 // per-column work (barriers only); 203: the generators skip the candidate generation;
-// 204: all three
+// 204: all three; 205: layer-1 chunk pairs share one accumulator; 206: two of the four MMAs per
+// layer-1 stage
 
 namespace mlpv {
 using namespace tc;
