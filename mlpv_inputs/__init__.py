@@ -14,6 +14,7 @@ from .configs import (  # noqa: F401
     NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8,
     ACT_SIGMOID, ACT_PL_SIGMOID, ACT_RELU,
     PERT_TUPLE_REPLACE, PERT_SUBSET_OFFSET, PERT_SUBSET_REPLACE, PERT_PHILOX_LATTICE, PERT_PHILOX_BOX,
+    PERT_PHILOX_CLAMP, cfg4_lattice, eight_bit_bf16,
     PROP_ARGMAX_UNCHANGED, PROP_TARGET_NEVER, PROP_THRESHOLD_LITERAL, PROP_THRESHOLD_LITERAL_ALL,
     Config, Net, Pert, Prop, CovSpec, make_config, CONFIG_IDS,
     f32_to_bf16_bits, bf16_bits_to_f32, vowel_net, pair_images, gamma_config,

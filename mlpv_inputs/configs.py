@@ -19,6 +19,7 @@ import numpy as np
 NUM_FP32, NUM_BF16, NUM_Q4_12, NUM_INT8 = 0, 1, 2, 3
 ACT_SIGMOID, ACT_PL_SIGMOID, ACT_RELU = 0, 1, 2
 PERT_TUPLE_REPLACE, PERT_SUBSET_OFFSET, PERT_SUBSET_REPLACE, PERT_PHILOX_LATTICE, PERT_PHILOX_BOX = 0, 1, 2, 3, 4
+PERT_PHILOX_CLAMP = 5
 PROP_ARGMAX_UNCHANGED, PROP_TARGET_NEVER, PROP_THRESHOLD_LITERAL, PROP_THRESHOLD_LITERAL_ALL = 0, 1, 2, 3
 
 CONFIG_IDS = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5_bf16", "cfg5_int8"]
@@ -244,19 +245,44 @@ def _cfg3() -> Config:
                   net, bases, pert, Prop(), CovSpec([1, 2]))
 
 
+def cfg4_lattice(eps: float = 0.05):
+    """(step, origin) of cfg4's 16-level lattice: step = bf16(2 eps / 15) (a dyadic value; for
+    eps = 0.05 it is 109 * 2^-14), origin = -7.5 step, so the offsets origin + l step, l = 0..15,
+    are the odd multiples of step / 2 in [-7.5 step, 7.5 step] (radius 7.5 step = 0.0499 for
+    eps = 0.05)."""
+    step = _bf16_scalar(2.0 * eps / 15.0)
+    return step, -7.5 * step
+
+
+def eight_bit_bf16(img: np.ndarray) -> np.ndarray:
+    """An image in [0, 1] as an 8-bit image (u8 / 255, as MNIST's pixels) stored as bf16 bits:
+    every pixel is 0 or >= 1/255."""
+    q = np.rint(np.clip(img.astype(np.float64), 0.0, 1.0) * 255.0) / 255.0
+    return f32_to_bf16_bits(q.astype(np.float32))
+
+
 def _cfg4() -> Config:
     sizes = [784, 256, 256, 10]
     W, b = _master_net(4, sizes, 2.0)
     Wb = [f32_to_bf16_bits(w) for w in W]
     img = smooth_blobs(_rng(4, 1), 1000)
-    bases = f32_to_bf16_bits(img)
+    bases = eight_bit_bf16(img)
     seed = int(_rng(4, 3).integers(2 ** 64, dtype=np.uint64))
     net = Net(sizes, ACT_RELU, NUM_BF16, Wb, b, acc_scale=[1.0, 1.0, 1.0])
-    # the exact L-inf box lattice (reading C14b): offsets -0.05 + l * 0.1/15, l = 0..15
-    pert = Pert(PERT_PHILOX_BOX, seed=seed, n_samples=2 ** 32, lattice_step=0.1 / 15.0, lattice_origin=-0.05)
+    # the L-inf box lattice of radius ~0.05 clamped to the image domain [0, 1] (reading C14)
+    step, origin = cfg4_lattice(0.05)
+    pert = Pert(PERT_PHILOX_CLAMP, seed=seed, n_samples=2 ** 32, lattice_step=step, lattice_origin=origin)
     pert.index_end = pert.n_samples
-    return Config("cfg4", "784-256-256-10 ReLU bf16, 1000 bases, 2^32 Philox L-inf eps=0.05 samples/base",
-                  net, bases, pert, Prop(), CovSpec([1, 2]))
+    return Config("cfg4", "784-256-256-10 ReLU bf16, 1000 bases, 2^32 Philox L-inf eps=0.05 samples/base, "
+                  "clamped to [0,1]", net, bases, pert, Prop(), CovSpec([1, 2]))
+
+
+def _cfg4_box() -> Config:
+    """cfg4's net and bases on the unclamped box (PHILOX_BOX, reading C14b): an extra space."""
+    c = copy.copy(_cfg4())
+    c.name = "cfg4_box"
+    c.pert = replace(c.pert, kind=PERT_PHILOX_BOX)
+    return c
 
 
 def _cfg5(variant: str) -> Config:
@@ -290,7 +316,7 @@ _CACHE = {}
 def make_config(name: str) -> Config:
     """Full-size config by name (cached; callers get a shallow copy)."""
     if name not in _CACHE:
-        builders = {"cfg1": _cfg1, "cfg2": _cfg2, "cfg3": _cfg3, "cfg4": _cfg4,
+        builders = {"cfg1": _cfg1, "cfg2": _cfg2, "cfg3": _cfg3, "cfg4": _cfg4, "cfg4_box": _cfg4_box,
                     "cfg5_bf16": lambda: _cfg5("bf16"), "cfg5_int8": lambda: _cfg5("int8")}
         _CACHE[name] = builders[name]()
     return copy.copy(_CACHE[name])

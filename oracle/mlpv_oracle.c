@@ -35,7 +35,7 @@
 
 enum { O_FP32 = 0, O_BF16 = 1, O_Q412 = 2, O_INT8 = 3 };
 enum { O_SIGMOID = 0, O_PLSIG = 1, O_RELU = 2 };
-enum { O_TUPLE = 0, O_SUB_OFF = 1, O_SUB_REP = 2, O_PHILOX = 3, O_BOX = 4 };
+enum { O_TUPLE = 0, O_SUB_OFF = 1, O_SUB_REP = 2, O_PHILOX = 3, O_BOX = 4, O_CLAMP = 5 };
 enum { O_UNCHANGED = 0, O_TARGET = 1, O_LITERAL = 2, O_LITERAL_ALL = 3 };
 
 typedef struct {
@@ -345,7 +345,11 @@ void orc_decode(int numeric, const opert *p, const void *base, int n0, int base_
 
 /* PHILOX_BOX (reading C14b): the same Philox levels as PHILOX_LATTICE, applied exactly,
  * x'_p = x_p + origin + l_p * step as a real number (no rounding to the input type, no clamping):
- * the 16-point lattice of the L-inf box of radius -origin around x.  Written as n0 doubles. */
+ * the 16-point lattice of the L-inf box of radius -origin around x.
+ * PHILOX_CLAMP (reading C14): the same point clamped to the image domain [0, 1],
+ * x'_p = min(max(x_p + origin + l_p * step, 0), 1) -- the box lattice intersected with the
+ * normalised images ("its values are normalized", §III.C; I in M^{mn},
+ * PAPER.md:438, 454).  Both written as n0 doubles (exact for dyadic step / origin). */
 void orc_decode_box(int numeric, const opert *p, const void *base, int n0, int base_id, uint64_t index, double *out) {
     uint32_t key[2] = { (uint32_t)p->seed, (uint32_t)(p->seed >> 32) };
     int nblk = (n0 + 31) / 32;
@@ -358,7 +362,9 @@ void orc_decode_box(int numeric, const opert *p, const void *base, int n0, int b
                 int px = 32 * j + 8 * ww + nb;
                 if (px >= n0) continue;
                 int l = (int)((w[ww] >> (4 * nb)) & 15u);
-                out[px] = in_get(numeric, base, px) + (p->origin + (double)l * p->step);
+                double v = in_get(numeric, base, px) + (p->origin + (double)l * p->step);
+                if (p->kind == O_CLAMP) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+                out[px] = v;
             }
     }
 }
@@ -524,6 +530,17 @@ static int within_restriction(int numeric, const void *base, const void *img, in
     return s2 <= b * b;
 }
 
+/* the same for a real-valued candidate (PHILOX_BOX / PHILOX_CLAMP): the sum over all pixels, in
+ * pixel order, of (x'_p - x_p)^2 in double against b^2 */
+static int within_restriction_real(int numeric, const void *base, const double *img, int n0, double b) {
+    double s2 = 0.0;
+    for (int p = 0; p < n0; p++) {
+        double d = img[p] - in_get(numeric, base, p);
+        s2 += d * d;
+    }
+    return s2 <= b * b;
+}
+
 /* ------------------------------------------------------------------ the check */
 
 static double rne(double v) { return nearbyint(v); }
@@ -564,7 +581,7 @@ int orc_check(const onet *n, const void *bases, int n_base, const opert *p, cons
             double *tc = (double *)malloc(sizeof(double) * T);
             double *h = (double *)malloc(sizeof(double) * dn.maxw), *hn = (double *)malloc(sizeof(double) * dn.maxw);
             void *img = malloc(esz * (size_t)n0);
-            double *ximg = p->kind == O_BOX ? (double *)malloc(sizeof(double) * (size_t)n0) : NULL;
+            double *ximg = (p->kind == O_BOX || p->kind == O_CLAMP) ? (double *)malloc(sizeof(double) * (size_t)n0) : NULL;
             uint32_t *wa = (uint32_t *)calloc(nwords + 1, 4), *wc = (uint32_t *)calloc(nwords + 1, 4);
             uint32_t *wt = (uint32_t *)calloc(nwords + 1, 4);
             int cert[64];
@@ -575,7 +592,8 @@ int orc_check(const onet *n, const void *bases, int n_base, const opert *p, cons
                 uint64_t c = (uint64_t)ci;
                 if (ximg) orc_decode_box(n->numeric, p, base, n0, b, c, ximg);
                 else orc_decode(n->numeric, p, base, n0, b, c, img);
-                if (p->restrict_l2 > 0 && !within_restriction(n->numeric, base, img, n0, p->restrict_l2))
+                if (p->restrict_l2 > 0 && !(ximg ? within_restriction_real(n->numeric, base, ximg, n0, p->restrict_l2)
+                                                 : within_restriction(n->numeric, base, img, n0, p->restrict_l2)))
                     continue;
                 if (forward_d(&dn, img, ximg, tc, h, hn)) lbad = 1;
                 int flag;

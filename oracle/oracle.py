@@ -189,12 +189,12 @@ def space_size(pert, n0: int) -> int:
 
 
 def decode(numeric: int, pert, base: np.ndarray, base_id: int, index: int) -> np.ndarray:
-    """Candidate `index` of base `base_id` in the net's input type; PHILOX_BOX candidates are
-    exact real values and come back as float64."""
+    """Candidate `index` of base `base_id` in the net's input type; PHILOX_BOX / PHILOX_CLAMP
+    candidates are exact real values and come back as float64."""
     keep = _Keep()
     p = _mk_pert(pert, keep)
     b = keep.arr(base, base.dtype)
-    if pert.kind == 4:
+    if pert.kind in (4, 5):                             # PHILOX_BOX, PHILOX_CLAMP
         out = np.empty(b.shape[0], np.float64)
         lib().orc_decode_box(numeric, C.byref(p), b.ctypes.data, b.shape[0], base_id, C.c_uint64(index),
                              _p(out, C.c_double))
@@ -229,6 +229,25 @@ def cover_traces(sizes, t1: List[np.ndarray], t2: List[np.ndarray], pairs, dg, d
                     len(pairs), _p(lo, C.c_int32), _p(g, C.c_double), _p(h, C.c_double),
                     _p(w, C.c_uint32))
     return w[:n]
+
+
+def cover_traces_tau(sizes, t1: List[np.ndarray], t2: List[np.ndarray], pairs, dg, dh, tau):
+    """As cover_traces, plus certain[p] = no predicate of pair p within tau of its decision
+    boundary (reading C20; tau per layer, trace units)."""
+    s = np.ascontiguousarray(sizes, dtype=np.int32)
+    a = np.ascontiguousarray(np.concatenate(t1), dtype=np.float64)
+    b = np.ascontiguousarray(np.concatenate(t2), dtype=np.float64)
+    lo = np.ascontiguousarray(pairs, dtype=np.int32)
+    g = np.ascontiguousarray(dg, dtype=np.float64)
+    h = np.ascontiguousarray(dh, dtype=np.float64)
+    tu = np.ascontiguousarray(tau, dtype=np.float64)
+    n, _ = coverage_layout(sizes, pairs)
+    w = np.zeros(max(n, 1), np.uint32)
+    cert = np.zeros(max(len(pairs), 1), np.int32)
+    lib().orc_cover_tau(_p(s, C.c_int32), len(sizes) - 1, _p(a, C.c_double), _p(b, C.c_double),
+                        len(pairs), _p(lo, C.c_int32), _p(g, C.c_double), _p(h, C.c_double),
+                        _p(tu, C.c_double), _p(w, C.c_uint32), _p(cert, C.c_int))
+    return w[:n], cert[:len(pairs)].astype(bool)
 
 
 def incremental_schedule(gamma: float, max_bound: int, granularity: int = 1) -> List[float]:

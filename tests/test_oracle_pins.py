@@ -455,7 +455,7 @@ def test_philox_box_values_and_linearity(oracle_mod):
     in both spaces), |x' - x| <= eps, levels uniform (chi^2), and the layer-1 potentials of a
     candidate equal W1 x' + b1 by numpy's float64 matmul (library routine)."""
     O = oracle_mod
-    cfg = M.make_config("cfg4")
+    cfg = M.make_config("cfg4_box")
     p = cfg.pert
     assert p.kind == M.PERT_PHILOX_BOX
     step, org = p.lattice_step, p.lattice_origin
@@ -485,6 +485,68 @@ def test_philox_box_values_and_linearity(oracle_mod):
         assert np.allclose(u1, W1 @ y + b1, rtol=1e-12, atol=1e-12)
     e = counts.sum() / 16
     assert float(np.sum((counts - e) ** 2 / e)) < 50.0
+
+
+def test_philox_clamp_is_the_clipped_box(oracle_mod):
+    """PHILOX_CLAMP (reading C14; "normalized", I in M^{mn} PAPER.md:438/454): each
+    candidate is the PHILOX_BOX point (pinned above) clipped to [0, 1] by numpy (library routine):
+    x'_p = x_p + origin + l_p step where that lies in [0, 1], else 0 / 1; so |x' - x| <= 7.5 step,
+    every pixel in [0, 1], the zero lattice (step = origin = 0) reproduces the base, and the
+    layer-1 potentials equal W1 x' + b1 by numpy's float64 matmul."""
+    O = oracle_mod
+    cfg = M.make_config("cfg4")
+    p = cfg.pert
+    assert p.kind == M.PERT_PHILOX_CLAMP and p.lattice_step == 109 * 2.0 ** -14 and p.lattice_origin == -7.5 * p.lattice_step
+    box = M.make_config("cfg4_box").pert
+    W1 = M.bf16_bits_to_f32(cfg.net.W[0]).astype(np.float64)
+    b1 = np.asarray(cfg.net.b[0], np.float64)
+    n_lo = n_hi = 0
+    for bi in (3, 500):
+        xb = cfg.bases[bi]
+        xv = M.bf16_bits_to_f32(xb).astype(np.float64)
+        for idx in (0, 1, 77, 2 ** 31 + 5, 2 ** 32 - 1):
+            y = O.decode(cfg.net.numeric, p, xb, bi, idx)
+            yb = O.decode(cfg.net.numeric, box, xb, bi, idx)
+            assert y.dtype == np.float64 and np.array_equal(y, np.clip(yb, 0.0, 1.0))
+            assert y.min() >= 0.0 and y.max() <= 1.0 and np.max(np.abs(y - xv)) <= 7.5 * p.lattice_step
+            n_lo += int(np.sum(yb < 0)); n_hi += int(np.sum(yb > 1))
+            u1 = O.forward(cfg.net, y)[0]
+            assert np.allclose(u1, W1 @ y + b1, rtol=1e-12, atol=1e-12)
+        z = Pert(M.PERT_PHILOX_CLAMP, seed=p.seed, n_samples=p.n_samples, lattice_step=0.0, lattice_origin=0.0)
+        assert np.array_equal(O.decode(cfg.net.numeric, z, xb, bi, 12345), xv)
+    assert n_lo > 1000 and n_hi > 0                       # both bounds are exercised on cfg4's bases
+
+
+def _clamp_net_cfg():
+    """n_0 = 2 (pixel 0 takes nibble 0 of Philox word 0), hidden u = (x0', -x0', x0' - 1) ReLU, logits
+    y0 = 0.995, y1 = 1000 (h1 + h2), y2 = 1.97 - h0.  With the clamp h1 = h2 = 0, so y1 = 0.
+    Base A, x0 = 253/256: class 0; violated iff x0' < 0.975, i.e. origin + l step < -0.0133, l <= 5.
+    Base B, x0 = bf16(0.01): class 2; never violated.  A candidate outside [0, 1] would light y1:
+    without the upper clamp A gains the l >= 10 candidates, without the lower one B gains l <= 5."""
+    f = np.float32
+    W = [M.f32_to_bf16_bits(np.array([[1, 0], [-1, 0], [1, 0]], f)),
+         M.f32_to_bf16_bits(np.array([[0, 0, 0], [0, 1000, 1000], [-1, 0, 0]], f))]
+    b = [np.array([0, 0, -1], f), np.array([0.995, 0, 1.97], f)]
+    net = Net([2, 3, 3], M.ACT_RELU, M.NUM_BF16, W, b, acc_scale=[1.0, 1.0])
+    bases = M.f32_to_bf16_bits(np.array([[253 / 256, 0.5], [0.01, 0.5]], f))
+    step, origin = M.cfg4_lattice(0.05)
+    pert = Pert(M.PERT_PHILOX_CLAMP, seed=0x1234_5678_9ABC_DEF0, n_samples=2 ** 32, lattice_step=step,
+                lattice_origin=origin, index_begin=1000, index_end=3000)
+    return Config("clampnet", "clamp closed form", net, bases, pert, Prop(), CovSpec([1]))
+
+
+def test_clamp_net_closed_form(oracle_mod):
+    """The check on PHILOX_CLAMP against levels read straight off the Philox stream: violations of
+    base A = #{c : l_0(c) <= 5}, first counterexample the first such c, base B none (C14/C15)."""
+    O = oracle_mod
+    cfg = _clamp_net_cfg()
+    r = O.check(cfg)
+    key = [cfg.pert.seed & 0xFFFFFFFF, cfg.pert.seed >> 32]
+    lv = np.array([int(O.philox([c, 0, 0, 0], key)[0]) & 15 for c in range(1000, 3000)])
+    hits = np.nonzero(lv <= 5)[0]
+    assert int(r.checked[0]) == 2000 and int(r.violated[0]) == len(hits) and int(r.first_cex[0]) == 1000 + hits[0]
+    assert int(r.violated[1]) == 0 and int(r.flagged.sum()) == 0
+    assert 2000 * 6 / 16 - 150 < len(hits) < 2000 * 6 / 16 + 150
 
 
 def test_philox_is_counter_sensitive(oracle_mod):
@@ -580,6 +642,70 @@ def test_check_invariants(oracle_mod):
             # and nothing below it is a violation
             lo = O.check(cfg.subset(n_base=1, base_start=bi, begin=0, end=int(full.first_cex[bi])))
             assert int(lo.violated[0]) == 0
+
+
+def test_target_never_closed_form(oracle_mod):
+    """TARGET_NEVER (C12, PAPER.md:466-479 with a target class): on the q = 5 threshold net class 1
+    iff a + b > 4 (ties to class 0), so t = 0 is violated by the 15 pairs with a + b <= 4, first at
+    c = 0, and t = 1 by the other 10, first at (1, 4) -> 9 -- unlike ARGMAX_UNCHANGED, t = 0 is
+    violated by the base class itself.  Float (levels l/4, exact): the 5 ties a + b = 4 are flagged."""
+    O = oracle_mod
+    for numeric, levels in ((M.NUM_Q4_12, np.array([1024 * l for l in range(5)], np.int16)),
+                            (M.NUM_FP32, np.array([l / 4 for l in range(5)], np.float32))):
+        for t, nv, first in ((0, 15, 0), (1, 10, 9)):
+            cfg = _threshold_cfg(numeric, 5, levels)
+            cfg.prop = Prop(M.PROP_TARGET_NEVER, t, 0.0)
+            r = O.check(cfg)
+            assert int(r.violated[0]) == nv and int(r.first_cex[0]) == first, (numeric, t)
+            assert int(r.flagged[0]) == (5 if numeric == M.NUM_FP32 else 0)
+
+
+def test_ambiguity_rules_inside_outside(oracle_mod):
+    """Reading C20, one rule at a time on a hand-built trace pair for pair (1, 2), tau = 0.01,
+    d = 0.1: a sign predicate with |u| < tau, a value predicate with ||du| - d| < tau and a
+    distance predicate (no layer-1 sign change) with |Linf - d| < tau make the pair uncertain;
+    the same traces with the quantity at 2 tau from the boundary are certain.  The covered words
+    do not depend on tau."""
+    O = oracle_mod
+    sizes, tau, d = [2, 2, 2], [0.01, 0.01], 0.1
+
+    def run(t1, t2):
+        w, cert = O.cover_traces_tau(sizes, [np.array(x, float) for x in t1], [np.array(x, float) for x in t2],
+                                     [1], [d, d], [d, d], tau)
+        w0 = O.cover_traces(sizes, [np.array(x, float) for x in t1], [np.array(x, float) for x in t2], [1], [d, d], [d, d])
+        assert np.array_equal(w, w0)
+        return bool(cert[0])
+
+    base = ([1.0, 2.0], [1.0, -1.0])
+    # everything far from every boundary: layer-1 Linf 0.5, layer-2 |du| = 0.5, no sign changes
+    assert run(base, ([1.5, 2.0], [1.5, -1.5]))
+    # sign: a layer-2 potential of the candidate at 0.005 (inside) / 0.02 (outside)
+    assert not run(base, ([1.5, 2.0], [0.005, -1.5]))
+    assert run(base, ([1.5, 2.0], [0.02, -1.5]))
+    # sign on layer 1 (the lower layer of the pair), and on the base trace
+    assert not run(base, ([-0.005, 2.0], [1.5, -1.5]))
+    assert not run(([0.005, 2.0], [1.0, -1.0]), ([1.5, 2.0], [1.5, -1.5]))
+    # value: layer-2 |du| = 0.105 (inside) / 0.12 (outside) of d = 0.1
+    assert not run(base, ([1.5, 2.0], [1.105, -1.5]))
+    assert run(base, ([1.5, 2.0], [1.12, -1.5]))
+    # distance: layer-1 Linf = 0.095 (inside) / 0.08 (outside), no sign change in layer 1
+    assert not run(base, ([1.095, 2.0], [1.5, -1.5]))
+    assert run(base, ([1.08, 2.0], [1.5, -1.5]))
+    # the distance rule applies only without a layer-1 sign change
+    assert run(([1.0, 2.0], [1.0, -1.0]), ([-1.0, 2.095], [1.5, -1.5]))
+
+
+def test_default_tau_closed_form(oracle_mod):
+    """C20: tau_l = 1e-6 + 1e-5 max over the bases of max |u_l^base|; on W1 = I, W2 = 2 I (fp32,
+    zero biases, ReLU) the base potentials are u1 = x, u2 = 2 ReLU(x)."""
+    O = oracle_mod
+    net = Net([2, 2, 2], M.ACT_RELU, M.NUM_FP32, [np.eye(2, dtype=np.float32), 2 * np.eye(2, dtype=np.float32)],
+              [np.zeros(2, np.float32), np.zeros(2, np.float32)], acc_scale=[1.0, 1.0])
+    bases = np.array([[0.5, -0.75], [0.25, 0.375]], np.float32)
+    cfg = Config("tau", "tau", net, bases, Pert(M.PERT_TUPLE_REPLACE, tuple=1, levels=np.zeros(1, np.float32)),
+                 Prop(), CovSpec([1]))
+    t = O.default_tau(cfg)
+    assert np.allclose(t, [1e-6 + 1e-5 * 0.75, 1e-6 + 1e-5 * 1.0], rtol=0, atol=1e-15)
 
 
 def _literal_cfg(numeric, prop_kind):

@@ -33,6 +33,16 @@ MUTATIONS = {
     "lattice clamp missing": ("v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);\n                    v = orc_rne_bf16(v);",
                               "v = orc_rne_bf16(v);"),
     "near-tie flag off": ("if (n > 1 && top1 - top2 < near_tie) *flag = 1;", "(void)top2;"),
+    # round 2 (VERDICT r1 "unpinned oracle parts")
+    "TARGET_NEVER inverted": ("if (pr->kind == O_TARGET) return cls == pr->target;",
+                              "if (pr->kind == O_TARGET) return cls != pr->target;"),
+    "distance ambiguity dropped": ("if (tau && n_sc == 0 && fabs(linf - dh[k - 1]) < tau[k - 1]) amb = 1;", ""),
+    "value ambiguity dropped": ("|| fabs(d - dg[k]) < tau[k])) amb = 1;", ")) amb = 1;"),
+    "sign ambiguity on one trace only": ("if (tau && (fabs(a1[i]) < tau[k - 1] || fabs(a2[i]) < tau[k - 1])) amb = 1;",
+                                         "if (tau && (fabs(a2[i]) < tau[k - 1])) amb = 1;"),
+    "box clamp missing (PHILOX_CLAMP)": ("if (p->kind == O_CLAMP) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);", ""),
+    "box clamp upper bound missing": ("if (p->kind == O_CLAMP) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);",
+                                      "if (p->kind == O_CLAMP) v = v < 0.0 ? 0.0 : v;"),
 }
 
 
