@@ -51,7 +51,7 @@ def alg_ops_per_candidate(cfg):
     (dense) spaces; the incremental layer-1 update (|S| x n_1) + dense later layers for subset spaces."""
     s = cfg.net.sizes
     dense_rest = sum(s[l - 1] * s[l] for l in range(2, len(s)))
-    if cfg.pert.kind in (3, 4):                  # Philox spaces: every pixel moves
+    if cfg.pert.kind in (3, 4, 5):                  # Philox spaces: every pixel moves
         return 2 * (s[0] * s[1] + dense_rest)
     changed = cfg.pert.tuple if cfg.pert.kind == 0 else len(cfg.pert.pixels)
     return 2 * (changed * s[1] + dense_rest)
@@ -119,7 +119,7 @@ def to_device(bases, device):
 
 
 def samples_for(cfg, args):
-    if cfg.pert.kind not in (3, 4):
+    if cfg.pert.kind not in (3, 4, 5):
         return None
     return args.samples or DEFAULT_SAMPLES[cfg.name]
 
@@ -319,7 +319,7 @@ def main():
     ops = alg_ops_per_candidate(cfg)
     kern_avg_s = (sum(kern_ms) / len(kern_ms)) / 1e3
     per_launch = n_cand / args.steps
-    if cfg.pert.kind in (3, 4):
+    if cfg.pert.kind in (3, 4, 5):
         bound, unit = "tensor", "TFLOP/s"
         peak = float(pk["bf16_tflops"]) * (2.0 if cfg.net.numeric == M.NUM_INT8 else 1.0)
         peak_note = f"{src} bf16 burst" + (" x2 (int8 nominal ratio)" if cfg.net.numeric == M.NUM_INT8 else "")
@@ -334,7 +334,7 @@ def main():
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get(cfg.name)
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                "traffic": traffic, "kernel": ("k_fused3" if cfg.pert.kind == 4 else "k_large") if cfg.pert.kind in (3, 4) else "k_small",
+                "traffic": traffic, "kernel": ("k_fused3" if cfg.pert.kind in (4, 5) else "k_large") if cfg.pert.kind in (3, 4, 5) else "k_small",
                 "kernel_ms": 1e3 * kern_avg_s, "peak_source": peak_note,
                 "alg_ops_per_candidate": ops, "candidates_per_launch": per_launch}
 

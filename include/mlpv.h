@@ -107,6 +107,19 @@ typedef struct {
  *                  origin W_1 1 + step W_1 l.  BF16 numerics, 3-layer nets with 256-wide hidden
  *                  layers (the k_fused3 path); other nets return MLPV_E_UNSUPPORTED.
  *                  mlpv_decode writes the candidate as n_0 doubles.
+ *   PHILOX_CLAMP   the same Philox levels and box lattice, clamped to the image domain:
+ *                  x'_p = min(max(x_p + origin + l_p * step, 0), 1) as a real number (reading C14:
+ *                  "its values are normalized", §III.C; the candidate I lies in
+ *                  M^{mn} of the restriction R).  BF16 numerics, base pixels
+ *                  in [0, 1].  The tensor-core path (k_fused3: 3-layer nets with 256-wide hidden
+ *                  layers, n_0 even, n_0 <= 1024) contracts d = x' - x = min(max(origin + l step,
+ *                  -x), 1 - x) exactly in fp16 against W_1, which needs: every offset
+ *                  (origin + l step) * 2^s and step * 2^(24+s) exactly representable in fp16 for
+ *                  the library's scale s (MLPV_E_UNSUPPORTED otherwise; cfg4's step = 109 * 2^-14,
+ *                  origin = -7.5 step qualify, s = -1), and every base pixel x = 0 or x * 2^s
+ *                  representable (x >= 2^(-17-s)); a base image that breaks the last rule is
+ *                  reported by mlpv_sync (MLPV_E_INVALID, the candidates' results are then not
+ *                  exact).  mlpv_decode writes the candidate as n_0 doubles.
  * `levels` element type: float (FP32) | uint16 bf16 bits (BF16) | int16 (Q4_12, INT8).
  * Every call processes the half-open index range [index_begin, index_end) of EVERY base input;
  * disjoint ranges merge by sum / min / OR (mlpv_merge). */
@@ -115,7 +128,8 @@ typedef enum {
     MLPV_PERT_SUBSET_OFFSET = 1,
     MLPV_PERT_SUBSET_REPLACE = 2,
     MLPV_PERT_PHILOX_LATTICE = 3,
-    MLPV_PERT_PHILOX_BOX = 4
+    MLPV_PERT_PHILOX_BOX = 4,
+    MLPV_PERT_PHILOX_CLAMP = 5
 } mlpv_pert_kind;
 
 typedef struct {
@@ -259,6 +273,12 @@ mlpv_status mlpv_eval(mlpv_t h, const void *base_inputs, int32_t n_base, int32_t
  * (base_input and image_out: host [n_0] in the input element type). */
 mlpv_status mlpv_decode(mlpv_numeric numeric, const mlpv_pert *pert, const void *base_input,
                         int32_t n_0, int32_t base_id, uint64_t index, void *image_out);
+
+/* Synchronise `stream` and report what the device found since the last call: MLPV_E_CUDA
+ * (sticky) for an asynchronous kernel fault, MLPV_E_INVALID for an input error detected on the
+ * device (a PHILOX_CLAMP base image that breaks its exactness rule; the status is then cleared).
+ * mlpv_check / mlpv_eval never synchronise; a caller that reads results calls this first. */
+mlpv_status mlpv_sync(mlpv_t h, void *stream);
 
 /* Merge n_parts partial results of disjoint index ranges (device, laid out part-major:
  * counts [n_parts x n_base], words [n_parts x n_words]) into `out` by sum / min / OR on `stream`.

@@ -24,7 +24,7 @@ STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_UNSUPPORTED", 4: "E_OVERF
 EXPORTS = ["mlpv_create", "mlpv_destroy", "mlpv_last_error", "mlpv_coverage_layout", "mlpv_space_size",
            "mlpv_check", "mlpv_eval", "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_pair_coverage",
            "mlpv_check_incremental", "mlpv_incremental_steps", "mlpv_incremental_bound",
-           "mlpv_profile", "mlpv_version"]
+           "mlpv_profile", "mlpv_sync", "mlpv_version"]
 
 
 class MlpvError(RuntimeError):
@@ -104,9 +104,10 @@ def lib() -> C.CDLL:
         L.mlpv_incremental_bound.restype = C.c_double
         L.mlpv_incremental_bound.argtypes = [C.POINTER(_Inc), C.c_int32]
         L.mlpv_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+        L.mlpv_sync.argtypes = [C.c_void_p, C.c_void_p]
         L.mlpv_version.restype = C.c_char_p
         for f in ("mlpv_create", "mlpv_coverage_layout", "mlpv_space_size", "mlpv_check", "mlpv_eval",
-                  "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_profile"):
+                  "mlpv_decode", "mlpv_merge", "mlpv_neuron_coverage", "mlpv_profile", "mlpv_sync"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -158,12 +159,12 @@ def _stream_ptr(stream):
 
 
 def decode(numeric: int, pert, base: np.ndarray, base_id: int, index: int) -> np.ndarray:
-    """Host-side candidate reconstruction (counterexample images); PHILOX_BOX candidates are exact
-    reals and come back as float64."""
+    """Host-side candidate reconstruction (counterexample images); PHILOX_BOX / PHILOX_CLAMP
+    candidates are exact reals and come back as float64."""
     keep = _Keep()
     p = _mk_pert(pert, keep)
     b = keep.arr(base, base.dtype)
-    out = np.empty(b.shape[0], np.float64) if pert.kind == 4 else np.empty_like(b)
+    out = np.empty(b.shape[0], np.float64) if pert.kind in (4, 5) else np.empty_like(b)
     _ck(lib().mlpv_decode(numeric, C.byref(p), b.ctypes.data, b.shape[0], base_id, C.c_uint64(int(index)),
                           out.ctypes.data))
     return out
@@ -309,6 +310,11 @@ class Checker:
                             C.c_void_p(indices.data_ptr()), n, C.c_void_p(out.data_ptr()), _stream_ptr(stream)),
             self._h)
         return out[:n]
+
+    def sync(self, stream=None):
+        """mlpv_sync: wait for `stream` and raise MlpvError for an asynchronous kernel fault or an
+        input error the device found (call before reading results)."""
+        _ck(lib().mlpv_sync(self._h, _stream_ptr(stream)), self._h)
 
     def profile(self, ev_begin=None, ev_end=None) -> int:
         """Record torch.cuda.Event pair around the enumeration kernel of later checks (None

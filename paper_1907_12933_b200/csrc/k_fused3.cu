@@ -147,8 +147,11 @@ struct Args {
   int64_t eval_n;
   int eval_base;
   float* eval_out;
-  float stepS;                               // PHILOX_BOX: step * 2^24 (u1 = base1 + stepS * acc)
-  const float* base1;                        // [n_base][256] W1 x + b1 + origin W1 1
+  float stepS;                               // u1 = base1 + stepS * acc: PHILOX_BOX step * 2^24, PHILOX_CLAMP 2^-s
+  const float* base1;                        // [n_base][256] W1 x + b1 (+ origin W1 1 for PHILOX_BOX)
+  int clamp;                                 // PHILOX_CLAMP: A = d 2^s = min(max(fma(l 2^-24, m, c), -x 2^s), (1-x) 2^s)
+  uint32_t cm2, cc2;                         // fp16x2 m = step 2^(24+s), c = origin 2^s
+  const uint4* clampc;                       // [n_base][ceil(n0/8)][2] {-x 2^s} | {(1-x) 2^s} fp16x2 words
 };
 
 struct alignas(16) Smem {
@@ -175,6 +178,7 @@ struct alignas(16) Smem {
   uint32_t sc2[8][128];                      // E2: sign-change words of layer 2
   uint16_t vc2[16][128];                     // E2 slow path: value-change bits of layer 2 (16 neurons)
   alignas(16) float c1row[8][128];           // E2: the layer-2 potentials of a warp's single cond1 row
+  alignas(16) uint4 ctab[kMaxN0 / 8][2];     // generators, PHILOX_CLAMP: the staged base's clamp bounds
 };
 
 constexpr size_t kTilesBytes = (size_t)(kSG + kSW) * kTile + (size_t)kChunks * kW3Chunk + 4 * kBiasTile;
@@ -236,6 +240,26 @@ __device__ __forceinline__ uint4 nibble_word(uint32_t w) {
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(o[k]) : "r"(lo), "r"(hi), "r"(sel));   // (__byte_perm drops
   }                                                                             //  the sign-replicate bit)
   return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// PHILOX_CLAMP (reading C14): the A operand of a pixel pair, d 2^s = min(max(off 2^s, -x 2^s), (1-x) 2^s)
+// in fp16, with off 2^s = fma(l 2^-24, step 2^(24+s), origin 2^s) from the subnormal levels.  Every
+// step is exact (the host picked s so that each offset is an fp16 value; the bounds are exact where
+// they bind, checked by the base prologue), so the layer-1 MMA contracts W1 (x' - x) exactly up to
+// its fp32 accumulation of small terms.
+__device__ __forceinline__ uint32_t clamp_pair(uint32_t lv, uint32_t m2, uint32_t c2, uint32_t nx, uint32_t px) {
+  // (intrinsics rather than asm so that ptxas can take m2 / c2 straight from the parameter bank)
+  const __half2 o = __hfma2(*reinterpret_cast<const __half2*>(&lv), *reinterpret_cast<const __half2*>(&m2),
+                            *reinterpret_cast<const __half2*>(&c2));
+  const __half2 d = __hmin2(__hmax2(o, *reinterpret_cast<const __half2*>(&nx)), *reinterpret_cast<const __half2*>(&px));
+  return *reinterpret_cast<const uint32_t*>(&d);
+}
+
+// four pixel pairs (one 16-byte chunk of the A row) with the chunk's staged bounds {nx | px}
+__device__ __forceinline__ uint4 clamp_chunk(uint4 o, const uint4 (&b)[2], uint32_t m2, uint32_t c2) {
+  const uint4 nx = b[0], px = b[1];
+  return make_uint4(clamp_pair(o.x, m2, c2, nx.x, px.x), clamp_pair(o.y, m2, c2, nx.y, px.y),
+                    clamp_pair(o.z, m2, c2, nx.z, px.z), clamp_pair(o.w, m2, c2, nx.w, px.w));
 }
 
 // h = max(u, 0) = hi + lo + O(2^-22 h): hi = RZ_f16(h), lo = RN_f16(h - hi) (relu'd), with the
@@ -608,9 +632,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
     const int nblk = (a.n0 + 31) / 32;                     // Philox blocks holding pixels
     const int kneed = 16 * a.nk16;                         // K elements the MMA reads
+    const bool clampk = a.clamp != 0;
+    int gbase = -1;                                        // base whose clamp bounds are staged
     for (uint64_t t = t_begin; t < t_end; t++, tl++) {
       if (gt == 0) TR(tl, 6);
       const TileInfo ti = tile_info(a, t);
+      if (clampk && ti.b != gbase) {
+        // every generator thread meets this barrier at the same tile (the tile sequence is the
+        // cluster's), after all its stages of the previous base: then the table is free
+        named_bar(13, 32 * kNGenGroups * 4);
+        const int nch = (a.n0 + 7) / 8;
+        const uint4* src = a.clampc + (size_t)ti.b * 2 * nch;
+        for (int i = gt; i < 2 * (kMaxN0 / 8); i += 32 * kNGenGroups * 4)
+          (&S.ctab[0][0])[i] = (i >> 1) < nch ? src[i] : make_uint4(0, 0, 0, 0);   // beyond n_0: d = 0
+        named_bar(13, 32 * kNGenGroups * 4);
+        gbase = ti.b;
+      }
       const int grow = 128 * (int)rank + r;
       uint64_t c;
       if (a.eval_idx) c = grow < ti.nvalid ? a.eval_idx[ti.start + grow] : 0;
@@ -620,16 +657,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       for (int kb = (int)((grp + kNGenGroups - gs0 % kNGenGroups) % kNGenGroups); kb < a.nkb1; kb += kNGenGroups) {
         const uint32_t gs = gs0 + kb;
         TRG(tl, kb, 0);
-        uint4 out[8];
+        // A operand of the 64-pixel K block: the first 32 pixels (Philox block 2 kb) are finished
+        // before the slot wait, the second block's words stay raw (4 registers) until after it
+        // (the clamped form would not fit the generator's 72 registers with all 8 chunks live)
+        uint4 out[4];
+        uint4 w1;
         {
           const int j = 2 * kb;
           const uint4 z = make_uint4(0, 0, 0, 0);
           const uint4 w0 = j < nblk ? philox(c0, c1, cb, (uint32_t)j, k0, k1) : z;
-          const uint4 w1 = j + 1 < nblk ? philox(c0, c1, cb, (uint32_t)(j + 1), k0, k1) : z;
+          w1 = j + 1 < nblk ? philox(c0, c1, cb, (uint32_t)(j + 1), k0, k1) : z;
           out[0] = nibble_word(w0.x); out[1] = nibble_word(w0.y);
           out[2] = nibble_word(w0.z); out[3] = nibble_word(w0.w);
-          out[4] = nibble_word(w1.x); out[5] = nibble_word(w1.y);
-          out[6] = nibble_word(w1.z); out[7] = nibble_word(w1.w);
+          if (clampk) {
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) out[ch] = clamp_chunk(out[ch], S.ctab[8 * kb + ch], a.cm2, a.cc2);
+          }
         }
         const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
         TRG(tl, kb, 1);
@@ -639,9 +682,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         uint8_t* slot = sG + st * kTile;
         const int e0 = 64 * kb;
 #pragma unroll
-        for (int ch = 0; ch < 8; ch++)
+        for (int ch = 0; ch < 4; ch++)
           if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)         // only the K steps the MMA reads
             *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = out[ch];
+        const uint32_t w1w[4] = {w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int ch = 4; ch < 8; ch++) {
+          uint4 o = nibble_word(w1w[ch - 4]);
+          if (clampk) o = clamp_chunk(o, S.ctab[8 * kb + ch], a.cm2, a.cc2);
+          if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)
+            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = o;
+        }
         fence_proxy_async();
         __syncwarp();
         TRG(tl, kb, 3);
@@ -1243,7 +1294,12 @@ cudaError_t prepare_fused3(const DevNet& net, const void* const* W_host, const v
     memcpy(blk.data() + L.ones + tc::none16_off((uint32_t)rr, 0), &one, 2);
     memcpy(blk.data() + L.ones + tc::none16_off((uint32_t)rr, 1), &one, 2);
   }
-  cudaError_t e = cudaMalloc(blk_dev, blk.size());
+  // the setmaxnreg budget assumes this register allocation (checked once per handle)
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, f3::k_fused3);
+  if (e != cudaSuccess) return e;
+  if (fa.numRegs != f3::kRegLaunch) return cudaErrorInvalidConfiguration;
+  e = cudaMalloc(blk_dev, blk.size());
   if (e != cudaSuccess) return e;
   return cudaMemcpy(*blk_dev, blk.data(), blk.size(), cudaMemcpyHostToDevice);
 }
@@ -1272,7 +1328,15 @@ cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases,
     if (cov.lower[p] == 2) a.pair23 = p;
   }
   a.eval_idx = eval_idx; a.eval_n = eval_n; a.eval_base = eval_base; a.eval_out = static_cast<float*>(eval_out);
-  a.stepS = (float)(pert.step_d * 16777216.0);         // step * 2^24 (the levels are l * 2^-24)
+  a.clamp = pert.kind == MLPV_PERT_PHILOX_CLAMP ? 1 : 0;
+  if (a.clamp) {
+    a.stepS = ldexpf(1.0f, -pert.clamp_s);             // the A operand is d * 2^s
+    a.cm2 = pert.clamp_m2;
+    a.cc2 = pert.clamp_c2;
+    a.clampc = ws.clampc;
+  } else {
+    a.stepS = (float)(pert.step_d * 16777216.0);       // step * 2^24 (the levels are l * 2^-24)
+  }
   a.base1 = ws.base1;
   if (eval_idx) {
     a.tiles_per_base = (uint64_t)((eval_n + 255) / 256);
@@ -1286,14 +1350,6 @@ cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases,
   if (nclusters > a.n_pairs_tiles) nclusters = a.n_pairs_tiles;
   cudaError_t e = cudaFuncSetAttribute(f3::k_fused3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::kSmemBytes);
   if (e != cudaSuccess) return e;
-  static int checked = 0;
-  if (!checked) {                                        // the setmaxnreg budget assumes this allocation
-    cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, f3::k_fused3);
-    if (e != cudaSuccess) return e;
-    if (fa.numRegs != f3::kRegLaunch) return cudaErrorInvalidConfiguration;
-    checked = 1;
-  }
   f3::k_fused3<<<(unsigned)(2 * nclusters), f3::kThreads, f3::kSmemBytes, st>>>(a);
   return cudaGetLastError();
 }

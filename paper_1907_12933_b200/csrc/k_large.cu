@@ -938,13 +938,15 @@ static bool use_fused3(const DevNet& net) {     // MLPV_NO_FUSED3=1: debugging o
 
 // Wt_dev[0]: generic tiles; Wt_dev[1]: k_fused3 weight block (when applicable)
 cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const void* const* b_host, void** Wt_dev,
-                          std::string* why) {
+                          size_t* scratch_per_cta, std::string* why) {
+  *scratch_per_cta = 0;
   if (fused3_applicable(net)) {
     cudaError_t e = prepare_fused3(net, W_host, b_host, &Wt_dev[1]);
     if (e != cudaSuccess) return e;
   }
   LargeGeom g;
   if (!geometry(net, &g, why)) return cudaSuccess;
+  *scratch_per_cta = g.scratch_per_cta;
   const bool fl = net.numeric == MLPV_NUM_BF16;
   std::vector<uint8_t> buf(g.w_total, 0);
   for (int l = 1; l <= net.L; l++) {
@@ -986,17 +988,14 @@ cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const vo
   return cudaSuccess;
 }
 
-static uint8_t* g_scratch = nullptr;               // per process; grown on demand (one device)
-static size_t g_scratch_size = 0;
-
-cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* bases, int n_base, const DevPert& pert,
-                         const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
+cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch, const void* bases, int n_base,
+                         const DevPert& pert, const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
                          cudaStream_t st, bool* supported, std::string* why) {
-  if (pert.kind == MLPV_PERT_PHILOX_BOX) {              // the exact box is built on the fused path only
+  if (pert.kind == MLPV_PERT_PHILOX_BOX || pert.kind == MLPV_PERT_PHILOX_CLAMP) {   // built on the fused path only
     if (!(use_fused3(net) && Wt[1])) {
       *supported = false;
-      *why = "PHILOX_BOX is built for 3-layer BF16 nets with 256-wide hidden layers (k_fused3)";
+      *why = "PHILOX_BOX / PHILOX_CLAMP are built for 3-layer BF16 nets with 256-wide hidden layers, n_0 even <= 1024 (k_fused3)";
       return cudaSuccess;
     }
     *supported = true;
@@ -1031,18 +1030,8 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* b
   if (a.n_tiles == 0) return cudaSuccess;
   const int grid = (int)(a.n_tiles < (uint64_t)num_sms ? a.n_tiles : (uint64_t)num_sms);
   a.scratch_per_cta = g.scratch_per_cta;
-  const size_t need = (size_t)grid * g.scratch_per_cta;
-  if (need > g_scratch_size) {
-    if (g_scratch) cudaFree(g_scratch);
-    g_scratch = nullptr;
-    g_scratch_size = 0;
-    cudaError_t e = cudaMalloc(&g_scratch, need);
-    if (e != cudaSuccess) return e;
-    e = cudaMemset(g_scratch, 0, need);           // K padding of the activations stays zero
-    if (e != cudaSuccess) return e;
-    g_scratch_size = need;
-  }
-  a.scratch = g_scratch;
+  if (!scratch) return cudaErrorInvalidValue;     // the handle's scratch: num_sms x scratch_per_cta, K padding zero
+  a.scratch = static_cast<uint8_t*>(scratch);
   a.soff[1] = 0;
   for (int l = 1; l <= net.L; l++) a.soff[l + 1] = a.soff[l] + ((net.sizes[l] + 3) & ~3);
   const size_t stage_bytes = (size_t)2 * a.soff[net.L + 1] * 4;

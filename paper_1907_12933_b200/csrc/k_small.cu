@@ -10,6 +10,7 @@
 //   a7 argmax (lowest index on ties), top-2 margin, property
 //   a8 sign / value / distance predicates and SS / SV / VS / VV pair bits
 //   a9 block-level reduction of counts, lowest-index counterexample and coverage words.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -136,7 +137,8 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
   // warp-shuffle sums
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (ws.base1 != nullptr) {                        // PHILOX_BOX: W1 x + b1 + origin W1 1 (fp64 sum)
-    const int n1 = net.sizes[1];
+    const int n1 = net.sizes[1];                    // PHILOX_CLAMP: W1 x + b1 (origin enters via d)
+    const double org = pert.kind == MLPV_PERT_PHILOX_BOX ? pert.origin_d : 0.0;
     for (int i = wid; i < n1; i += nw) {
       double acc = 0.0;
       if (net.numeric == MLPV_NUM_BF16 && (n0 & 7) == 0) {          // 8 bf16 weights per 16-byte load
@@ -146,18 +148,54 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
           const uint32_t ws[4] = {w8.x, w8.y, w8.z, w8.w};
 #pragma unroll
           for (int k = 0; k < 4; k++) {
-            acc += (double)__uint_as_float(ws[k] << 16) * ((double)hf[8 * qq + 2 * k] + pert.origin_d);
-            acc += (double)__uint_as_float(ws[k] & 0xFFFF0000u) * ((double)hf[8 * qq + 2 * k + 1] + pert.origin_d);
+            acc += (double)__uint_as_float(ws[k] << 16) * ((double)hf[8 * qq + 2 * k] + org);
+            acc += (double)__uint_as_float(ws[k] & 0xFFFF0000u) * ((double)hf[8 * qq + 2 * k + 1] + org);
           }
         }
       } else {
         for (int j = lane; j < n0; j += 32)
-          acc += (double)wload_f(net.W[0], net.numeric, (size_t)i * n0 + j) * ((double)hf[j] + pert.origin_d);
+          acc += (double)wload_f(net.W[0], net.numeric, (size_t)i * n0 + j) * ((double)hf[j] + org);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) ws.base1[(size_t)b * n1 + i] = (float)(acc + (double)static_cast<const float*>(net.b[0])[i]);
     }
+  }
+  if (ws.clampc != nullptr) {
+    // PHILOX_CLAMP clamp bounds of every pixel for k_fused3's generator: d = min(max(off, -x), 1 - x)
+    // in units of 2^-s, as fp16 (RN).  The contraction is exact iff each bound is exact where it
+    // can bind: -x 2^s when x <= -min(off) (x = 0, or x >= 2^(-17-s) for a bf16 x), 1 - x when
+    // 1 - x <= max(off).  A pixel outside [0, 1] or with an inexact binding bound is reported
+    // through the status word (mlpv_sync).
+    const int nch = (n0 + 7) / 8;
+    const float sc = exp2f((float)pert.clamp_s);
+    const double o15 = pert.origin_d + 15.0 * pert.step_d;
+    const double offlo = fmin(pert.origin_d, o15), offhi = fmax(pert.origin_d, o15);
+    uint32_t bad = 0;
+    for (int e = threadIdx.x; e < 4 * nch; e += blockDim.x) {
+      const int ch = e >> 2, k = e & 3;
+      uint32_t nx2 = 0, px2 = 0;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int p = 8 * ch + 2 * k + h;
+        uint16_t nx = 0, px = 0;
+        if (p < n0) {
+          const float xv = hf[p];
+          const __half hn = __float2half_rn(-xv * sc), hp = __float2half_rn((1.0f - xv) * sc);
+          nx = __half_as_ushort(hn);
+          px = __half_as_ushort(hp);
+          if (!(xv >= 0.0f && xv <= 1.0f)) bad = 1;
+          if ((double)xv <= -offlo && __half2float(hn) != -xv * sc) bad = 1;         // the lower bound binds
+          if (1.0 - (double)xv <= offhi && __half2float(hp) != (1.0f - xv) * sc) bad = 1;   // the upper one
+        }
+        nx2 |= (uint32_t)nx << (16 * h);
+        px2 |= (uint32_t)px << (16 * h);
+      }
+      uint32_t* dst = reinterpret_cast<uint32_t*>(ws.clampc + (size_t)b * 2 * nch + 2 * ch);
+      dst[k] = nx2;
+      dst[4 + k] = px2;
+    }
+    if (bad) atomicOr(ws.status, kStatusClampBase);
   }
   const int T = net.trace_len;
   for (int l = 1; l <= net.L; l++) {

@@ -2,6 +2,7 @@
 // copies of the net, per-call workspace, and the launch sequence of the check
 //   init results -> K0 base prologue -> (tau) -> enumeration kernel (k_small / k_large).
 // No torch types; plain pointers and sizes only.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -17,12 +18,12 @@ using namespace mlpv;
 
 namespace mlpv {
 // k_large.cu
-cudaError_t launch_large(const DevNet& net, const void* const* Wt, const void* bases, int n_base,
+cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch, const void* bases, int n_base,
                          const DevPert& pert, const DevProp& prop, const DevCov& cov, const DevResult& res,
                          BaseWS ws, const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
                          int num_sms, cudaStream_t st, bool* supported, std::string* why);
 cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const void* const* b_host, void** Wt_dev,
-                          std::string* why);
+                          size_t* scratch_per_cta, std::string* why);
 }  // namespace mlpv
 
 struct mlpv_ctx {
@@ -41,6 +42,8 @@ struct mlpv_ctx {
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;   // mlpv_profile
   uint64_t launches = 0;
   void* steps_dev = nullptr;          // incremental bounds: [kMaxSteps] r2 values (NEXT-2)
+  void* scratch = nullptr;            // k_large activation scratch: [num_sms][scratch_per_cta], zeroed once
+  uint32_t* dev_status = nullptr;     // device status word (input errors found on the device; mlpv_sync)
 };
 
 static thread_local std::string g_err;
@@ -79,6 +82,17 @@ static double bf16_to_double(uint16_t b) {
   float f;
   memcpy(&f, &u, 4);
   return f;
+}
+static bool f16_exact(double v, uint16_t* bits) {     // v is an fp16 value (RN round trip)
+  const float f = (float)v;
+  if ((double)f != v) return false;
+  const __half hh = __float2half_rn(f);
+  if ((double)__half2float(hh) != v) return false;
+  memcpy(bits, &hh, 2);
+  return true;
+}
+static bool is_philox(int kind) {
+  return kind == MLPV_PERT_PHILOX_LATTICE || kind == MLPV_PERT_PHILOX_BOX || kind == MLPV_PERT_PHILOX_CLAMP;
 }
 static bool is_bf16_value(double v) {
   float f = (float)v;
@@ -193,10 +207,28 @@ extern "C" mlpv_status mlpv_create(const mlpv_net* net, const mlpv_quant* quant,
     h->acc_scale[l] = quant->acc_scale ? quant->acc_scale[l] : (num == MLPV_NUM_Q4_12 ? 1.0 / 16777216.0 : 1.0);
   // tensor-core layouts for the large-net path (PHILOX spaces, BF16 / INT8)
   if (num == MLPV_NUM_BF16 || num == MLPV_NUM_INT8) {
-    cudaError_t pe = prepare_large(d, net->W, net->b, h->Wt, &h->large_why);
+    size_t per_cta = 0;
+    cudaError_t pe = prepare_large(d, net->W, net->b, h->Wt, &per_cta, &h->large_why);
     if (pe != cudaSuccess) { mlpv_destroy(h); return fail(nullptr, MLPV_E_CUDA, "prepare_large: %s", cudaGetErrorString(pe)); }
     h->large_ready = h->large_why.empty();
     for (int l = 0; l < L; l++) if (h->Wt[l]) h->allocs.push_back(h->Wt[l]);
+    if (h->large_ready && per_cta > 0) {
+      // the handle's own activation scratch (K padding zeroed once; the kernels never write it)
+      const size_t bytes = per_cta * (size_t)h->num_sms;
+      if (cudaMalloc(&h->scratch, bytes) != cudaSuccess) { h->scratch = nullptr; mlpv_destroy(h); return fail(nullptr, MLPV_E_OOM, "k_large scratch of %zu bytes", bytes); }
+      h->allocs.push_back(h->scratch);
+      if (cudaMemset(h->scratch, 0, bytes) != cudaSuccess) { mlpv_destroy(h); return fail(nullptr, MLPV_E_CUDA, "scratch memset"); }
+    }
+  }
+  {
+    void* p = nullptr;
+    if (cudaMalloc(&p, 8 * kMaxSteps) != cudaSuccess) { mlpv_destroy(h); return fail(nullptr, MLPV_E_OOM, "steps buffer"); }
+    h->allocs.push_back(p);
+    h->steps_dev = p;
+    if (cudaMalloc(&p, 256) != cudaSuccess) { mlpv_destroy(h); return fail(nullptr, MLPV_E_OOM, "status word"); }
+    h->allocs.push_back(p);
+    h->dev_status = static_cast<uint32_t*>(p);
+    if (cudaMemset(p, 0, 256) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) { mlpv_destroy(h); return fail(nullptr, MLPV_E_CUDA, "status memset"); }
   }
   *out = h;
   return MLPV_OK;
@@ -207,7 +239,7 @@ extern "C" void mlpv_destroy(mlpv_t h) {
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   for (void* p : h->allocs) cudaFree(p);
-  if (h->ws) cudaFree(h->ws);
+  if (h->ws) cudaFree(h->ws);                     // stream-ordered allocation; the device is idle
   delete h;
 }
 
@@ -328,13 +360,43 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
       dp->origin_d = p->lattice_origin;
       dp->seed = p->seed;
       break;
+    case MLPV_PERT_PHILOX_CLAMP: {
+      if (num != MLPV_NUM_BF16) return fail(h, MLPV_E_UNSUPPORTED, "PHILOX_CLAMP is built for BF16 nets");
+      if (p->n_samples < 1 || p->n_samples > (1ull << 32)) return fail(h, MLPV_E_INVALID, "pert.n_samples = %llu (1..2^32)", (unsigned long long)p->n_samples);
+      if (!std::isfinite(p->lattice_step) || !std::isfinite(p->lattice_origin) || std::fabs(p->lattice_step) > 1.0 ||
+          std::fabs(p->lattice_origin) > 1.0 || std::fabs(p->lattice_origin + 15.0 * p->lattice_step) > 1.0)
+        return fail(h, MLPV_E_INVALID, "pert.lattice_step / lattice_origin must be finite with |origin|, |origin + 15 step| <= 1");
+      // the scale s of the fp16 contraction (reading C19): the largest s with
+      // step 2^(24+s) <= 65504 and step 2^(24+s), origin 2^s and every offset (origin + l step) 2^s
+      // exact in fp16
+      bool found = false;
+      for (int sc = 24; sc >= -40 && !found; sc--) {
+        uint16_t mb, cb, ob;
+        const double m = std::ldexp(p->lattice_step, 24 + sc);
+        if (std::fabs(m) > 65504.0 || !f16_exact(m, &mb) || !f16_exact(std::ldexp(p->lattice_origin, sc), &cb)) continue;
+        bool ok = true;
+        for (int l = 0; l < 16 && ok; l++) ok = f16_exact(std::ldexp(p->lattice_origin + l * p->lattice_step, sc), &ob);
+        if (!ok) continue;
+        dp->clamp_s = sc;
+        dp->clamp_m2 = (uint32_t)mb | ((uint32_t)mb << 16);
+        dp->clamp_c2 = (uint32_t)cb | ((uint32_t)cb << 16);
+        found = true;
+      }
+      if (!found) return fail(h, MLPV_E_UNSUPPORTED, "PHILOX_CLAMP: the offsets origin + l * step are not exactly representable in fp16 at any scale 2^s");
+      dp->step_f = (float)p->lattice_step;
+      dp->origin_f = (float)p->lattice_origin;
+      dp->step_d = p->lattice_step;
+      dp->origin_d = p->lattice_origin;
+      dp->seed = p->seed;
+      break;
+    }
     default:
       return fail(h, MLPV_E_INVALID, "pert.kind = %d", (int)p->kind);
   }
   if (!std::isfinite(p->restrict_l2) || p->restrict_l2 < 0)
     return fail(h, MLPV_E_INVALID, "pert.restrict_l2 = %g (finite, >= 0)", p->restrict_l2);
   if (p->restrict_l2 > 0) {
-    if (p->kind == MLPV_PERT_PHILOX_LATTICE || p->kind == MLPV_PERT_PHILOX_BOX)
+    if (is_philox(p->kind))
       return fail(h, MLPV_E_UNSUPPORTED, "pert.restrict_l2 is built for the subset and tuple spaces");
     dp->restrict_on = 1;
     const double b = p->restrict_l2;
@@ -345,7 +407,7 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
       dp->r2_f = b * b;
     }
   }
-  if (p->kind != MLPV_PERT_PHILOX_LATTICE && p->kind != MLPV_PERT_PHILOX_BOX) {
+  if (!is_philox(p->kind)) {
     if (p->n_levels < 1 || p->n_levels > 256) return fail(h, MLPV_E_INVALID, "pert.n_levels = %d (1..256)", p->n_levels);
     if (!p->levels) return fail(h, MLPV_E_INVALID, "pert.levels is NULL");
     for (int q = 0; q < p->n_levels; q++) {
@@ -366,7 +428,7 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
   dp->n_pixels = p->n_pixels;
   dp->q2 = (uint64_t)dp->n_levels * dp->n_levels;
   const uint64_t space = space_of(n, p);
-  if (space == ~0ull && p->kind != MLPV_PERT_PHILOX_LATTICE) return fail(h, MLPV_E_INVALID, "perturbation space exceeds 2^64");
+  if (space == ~0ull && !is_philox(p->kind)) return fail(h, MLPV_E_INVALID, "perturbation space exceeds 2^64");
   if (check_range) {
     if (p->index_begin > p->index_end || p->index_end > space)
       return fail(h, MLPV_E_INVALID, "pert index range [%llu, %llu) not within [0, %llu)", (unsigned long long)p->index_begin,
@@ -396,12 +458,19 @@ static mlpv_status build_prop(mlpv_ctx* h, const mlpv_property* pr, DevProp* d) 
   return MLPV_OK;
 }
 
-// device workspace: [trace n_base*T*4][cls n_base*4][tau 8*4][delta][pixels][levels]
-static mlpv_status ensure_ws(mlpv_ctx* h, size_t bytes) {
+// device workspace: [trace n_base*T*4][cls n_base*4][tau 8*4][delta][pixels][levels][base1][clampc].
+// Grown with stream-ordered allocation on the caller's stream (no device synchronisation); the
+// work of one handle is ordered on one stream at a time (mlpv.h conventions).
+static mlpv_status ensure_ws(mlpv_ctx* h, size_t bytes, cudaStream_t st) {
   if (h->ws_size >= bytes) return MLPV_OK;
-  if (h->ws) { cudaFree(h->ws); h->ws = nullptr; h->ws_size = 0; }
+  if (h->ws) {
+    cudaError_t e = cudaFreeAsync(h->ws, st);
+    h->ws = nullptr;
+    h->ws_size = 0;
+    if (e != cudaSuccess) return cuda_fail(h, e, "workspace free");
+  }
   size_t want = bytes + bytes / 4 + 4096;
-  cudaError_t e = cudaMalloc(&h->ws, want);
+  cudaError_t e = cudaMallocAsync(&h->ws, want, st);
   if (e != cudaSuccess) { h->ws = nullptr; return fail(h, MLPV_E_OOM, "workspace of %zu bytes: %s", want, cudaGetErrorString(e)); }
   h->ws_size = want;
   return MLPV_OK;
@@ -418,16 +487,18 @@ static mlpv_status prepare(mlpv_ctx* h, const void* bases, int n_base, const mlp
                            DevCov* dc, Plan* plan, cudaStream_t st, bool need_tau) {
   const DevNet& n = h->net;
   const int T = n.trace_len;
-  const bool subset = pert->kind != MLPV_PERT_PHILOX_LATTICE && pert->kind != MLPV_PERT_PHILOX_BOX;
-  const bool box = pert->kind == MLPV_PERT_PHILOX_BOX;
+  const bool subset = !is_philox(pert->kind);
+  const bool clamp = pert->kind == MLPV_PERT_PHILOX_CLAMP;
+  const bool box = pert->kind == MLPV_PERT_PHILOX_BOX || clamp;   // base1 = W1 x + b1 (+ origin W1 1)
   const int S = pert->kind == MLPV_PERT_TUPLE_REPLACE ? n.sizes[0] : pert->n_pixels;
   const size_t delta_bytes = subset ? 4ull * n_base * S * dp.n_levels * n.sizes[1] : 0;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t o_trace = 0, o_cls = al(4ull * n_base * T), o_tau = o_cls + al(4ull * n_base);
   const size_t o_delta = o_tau + al(4 * kMaxL), o_pix = o_delta + al(delta_bytes);
   const size_t o_lv = o_pix + al(4 * 64), o_b1 = o_lv + al(4 * 256);
-  const size_t total = o_b1 + (box ? al(4ull * n_base * n.sizes[1]) : 0);
-  mlpv_status s = ensure_ws(h, total);
+  const size_t o_cc = o_b1 + (box ? al(4ull * n_base * n.sizes[1]) : 0);
+  const size_t total = o_cc + (clamp ? al(32ull * n_base * ((n.sizes[0] + 7) / 8)) : 0);
+  mlpv_status s = ensure_ws(h, total, st);
   if (s != MLPV_OK) return s;
   char* w = static_cast<char*>(h->ws);
   plan->ws.trace = w + o_trace;
@@ -435,6 +506,8 @@ static mlpv_status prepare(mlpv_ctx* h, const void* bases, int n_base, const mlp
   plan->ws.delta = subset ? w + o_delta : nullptr;
   plan->ws.S = S;
   plan->ws.base1 = box ? reinterpret_cast<float*>(w + o_b1) : nullptr;
+  plan->ws.clampc = clamp ? reinterpret_cast<uint4*>(w + o_cc) : nullptr;
+  plan->ws.status = h->dev_status;
   plan->tau_dev = reinterpret_cast<float*>(w + o_tau);
   plan->pixels_dev = reinterpret_cast<int32_t*>(w + o_pix);
   plan->levels_dev = w + o_lv;
@@ -467,11 +540,11 @@ static mlpv_status run_kernel(mlpv_ctx* h, const void* bases, int n_base, const 
   bool supported = false;
   cudaError_t e;
   if (h->ev_begin) CUDA_TRY(h, cudaEventRecord(h->ev_begin, st), "profile event");
-  if (pert->kind == MLPV_PERT_PHILOX_LATTICE || pert->kind == MLPV_PERT_PHILOX_BOX) {
+  if (is_philox(pert->kind)) {
     if (!h->large_ready) return fail(h, MLPV_E_UNSUPPORTED, "large-net path unavailable for this net: %s", h->large_why.c_str());
     std::string why;
-    e = launch_large(h->net, h->Wt, bases, n_base, dp, dprop, dc, dr, plan.ws, eval_idx, eval_n, eval_base, eval_out,
-                     h->num_sms, st, &supported, &why);
+    e = launch_large(h->net, h->Wt, h->scratch, bases, n_base, dp, dprop, dc, dr, plan.ws, eval_idx, eval_n, eval_base,
+                     eval_out, h->num_sms, st, &supported, &why);
     if (!supported) return fail(h, MLPV_E_UNSUPPORTED, "large-net kernel: %s", why.c_str());
   } else {
     dp.levels = plan.levels_dev;
@@ -572,17 +645,13 @@ static mlpv_status check_impl(mlpv_t h, const void* base_inputs, int32_t n_base,
     if (inc->max_bound < 1 || inc->granularity < 1) return fail(h, MLPV_E_INVALID, "inc.max_bound / granularity must be >= 1");
     const int n_steps = mlpv_incremental_steps(inc);
     if (n_steps > kMaxSteps) return fail(h, MLPV_E_INVALID, "inc: %d steps (max %d)", n_steps, kMaxSteps);
-    if (pert->kind == MLPV_PERT_PHILOX_LATTICE || pert->kind == MLPV_PERT_PHILOX_BOX)
+    if (is_philox(pert->kind))
       return fail(h, MLPV_E_UNSUPPORTED, "incremental bounds are built for the subset and tuple spaces");
     if (pert->index_end > (1ull << kStepShift)) return fail(h, MLPV_E_UNSUPPORTED, "incremental bounds need index_end <= 2^48");
     pinc = *pert;
     pinc.restrict_l2 = inc->gamma;               // the kernel enumerates the whole gamma ball once
     pert = &pinc;
     if ((s = build_pert(h, pert, &dp, true)) != MLPV_OK) return s;
-    if (!h->steps_dev) {
-      CUDA_TRY(h, cudaMalloc(&h->steps_dev, 8 * kMaxSteps), "steps buffer");
-      h->allocs.push_back(h->steps_dev);
-    }
     std::vector<double> r2f(n_steps);
     std::vector<long long> r2i(n_steps);
     const bool fx = is_fixed(h->net.numeric);
@@ -709,7 +778,7 @@ extern "C" mlpv_status mlpv_decode(mlpv_numeric numeric, const mlpv_pert* p, con
     return MLPV_OK;
   }
   const uint32_t k0 = (uint32_t)p->seed, k1 = (uint32_t)(p->seed >> 32);
-  if (p->kind == MLPV_PERT_PHILOX_BOX) {        // exact real candidate, written as doubles
+  if (p->kind == MLPV_PERT_PHILOX_BOX || p->kind == MLPV_PERT_PHILOX_CLAMP) {   // exact real candidate (doubles)
     double* o = static_cast<double*>(out);
     for (int j = 0; j < n0; j++) o[j] = get(base, j);
     for (int j = 0; j < (n0 + 31) / 32; j++) {
@@ -718,7 +787,10 @@ extern "C" mlpv_status mlpv_decode(mlpv_numeric numeric, const mlpv_pert* p, con
       for (int ww = 0; ww < 4; ww++)
         for (int nb = 0; nb < 8; nb++) {
           const int px = 32 * j + 8 * ww + nb;
-          if (px < n0) o[px] += p->lattice_origin + (double)((w[ww] >> (4 * nb)) & 15) * p->lattice_step;
+          if (px >= n0) continue;
+          double v = o[px] + (p->lattice_origin + (double)((w[ww] >> (4 * nb)) & 15) * p->lattice_step);
+          if (p->kind == MLPV_PERT_PHILOX_CLAMP) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+          o[px] = v;
         }
     }
     return MLPV_OK;
@@ -761,6 +833,23 @@ extern "C" mlpv_status mlpv_decode(mlpv_numeric numeric, const mlpv_pert* p, con
   return MLPV_OK;
 }
 
+extern "C" mlpv_status mlpv_sync(mlpv_t h, void* stream) {
+  if (!h) return fail(nullptr, MLPV_E_INVALID, "handle is NULL");
+  if (h->sticky != MLPV_OK) return fail(h, h->sticky, "handle has a sticky CUDA error: %s", h->err.c_str());
+  CUDA_TRY(h, cudaSetDevice(h->device), "cudaSetDevice");
+  CUDA_TRY(h, cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "asynchronous kernel fault");
+  uint32_t st = 0;
+  CUDA_TRY(h, cudaMemcpy(&st, h->dev_status, 4, cudaMemcpyDeviceToHost), "status read");
+  if (st != 0) {
+    CUDA_TRY(h, cudaMemset(h->dev_status, 0, 4), "status reset");
+    if (st & kStatusClampBase)
+      return fail(h, MLPV_E_INVALID, "PHILOX_CLAMP: a base pixel is outside [0, 1] or its binding clamp bound is not "
+                                     "exactly representable at the contraction scale (mlpv.h); those results are not exact");
+    return fail(h, MLPV_E_INVALID, "device status 0x%x", st);
+  }
+  return MLPV_OK;
+}
+
 extern "C" mlpv_status mlpv_merge(const mlpv_result* parts, int32_t n_parts, int32_t n_base, size_t n_words,
                                   const mlpv_result* out, void* stream) {
   if (!parts || !out || n_parts < 1 || n_parts > kMaxParts || n_base < 1)
@@ -790,7 +879,7 @@ extern "C" mlpv_status mlpv_pair_coverage(mlpv_t h, const void* images, int32_t 
   const DevNet& n = h->net;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t o_cls = al(4ull * n_images * n.trace_len), o_tau = o_cls + al(4ull * n_images);
-  if ((s = ensure_ws(h, o_tau + al(4 * kMaxL))) != MLPV_OK) return s;
+  if ((s = ensure_ws(h, o_tau + al(4 * kMaxL), st)) != MLPV_OK) return s;
   char* w = static_cast<char*>(h->ws);
   BaseWS ws{};
   ws.trace = w;

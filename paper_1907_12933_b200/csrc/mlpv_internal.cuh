@@ -49,7 +49,11 @@ struct DevPert {
   uint64_t begin, end;        // index range
   uint64_t seed;
   float step_f, origin_f;     // PHILOX (BF16 values) / PHILOX_BOX (fp32 of the doubles)
-  double step_d, origin_d;    // PHILOX_BOX
+  double step_d, origin_d;    // PHILOX_BOX / PHILOX_CLAMP
+  // PHILOX_CLAMP on k_fused3: A = d * 2^clamp_s in fp16, d = min(max(origin + l step, -x), 1 - x);
+  // the offsets come from the fp16-subnormal levels l * 2^-24 as fma(l 2^-24, clamp_m, clamp_c)
+  int clamp_s;                // scale exponent s
+  uint32_t clamp_m2, clamp_c2;   // fp16x2 {step 2^(24+s), step 2^(24+s)} / {origin 2^s, origin 2^s}
   int step_i, origin_i;       // PHILOX (INT8)
   uint64_t q2;                // TUPLE: q^2
   // restriction R (reading C27): keep delta(I^d, I) <= b; subset / tuple spaces (k_small)
@@ -77,8 +81,14 @@ struct BaseWS {
   int32_t* cls;               // [n_base] base class
   void* delta;                // [n_base x S x q x n_1] layer-1 delta tables (subset/tuple spaces)
   int S;                      // slots per base: n_0 (TUPLE) or K (SUBSET)
-  float* base1;               // PHILOX_BOX: [n_base x n_1] W1 x + b1 + origin W1 1 (fp64 sum, fp32)
+  float* base1;               // PHILOX_BOX: [n_base x n_1] W1 x + b1 + origin W1 1 (fp64 sum, fp32);
+                              // PHILOX_CLAMP: W1 x + b1
+  uint4* clampc;              // PHILOX_CLAMP: [n_base][ceil(n_0 / 8)][2] fp16x2 words {-x 2^s} | {(1-x) 2^s}
+                              // of 8 pixels (pairs in pixel order; 0 beyond n_0)
+  uint32_t* status;           // handle's device status word (input errors found on the device)
 };
+// bits of the device status word (mlpv_sync reports them)
+constexpr uint32_t kStatusClampBase = 1u;      // a PHILOX_CLAMP base pixel outside [0, 1] or not fp16-exact
 
 // Launchers (kernels in k_small.cu / k_large.cu / k_util.cu)
 cudaError_t launch_base_prologue(const DevNet& net, const void* bases, int n_base, const DevPert& pert,

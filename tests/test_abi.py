@@ -68,7 +68,7 @@ def test_create_validation_is_synchronous(P):
     assert s == 1 and "finite" in msg
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5_int8"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg4_box", "cfg5_int8"])
 def test_host_decoder_matches_oracle(P, name, oracle_mod):
     cfg = M.make_config(name)
     rng = np.random.default_rng(1)
