@@ -288,13 +288,16 @@ def _cfg4_box() -> Config:
 def _cfg5(variant: str) -> Config:
     sizes = [3072, 1024, 512, 10]
     W, b = _master_net(5, sizes, 2.0)
-    x = _rng(5, 1).random((256, 3072), dtype=np.float32)
+    # 8-bit images (CIFAR's pixels are u8): the bf16 variant holds u8 / 255 as bf16, the int8 one u8
+    x = np.rint(_rng(5, 1).random((256, 3072), dtype=np.float32).astype(np.float64) * 255.0) / 255.0
     seed = int(_rng(5, 3).integers(2 ** 64, dtype=np.uint64))
     if variant == "bf16":
         net = Net(sizes, ACT_RELU, NUM_BF16, [f32_to_bf16_bits(w) for w in W], b, acc_scale=[1.0] * 3)
-        bases = f32_to_bf16_bits(x)
+        bases = eight_bit_bf16(x)
+        # offsets (l - 8) step, step = bf16(1/255) = 129 * 2^-15, clamped to [0, 1] (reading C14);
+        # the int8 variant takes the same draws as u8 offsets l - 8
         step = _bf16_scalar(1.0 / 255.0)
-        pert = Pert(PERT_PHILOX_LATTICE, seed=seed, n_samples=2 ** 30,
+        pert = Pert(PERT_PHILOX_CLAMP, seed=seed, n_samples=2 ** 30,
                     lattice_step=step, lattice_origin=-8.0 * step)
         name = "cfg5_bf16"
     else:

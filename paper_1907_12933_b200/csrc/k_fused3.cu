@@ -35,7 +35,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
+#include <type_traits>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -71,6 +73,10 @@ __device__ unsigned long long g_trace_e2[2][8][2][8];
 __device__ unsigned long long g_trace_grp[8][8][5];
 #define TRP(tl, i, ev) do { if (cluster == 0 && rank == 0 && lane == 0 && (tl) == 9) \
     g_trace_grp[warp - kWE][(i)][(ev)] = clock64(); } while (0)
+// E1 per piece, tile 9, cluster 0: [rank][epilogue warp][piece step][0 top, 1 ld done, 2 computed, 3 signed off]
+__device__ unsigned long long g_trace_e1p[2][8][5][4];
+#define TR1(tl, i, ev) do { if (cluster == 0 && lane == 0 && (tl) == 9) \
+    g_trace_e1p[rank][warp - kWE][(i)][(ev)] = clock64(); } while (0)
 // completion time of every layer-1 stage of tiles 8..11 (observed by the idle warp 3)
 __device__ unsigned long long g_trace_done[4][13];
 #define TRI(tl, kb, ev) do { if (cluster == 0 && (tl) >= 8 && (tl) < 12) g_trace_iss[(tl) - 8][(kb)][(ev)] = clock64(); } while (0)
@@ -85,6 +91,7 @@ __device__ unsigned long long g_trace_gen[2][2][4][13][5];
 #define TRE(team, tl, ev) do { } while (0)
 #define TRE2(tl, i, ev) do { } while (0)
 #define TRP(tl, i, ev) do { } while (0)
+#define TR1(tl, i, ev) do { } while (0)
 #endif
 
 constexpr int kThreads = 768;
@@ -152,6 +159,8 @@ struct Args {
   int clamp;                                 // PHILOX_CLAMP: A = d 2^s = min(max(fma(l 2^-24, m, c), -x 2^s), (1-x) 2^s)
   uint32_t cm2, cc2;                         // fp16x2 m = step 2^(24+s), c = origin 2^s
   const uint4* clampc;                       // [n_base][ceil(n0/8)][2] {-x 2^s} | {(1-x) 2^s} fp16x2 words
+  uint32_t rk[20];                           // Philox round keys of pert.seed
+  float offlo, offhi;                        // PHILOX_CLAMP: smallest / largest offset * 2^s
 };
 
 struct alignas(16) Smem {
@@ -179,6 +188,7 @@ struct alignas(16) Smem {
   uint16_t vc2[16][128];                     // E2 slow path: value-change bits of layer 2 (16 neurons)
   alignas(16) float c1row[8][128];           // E2: the layer-2 potentials of a warp's single cond1 row
   alignas(16) uint4 ctab[kMaxN0 / 8][2];     // generators, PHILOX_CLAMP: the staged base's clamp bounds
+  uint8_t stype[kMaxN0 / 64];                // ... and each stage's clamp type (kGen*)
 };
 
 constexpr size_t kTilesBytes = (size_t)(kSG + kSW) * kTile + (size_t)kChunks * kW3Chunk + 4 * kBiasTile;
@@ -214,14 +224,16 @@ __device__ __forceinline__ void cluster_range(uint64_t n, uint64_t c, uint64_t n
   t1 = t0 + q + (c < r ? 1 : 0);
 }
 
-__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+// Philox4x32-10 (reading C15) with the round keys of the launch's seed precomputed on the host
+// (rk[2r], rk[2r+1] = key + r * Weyl): they stay in the parameter bank, so a round is two IMAD.WIDE
+// and two LOP3 with a constant operand (no per-call key schedule).
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const uint32_t (&rk)[20]) {
 #pragma unroll
   for (int r = 0; r < 10; r++) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
     const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r], n2 = hi0 ^ c3 ^ rk[2 * r + 1];
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
   }
   return make_uint4(c0, c1, c2, c3);
 }
@@ -247,19 +259,38 @@ __device__ __forceinline__ uint4 nibble_word(uint32_t w) {
 // step is exact (the host picked s so that each offset is an fp16 value; the bounds are exact where
 // they bind, checked by the base prologue), so the layer-1 MMA contracts W1 (x' - x) exactly up to
 // its fp32 accumulation of small terms.
-__device__ __forceinline__ uint32_t clamp_pair(uint32_t lv, uint32_t m2, uint32_t c2, uint32_t nx, uint32_t px) {
-  // (intrinsics rather than asm so that ptxas can take m2 / c2 straight from the parameter bank)
-  const __half2 o = __hfma2(*reinterpret_cast<const __half2*>(&lv), *reinterpret_cast<const __half2*>(&m2),
-                            *reinterpret_cast<const __half2*>(&c2));
-  const __half2 d = __hmin2(__hmax2(o, *reinterpret_cast<const __half2*>(&nx)), *reinterpret_cast<const __half2*>(&px));
-  return *reinterpret_cast<const uint32_t*>(&d);
-}
 
+// Stage clamp types (per base and 64-pixel stage, found when the base's bounds are staged): which
+// bounds can bind anywhere in the stage.  kGenRelu: every pixel is 0, d = max(off, 0) = ReLU(off)
+// (the FMA's .relu); kGenLower: only lower bounds bind, d = max(off, -x); kGenInterior: none, d = off;
+// kGenGeneral: d = min(max(off, -x), 1 - x); kGenBox: PHILOX_BOX, A = the levels themselves.
+constexpr int kGenRelu = 0, kGenLower = 1, kGenInterior = 2, kGenGeneral = 3, kGenBox = 4;
+template <int TY>
+__device__ __forceinline__ uint32_t gen_pair(uint32_t lv, uint32_t m2, uint32_t c2, uint32_t nx, uint32_t px) {
+  if constexpr (TY == kGenBox) {
+    return lv;
+  } else if constexpr (TY == kGenRelu) {
+    uint32_t d;
+    asm("fma.rn.relu.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(lv), "r"(m2), "r"(c2));
+    return d;
+  } else {
+    const __half2 o = __hfma2(*reinterpret_cast<const __half2*>(&lv), *reinterpret_cast<const __half2*>(&m2),
+                              *reinterpret_cast<const __half2*>(&c2));
+    if constexpr (TY == kGenInterior) return *reinterpret_cast<const uint32_t*>(&o);
+    __half2 d = __hmax2(o, *reinterpret_cast<const __half2*>(&nx));
+    if constexpr (TY == kGenGeneral) d = __hmin2(d, *reinterpret_cast<const __half2*>(&px));
+    return *reinterpret_cast<const uint32_t*>(&d);
+  }
+}
 // four pixel pairs (one 16-byte chunk of the A row) with the chunk's staged bounds {nx | px}
-__device__ __forceinline__ uint4 clamp_chunk(uint4 o, const uint4 (&b)[2], uint32_t m2, uint32_t c2) {
-  const uint4 nx = b[0], px = b[1];
-  return make_uint4(clamp_pair(o.x, m2, c2, nx.x, px.x), clamp_pair(o.y, m2, c2, nx.y, px.y),
-                    clamp_pair(o.z, m2, c2, nx.z, px.z), clamp_pair(o.w, m2, c2, nx.w, px.w));
+template <int TY>
+__device__ __forceinline__ uint4 gen_chunk(uint4 o, const uint4 (&b)[2], uint32_t m2, uint32_t c2) {
+  if constexpr (TY == kGenBox) return o;
+  uint4 nx = make_uint4(0, 0, 0, 0), px = nx;
+  if constexpr (TY == kGenLower || TY == kGenGeneral) nx = b[0];
+  if constexpr (TY == kGenGeneral) px = b[1];
+  return make_uint4(gen_pair<TY>(o.x, m2, c2, nx.x, px.x), gen_pair<TY>(o.y, m2, c2, nx.y, px.y),
+                    gen_pair<TY>(o.z, m2, c2, nx.z, px.z), gen_pair<TY>(o.w, m2, c2, nx.w, px.w));
 }
 
 // h = max(u, 0) = hi + lo + O(2^-22 h): hi = RZ_f16(h), lo = RN_f16(h - hi) (relu'd), with the
@@ -557,8 +588,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           if (__any_sync(0xffffffffu, l3go)) l3_kb++;
           pend_g = cg; pend_w = cw;
           if (full && __any_sync(0xffffffffu, notready)) {
+            // wait for the next stage; meanwhile issue whatever layer-3 block E2 has handed over
+            // (the pipe would otherwise hold L3 -- and so E3, and the next E1 -- behind a
+            // generator-bound layer 1)
             TRI(tl, kb, 1);
-            mbar_wait2(&S.g_full[gslot], gph, &S.w_full[wslot], wph);
+            bool d1 = false, d2 = false;
+            while (true) {
+              if (!d1) d1 = mbar_try_ns(&S.g_full[gslot], gph, 200u);
+              if (!d2) d2 = mbar_test(&S.w_full[wslot], wph);
+              if (__all_sync(0xffffffffu, d1 && d2)) break;
+              if (l3_kb < kNkb2 && __all_sync(0xffffffffu, mbar_test(&S.h2_kb[l3_kb & 3], l3_tl & 1u))) {
+                fence_after();
+                if (el) issue_l3();
+                l3_kb++;
+              }
+            }
             TRI(tl, kb, 3);
           }
         }
@@ -629,7 +673,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const int r = 32 * (gw & 3) + lane;                    // row of this CTA's A tile
     const int gt = 32 * gw + lane;                         // 0..383
     uint32_t tl = 0;
-    const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
     const int nblk = (a.n0 + 31) / 32;                     // Philox blocks holding pixels
     const int kneed = 16 * a.nk16;                         // K elements the MMA reads
     const bool clampk = a.clamp != 0;
@@ -646,6 +689,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         for (int i = gt; i < 2 * (kMaxN0 / 8); i += 32 * kNGenGroups * 4)
           (&S.ctab[0][0])[i] = (i >> 1) < nch ? src[i] : make_uint4(0, 0, 0, 0);   // beyond n_0: d = 0
         named_bar(13, 32 * kNGenGroups * 4);
+        if (gt < kMaxN0 / 64) {
+          // the stage's type from its 64 pixels' bounds (padding pixels, nx = px = +0, constrain nothing)
+          bool lower = false, upper = false, zero = true;
+          for (int ch = 0; ch < 8; ch++)
+            for (int w = 0; w < 4; w++) {
+              const uint32_t nx2 = (&S.ctab[8 * gt + ch][0].x)[w], px2 = (&S.ctab[8 * gt + ch][1].x)[w];
+              for (int hh = 0; hh < 2; hh++) {
+                const uint16_t nb = (uint16_t)(nx2 >> (16 * hh)), pb = (uint16_t)(px2 >> (16 * hh));
+                if (nb == 0 && pb == 0) continue;
+                const float nx = __half2float(__ushort_as_half(nb)), px = __half2float(__ushort_as_half(pb));
+                if (nx > a.offlo) lower = true;
+                if (px < a.offhi) upper = true;
+                if (nb != 0x8000u) zero = false;
+              }
+            }
+          S.stype[gt] = (uint8_t)(upper ? kGenGeneral : (lower ? (zero ? kGenRelu : kGenLower) : kGenInterior));
+        }
+        named_bar(13, 32 * kNGenGroups * 4);
         gbase = ti.b;
       }
       const int grow = 128 * (int)rank + r;
@@ -656,47 +717,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const uint32_t gs0 = tl * (uint32_t)a.nkb1;          // global index of this tile's first stage
       for (int kb = (int)((grp + kNGenGroups - gs0 % kNGenGroups) % kNGenGroups); kb < a.nkb1; kb += kNGenGroups) {
         const uint32_t gs = gs0 + kb;
-        TRG(tl, kb, 0);
-        // A operand of the 64-pixel K block: the first 32 pixels (Philox block 2 kb) are finished
-        // before the slot wait, the second block's words stay raw (4 registers) until after it
-        // (the clamped form would not fit the generator's 72 registers with all 8 chunks live)
-        uint4 out[4];
-        uint4 w1;
-        {
-          const int j = 2 * kb;
-          const uint4 z = make_uint4(0, 0, 0, 0);
-          const uint4 w0 = j < nblk ? philox(c0, c1, cb, (uint32_t)j, k0, k1) : z;
-          w1 = j + 1 < nblk ? philox(c0, c1, cb, (uint32_t)(j + 1), k0, k1) : z;
-          out[0] = nibble_word(w0.x); out[1] = nibble_word(w0.y);
-          out[2] = nibble_word(w0.z); out[3] = nibble_word(w0.w);
-          if (clampk) {
+        // one stage, specialised on its clamp type (uniform per stage; see gen_chunk)
+        auto stage = [&](auto tyc) {
+          constexpr int TY = decltype(tyc)::value;
+          TRG(tl, kb, 0);
+          // A operand of the 64-pixel K block: the first 32 pixels (Philox block 2 kb) are finished
+          // before the slot wait, the second block's words stay raw (4 registers) until after it
+          // (the clamped form would not fit the generator's 72 registers with all 8 chunks live)
+          uint4 out[4];
+          uint4 w1;
+          {
+            const int j = 2 * kb;
+            const uint4 z = make_uint4(0, 0, 0, 0);
+            const uint4 w0 = j < nblk ? philox(c0, c1, cb, (uint32_t)j, a.rk) : z;
+            w1 = j + 1 < nblk ? philox(c0, c1, cb, (uint32_t)(j + 1), a.rk) : z;
+            out[0] = nibble_word(w0.x); out[1] = nibble_word(w0.y);
+            out[2] = nibble_word(w0.z); out[3] = nibble_word(w0.w);
 #pragma unroll
-            for (int ch = 0; ch < 4; ch++) out[ch] = clamp_chunk(out[ch], S.ctab[8 * kb + ch], a.cm2, a.cc2);
+            for (int ch = 0; ch < 4; ch++) out[ch] = gen_chunk<TY>(out[ch], S.ctab[8 * kb + ch], a.cm2, a.cc2);
           }
-        }
-        const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
-        TRG(tl, kb, 1);
-        if ((gw & 3) == 0) mbar_wait_sleep(&S.g_empty[st], ph ^ 1u, 128);   // one poller per group
-        named_bar(6 + grp, 128);
-        TRG(tl, kb, 2);
-        uint8_t* slot = sG + st * kTile;
-        const int e0 = 64 * kb;
+          const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
+          TRG(tl, kb, 1);
+          if ((gw & 3) == 0) mbar_wait_sleep(&S.g_empty[st], ph ^ 1u, 128);   // one poller per group
+          named_bar(6 + grp, 128);
+          TRG(tl, kb, 2);
+          uint8_t* slot = sG + st * kTile;
+          const int e0 = 64 * kb;
 #pragma unroll
-        for (int ch = 0; ch < 4; ch++)
-          if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)         // only the K steps the MMA reads
-            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = out[ch];
-        const uint32_t w1w[4] = {w1.x, w1.y, w1.z, w1.w};
+          for (int ch = 0; ch < 4; ch++)
+            if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)         // only the K steps the MMA reads
+              *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = out[ch];
+          const uint32_t w1w[4] = {w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-        for (int ch = 4; ch < 8; ch++) {
-          uint4 o = nibble_word(w1w[ch - 4]);
-          if (clampk) o = clamp_chunk(o, S.ctab[8 * kb + ch], a.cm2, a.cc2);
-          if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)
-            *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = o;
+          for (int ch = 4; ch < 8; ch++) {
+            const uint4 o = gen_chunk<TY>(nibble_word(w1w[ch - 4]), S.ctab[8 * kb + ch], a.cm2, a.cc2);
+            if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)
+              *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = o;
+          }
+          fence_proxy_async();
+          __syncwarp();
+          TRG(tl, kb, 3);
+          if (lane == 0) arrive_leader(&S.g_full[st], rank);
+        };
+        switch (clampk ? (int)S.stype[kb] : kGenBox) {
+          case kGenRelu: stage(std::integral_constant<int, kGenRelu>{}); break;
+          case kGenLower: stage(std::integral_constant<int, kGenLower>{}); break;
+          case kGenInterior: stage(std::integral_constant<int, kGenInterior>{}); break;
+          case kGenBox: stage(std::integral_constant<int, kGenBox>{}); break;
+          default: stage(std::integral_constant<int, kGenGeneral>{}); break;
         }
-        fence_proxy_async();
-        __syncwarp();
-        TRG(tl, kb, 3);
-        if (lane == 0) arrive_leader(&S.g_full[st], rank);
         TRG(tl, kb, 4);
       }
       if (gt == 0) TR(tl, 7);
@@ -720,6 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const bool eval = a.eval_idx != nullptr;
     const bool need12 = a.pair12 >= 0 && !eval, need23 = a.pair23 >= 0 && !eval;
     const float stepS = a.stepS;
+    const bool clampk = a.clamp != 0;
     uint32_t tl = 0;
     for (uint64_t t = t_begin; t < t_end; t++, tl++) {
       const TileInfo ti = tile_info(a, t);
@@ -792,8 +862,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         const int p = h ? 2 * k4 + 3 : (k4 < 2 ? k4 : 2 * k4 - 2);   // piece: groups 2p, 2p + 1
         const int kbs = p >> 1;                            // the 64-neuron block it completes a part of
         uint32_t v[32];
+        TR1(tl, k4, 0);
         tmem_ld32(R1 + loff + 32u * p, v);
         tmem_ld_wait();
+        TR1(tl, k4, 1);
+        // statistics wanted while some row of the warp can still end with <= 1 change (below)
+        const bool stat1 = __any_sync(0xffffffffu, need12 && valid && nsc1 <= 1);
+        if (stat1 && clampk) {
+          // PHILOX_CLAMP: u1 - u1_base = 2^-s acc exactly up to the accumulation (the base trace is
+          // base1), so the L-inf partial is max |acc| (scaled by 2^-s once, after the pass)
+          float aa[16], ab[16];
+#pragma unroll
+          for (int j = 0; j < 16; j++) { aa[j] = __uint_as_float(v[j]); ab[j] = __uint_as_float(v[16 + j]); }
+          linf1 = max_abs16(max_abs16(linf1, aa), ab);
+        }
         acc_to_u1(v, S.b1 + 32 * p, stepS);
         uint32_t hl[32];                                   // [hi 2p | lo 2p | hi 2p+1 | lo 2p+1]
 #pragma unroll
@@ -809,7 +891,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 #pragma unroll
           for (int j = 0; j < 32; j++) a.eval_out[cidx * a.T + 32 * p + j] = __uint_as_float(v[j]);
         }
-        if (__any_sync(0xffffffffu, need12 && valid && nsc1 <= 1)) {
+        if (stat1 && clampk) {
+          float u0[16], u1v[16];
+#pragma unroll
+          for (int j = 0; j < 16; j++) { u0[j] = __uint_as_float(v[j]); u1v[j] = __uint_as_float(v[16 + j]); }
+          minab1 = min_abs16(min_abs16(minab1, u0), u1v);
+        } else if (stat1) {
 #pragma unroll
           for (int hh = 0; hh < 2; hh++) {
             const float4* ub = reinterpret_cast<const float4*>(S.ub1 + 32 * p + 16 * hh);
@@ -828,6 +915,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             minab1 = min_abs16(minab1, uu);
           }
         }
+        TR1(tl, k4, 2);
         {                                                  // every piece signs off its half of the block
           tmem_st_wait();
           fence_before();
@@ -836,6 +924,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           TRE(0, tl, 2 + kbs);
           TRE2(tl, 0, 2 + kbs);
         }
+        TR1(tl, k4, 3);
       }
       TRE(0, tl, 1);
       pair_exchange_i(S, h, r, nsc1, istar1, 9 + q);
@@ -845,6 +934,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const bool slow1 = __any_sync(0xffffffffu, need12 && valid && nsc1 <= 1);
       float dummy = 0.f;
       if (slow1) pair_exchange_f(S, h, r, linf1, minab1, dummy, 9 + q);
+      if (clampk) linf1 *= stepS;                         // max |acc| -> max |u1 - u1_base|
       minab1 = fminf(minab1, S.minub1);
       const bool cond1 = need12 && valid && ((nsc1 == 1) || (nsc1 == 0 && linf1 >= th1));
       const bool amb1 = minab1 < tau0 || (nsc1 == 0 && fabsf(linf1 - th1) < tau0);
@@ -1204,6 +1294,9 @@ extern "C" int mlpv_f3_trace_e2_read(void* host) {
 extern "C" int mlpv_f3_trace_done_read(void* host) {
   return (int)cudaMemcpyFromSymbol(host, f3::g_trace_done, sizeof f3::g_trace_done);
 }
+extern "C" int mlpv_f3_trace_e1p_read(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, f3::g_trace_e1p, sizeof f3::g_trace_e1p);
+}
 extern "C" int mlpv_f3_trace_gen_read(void* host) {
   return (int)cudaMemcpyFromSymbol(host, f3::g_trace_gen, sizeof f3::g_trace_gen);
 }
@@ -1334,10 +1427,22 @@ cudaError_t launch_fused3(const DevNet& net, const void* blk, const void* bases,
     a.cm2 = pert.clamp_m2;
     a.cc2 = pert.clamp_c2;
     a.clampc = ws.clampc;
+    const double o15 = pert.origin_d + 15.0 * pert.step_d;
+    a.offlo = (float)std::ldexp(std::fmin(pert.origin_d, o15), pert.clamp_s);
+    a.offhi = (float)std::ldexp(std::fmax(pert.origin_d, o15), pert.clamp_s);
   } else {
     a.stepS = (float)(pert.step_d * 16777216.0);       // step * 2^24 (the levels are l * 2^-24)
   }
   a.base1 = ws.base1;
+  {
+    uint32_t k0 = (uint32_t)pert.seed, k1 = (uint32_t)(pert.seed >> 32);
+    for (int r = 0; r < 10; r++) {
+      a.rk[2 * r] = k0;
+      a.rk[2 * r + 1] = k1;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+  }
   if (eval_idx) {
     a.tiles_per_base = (uint64_t)((eval_n + 255) / 256);
     a.n_pairs_tiles = a.tiles_per_base;

@@ -90,6 +90,12 @@ struct LargeArgs {
   int pair_of_lower[kMaxL + 1];    // pair index whose lower layer is k, or -1
   int soff[kMaxL + 2];             // staged bias / base potentials: layer l at [soff[l], soff[l+1]) (x4 aligned)
   int staged;                      // 1: biases and the tile's base potentials live in shared memory
+  // PHILOX_CLAMP (reading C14): layer 1 contracts A = d 2^s (fp16, d = x' - x exact) against the fp16
+  // copy of W1 (W1h, the layer-1 tile layout) and forms u1 = base1 + 2^-s acc
+  int clamp;
+  float stepS;
+  uint32_t cm2, cc2;
+  const uint8_t* W1h;
 };
 
 struct TileInfo {
@@ -178,13 +184,49 @@ __device__ __forceinline__ uint2 lattice8_u8(uint32_t w, uint2 x8, uint32_t s, u
   return make_uint2(prmt(y[0], y[1], 0x6420u), prmt(y[2], y[3], 0x6420u));
 }
 
+// PHILOX_CLAMP: the 8 levels of a Philox word as fp16 subnormals l 2^-24 (pairs in pixel order),
+// then d 2^s = min(max(fma(l 2^-24, step 2^(24+s), origin 2^s), -x 2^s), (1-x) 2^s) per pair
+// (k_fused3.cu has the same construction; every step is exact, C14/C19)
+__device__ __forceinline__ uint4 clamp_word(uint32_t w, uint4 nx, uint4 px, uint32_t m2, uint32_t c2) {
+  const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
+  uint32_t o[4];
+  const uint32_t nxa[4] = {nx.x, nx.y, nx.z, nx.w}, pxa[4] = {px.x, px.y, px.z, px.w};
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const uint32_t lv = prmt(lo, hi, (uint32_t)k | ((8u + k) << 4) | ((4u + k) << 8) | ((12u + k) << 12));
+    const __half2 off = __hfma2(*reinterpret_cast<const __half2*>(&lv), *reinterpret_cast<const __half2*>(&m2),
+                                *reinterpret_cast<const __half2*>(&c2));
+    const __half2 d = __hmin2(__hmax2(off, *reinterpret_cast<const __half2*>(&nxa[k])),
+                              *reinterpret_cast<const __half2*>(&pxa[k]));
+    o[k] = *reinterpret_cast<const uint32_t*>(&d);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 // ----------------------------------------------------------------------------- generator
 __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot) {
   const int n0 = a.net.sizes[0];
   const uint64_t c = row_index(a, ti, r);
   const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
   const bool valid = r < ti.nvalid;
-  if (a.net.numeric == MLPV_NUM_BF16) {
+  if (a.clamp) {
+    const int nch = (n0 + 7) / 8;
+    const uint4* tab = a.ws.clampc + (size_t)ti.b * 2 * nch;
+#pragma unroll
+    for (int hb = 0; hb < 2; hb++) {
+      const int j = 2 * kb + hb;
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (32 * j < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, k0, k1);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int ww = 0; ww < 4; ww++) {
+        const int ch = 4 * j + ww;                       // 8-pixel chunk; beyond n_0: bounds 0, d = 0
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        const uint4 nx = ch < nch ? __ldg(tab + 2 * ch) : z, px = ch < nch ? __ldg(tab + 2 * ch + 1) : z;
+        *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (4 * hb + ww))) = clamp_word(ws[ww], nx, px, a.cm2, a.cc2);
+      }
+    }
+  } else if (a.net.numeric == MLPV_NUM_BF16) {
     const uint16_t* x = reinterpret_cast<const uint16_t*>(a.bases) + (size_t)ti.b * n0;
     const __nv_bfloat162 step2 = __floats2bfloat162_rn(a.pert.step_f, a.pert.step_f);
     const __nv_bfloat162 org2 = __floats2bfloat162_rn(a.pert.origin_f, a.pert.origin_f);
@@ -364,9 +406,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         float linf_f = 0.f, minab = 3.0e38f, vcamb = 3.0e38f;
         int32_t linf_i = 0;
         const float* bias_f = a.staged ? reinterpret_cast<const float*>(s_bias + a.soff[l]) : static_cast<const float*>(a.net.b[l - 1]);
+        // PHILOX_CLAMP layer 1: u1 = base1 + 2^-s acc (fma with 1.0 elsewhere: the same rounding as +)
+        const float sS = (l == 1 && a.clamp) ? a.stepS : 1.0f;
+        if (l == 1 && a.clamp) bias_f = a.ws.base1 + (size_t)ti.b * a.net.sizes[1];
+
         const int32_t* bias_i = a.staged ? reinterpret_cast<const int32_t*>(s_bias + a.soff[l]) : static_cast<const int32_t*>(a.net.b[l - 1]);
         const float* ub_f = a.staged ? reinterpret_cast<const float*>(s_ub + a.soff[l])
                                      : static_cast<const float*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
+        // float layers l >= 2 in the delta form (reading C19): the MMA contracts W_l (h_{l-1} -
+        // h_{l-1}^base) and u_l = u_l^base + acc, so the fp32 accumulation only carries the small
+        // perturbation terms (the bias is inside u_l^base)
+        if (l >= 2) bias_f = ub_f;
         const int32_t* ub_i = a.staged ? reinterpret_cast<const int32_t*>(s_ub + a.soff[l])
                                        : static_cast<const int32_t*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
         uint8_t* hdst = scratch + a.h_off[l];
@@ -397,10 +447,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
 #pragma unroll
                 for (int q4 = 0; q4 < 8; q4++) {
                   const float4 b4 = reinterpret_cast<const float4*>(bias_f + j0)[q4];
-                  u[4 * q4] = __uint_as_float(v[4 * q4]) + b4.x;
-                  u[4 * q4 + 1] = __uint_as_float(v[4 * q4 + 1]) + b4.y;
-                  u[4 * q4 + 2] = __uint_as_float(v[4 * q4 + 2]) + b4.z;
-                  u[4 * q4 + 3] = __uint_as_float(v[4 * q4 + 3]) + b4.w;
+                  u[4 * q4] = fmaf(__uint_as_float(v[4 * q4]), sS, b4.x);
+                  u[4 * q4 + 1] = fmaf(__uint_as_float(v[4 * q4 + 1]), sS, b4.y);
+                  u[4 * q4 + 2] = fmaf(__uint_as_float(v[4 * q4 + 2]), sS, b4.z);
+                  u[4 * q4 + 3] = fmaf(__uint_as_float(v[4 * q4 + 3]), sS, b4.w);
                 }
                 if ((ua & 15u) == 0) {
 #pragma unroll
@@ -419,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                   const bool in = i < nin;
-                  u[i] = in ? __uint_as_float(v[i]) + bias_f[j0 + i] : 0.f;
+                  u[i] = in ? fmaf(__uint_as_float(v[i]), sS, bias_f[j0 + i]) : 0.f;
                   ubv[i] = in ? ub_f[j0 + i] : 0.f;
                 }
               }
@@ -467,7 +517,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
                 // h = hi + lo, two fp16 (RN), reading C19
 #pragma unroll
                 for (int i = 0; i < 16; i++) {
-                  const float h0 = fmaxf(u[2 * i], 0.f), h1 = fmaxf(u[2 * i + 1], 0.f);
+                  // dh = ReLU(u) - ReLU(u_base), the next layer's A operand in the delta form
+                  const float h0 = fmaxf(u[2 * i], 0.f) - fmaxf(ubv[2 * i], 0.f);
+                  const float h1 = fmaxf(u[2 * i + 1], 0.f) - fmaxf(ubv[2 * i + 1], 0.f);
                   const __half2 hi2 = __floats2half2_rn(h0, h1);
                   const float2 hf = __half22float2(hi2);
                   const __half2 lo2 = __floats2half2_rn(h0 - hf.x, h1 - hf.y);
@@ -716,7 +768,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               const uint32_t st = psA % kSPA, ph = (psA / kSPA) & 1u;
               mbar_wait(&pemptyA[st], ph ^ 1u);
               mbar_expect_tx(&pfullA[st], wb);
-              bulk_g2s(sPA + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wb, &pfullA[st]);
+              const uint8_t* W = a.clamp ? a.W1h : ld.W;     // PHILOX_CLAMP: the fp16 copy of W1
+              bulk_g2s(sPA + st * kWBytes, W + ((size_t)ch * ld.nkb + kb) * wbytes, wb, &pfullA[st]);
               psA++;
             } else {
               const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
@@ -744,7 +797,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         KT(tl, 0);
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
-          const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, l == 1 ? 1 : 0, l == 1 ? 1 : 0);
+          const uint32_t bf1 = (l == 1 && !a.clamp) ? 1u : 0u;          // layer 1: bf16 x bf16, or f16 (clamp)
+          const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, bf1, bf1);
           if (l == 1 && (ld.nchunks & 1) == 0) {
             // chunk pairs: both accumulators, one generated A stage per K block (half the Philox work)
             for (int cp = 0; cp < ld.nchunks / 2; cp++) {
@@ -936,7 +990,13 @@ static bool use_fused3(const DevNet& net) {     // MLPV_NO_FUSED3=1: debugging o
   return fused3_applicable(net) && !(env && env[0] == '1');
 }
 
-// Wt_dev[0]: generic tiles; Wt_dev[1]: k_fused3 weight block (when applicable)
+static size_t L_bytes_layer1(const LargeGeom& g) {
+  const LayerDesc& d = g.lay[1];
+  return (size_t)d.nchunks * d.nkb * d.nc * 128;
+}
+
+// Wt_dev[0]: generic tiles; Wt_dev[1]: k_fused3 weight block (when applicable); Wt_dev[2]: BF16 nets,
+// the fp16 copy of the layer-1 tiles (PHILOX_CLAMP)
 cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const void* const* b_host, void** Wt_dev,
                           size_t* scratch_per_cta, std::string* why) {
   *scratch_per_cta = 0;
@@ -985,6 +1045,27 @@ cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const vo
   e = cudaMemcpy(p, buf.data(), g.w_total, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) { cudaFree(p); return e; }
   Wt_dev[0] = p;                                   // one allocation; layers at w_off
+  if (fl) {
+    // PHILOX_CLAMP: W1 as fp16 in the layer-1 tile layout (the A operand is fp16); bf16 -> fp16 is
+    // exact for |w| >= 2^-17, smaller weights round with absolute error <= 2^-25 (C19)
+    const size_t n1b = L_bytes_layer1(g);
+    std::vector<uint8_t> hb(buf.begin() + g.w_off[1], buf.begin() + g.w_off[1] + n1b);
+    for (size_t i = 0; i + 1 < n1b; i += 2) {
+      const uint16_t b = (uint16_t)(hb[i] | (hb[i + 1] << 8));
+      uint32_t u = (uint32_t)b << 16;
+      float f;
+      memcpy(&f, &u, 4);
+      const uint16_t hh = host_f2h(f);
+      hb[i] = (uint8_t)(hh & 0xFF);
+      hb[i + 1] = (uint8_t)(hh >> 8);
+    }
+    void* q = nullptr;
+    e = cudaMalloc(&q, n1b);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(q, hb.data(), n1b, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(q); return e; }
+    Wt_dev[2] = q;
+  }
   return cudaSuccess;
 }
 
@@ -992,15 +1073,17 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
                          const DevPert& pert, const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out, int num_sms,
                          cudaStream_t st, bool* supported, std::string* why) {
-  if (pert.kind == MLPV_PERT_PHILOX_BOX || pert.kind == MLPV_PERT_PHILOX_CLAMP) {   // built on the fused path only
-    if (!(use_fused3(net) && Wt[1])) {
+  if (pert.kind == MLPV_PERT_PHILOX_BOX || pert.kind == MLPV_PERT_PHILOX_CLAMP) {
+    if (use_fused3(net) && Wt[1]) {                   // 784-256-256-n nets: the fused kernel
+      *supported = true;
+      return launch_fused3(net, Wt[1], bases, n_base, pert, prop, cov, res, ws, eval_idx, eval_n, eval_base,
+                           eval_out, num_sms, st);
+    }
+    if (pert.kind == MLPV_PERT_PHILOX_BOX || !Wt[2]) {  // the generic kernel builds the clamped box only
       *supported = false;
-      *why = "PHILOX_BOX / PHILOX_CLAMP are built for 3-layer BF16 nets with 256-wide hidden layers, n_0 even <= 1024 (k_fused3)";
+      *why = "PHILOX_BOX is built for 3-layer BF16 nets with 256-wide hidden layers, n_0 even <= 1024 (k_fused3)";
       return cudaSuccess;
     }
-    *supported = true;
-    return launch_fused3(net, Wt[1], bases, n_base, pert, prop, cov, res, ws, eval_idx, eval_n, eval_base,
-                         eval_out, num_sms, st);
   }
   LargeGeom g;
   *supported = geometry(net, &g, why);
@@ -1032,6 +1115,13 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
   a.scratch_per_cta = g.scratch_per_cta;
   if (!scratch) return cudaErrorInvalidValue;     // the handle's scratch: num_sms x scratch_per_cta, K padding zero
   a.scratch = static_cast<uint8_t*>(scratch);
+  if (pert.kind == MLPV_PERT_PHILOX_CLAMP) {
+    a.clamp = 1;
+    a.stepS = ldexpf(1.0f, -pert.clamp_s);
+    a.cm2 = pert.clamp_m2;
+    a.cc2 = pert.clamp_c2;
+    a.W1h = static_cast<const uint8_t*>(Wt[2]);
+  }
   a.soff[1] = 0;
   for (int l = 1; l <= net.L; l++) a.soff[l + 1] = a.soff[l] + ((net.sizes[l] + 3) & ~3);
   const size_t stage_bytes = (size_t)2 * a.soff[net.L + 1] * 4;

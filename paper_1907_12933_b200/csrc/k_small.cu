@@ -116,15 +116,17 @@ __device__ __forceinline__ float act_float(int act, float u) {
 // the fixed-point numerics, fp32 for the float numerics), base class, and the layer-1 delta
 // tables Delta[s][l][i] = W1[i, p_s] * (x'_{p_s}(l) - x_{p_s}) of subset / tuple spaces.
 __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, const void* levels, BaseWS ws) {
-  extern __shared__ float sm_f[];
+  extern __shared__ double sm_d[];
   const int b = blockIdx.x;
   const int n0 = net.sizes[0];
   int maxw = 0;
   for (int l = 0; l <= net.L; l++) maxw = max(maxw, net.sizes[l]);
-  float* hf = sm_f;                               // [maxw]
-  float* hn = sm_f + maxw;                        // [maxw]
-  int32_t* hi = reinterpret_cast<int32_t*>(sm_f);
-  int32_t* hin = reinterpret_cast<int32_t*>(sm_f + maxw);
+  // float numerics: the base trace in double (every potential rounded to fp32 once; reading C19 /
+  // C23: the float kernels take the base potentials as their reference point)
+  double* hf = sm_d;                              // [maxw]
+  double* hn = sm_d + maxw;                       // [maxw]
+  int32_t* hi = reinterpret_cast<int32_t*>(sm_d);
+  int32_t* hin = reinterpret_cast<int32_t*>(sm_d + maxw);
   const bool fixed = net.numeric == MLPV_NUM_Q4_12 || net.numeric == MLPV_NUM_INT8;
   const size_t in_sz = net.numeric == MLPV_NUM_FP32 ? 4 : (net.numeric == MLPV_NUM_INT8 ? 1 : 2);
   const char* x = static_cast<const char*>(bases) + in_sz * (size_t)n0 * b;
@@ -180,7 +182,7 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
         const int p = 8 * ch + 2 * k + h;
         uint16_t nx = 0, px = 0;
         if (p < n0) {
-          const float xv = hf[p];
+          const float xv = (float)hf[p];
           const __half hn = __float2half_rn(-xv * sc), hp = __float2half_rn((1.0f - xv) * sc);
           nx = __half_as_ushort(hn);
           px = __half_as_ushort(hp);
@@ -210,13 +212,18 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
           if (l < net.L) hin[i] = act_fixed(net.numeric, net.act, acc, net.shift[l - 1], net.knots);
         }
       } else {
-        float acc = row_dot_f(net.W[l - 1], net.numeric, i, fan, hf, lane);
+        double acc = 0.0;
+        for (int j = lane; j < fan; j += 32) acc += (double)wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hf[j];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
-          acc += static_cast<const float*>(net.b[l - 1])[i];
-          static_cast<float*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
-          if (l < net.L) hn[i] = act_float(net.act, acc);
+          acc += (double)static_cast<const float*>(net.b[l - 1])[i];
+          float u = (float)acc;
+          // PHILOX_CLAMP: the base's layer-1 potentials are base1 (the fp64 sum rounded once), the
+          // value the kernels form for the zero perturbation (reading C23); this lane wrote it above
+          if (l == 1 && pert.kind == MLPV_PERT_PHILOX_CLAMP && ws.base1 != nullptr) u = ws.base1[(size_t)b * net.sizes[1] + i];
+          static_cast<float*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = u;
+          if (l < net.L) hn[i] = net.act == MLPV_ACT_SIGMOID ? 1.0 / (1.0 + exp(-acc)) : (acc > 0.0 ? acc : 0.0);
         }
       }
     }
@@ -271,7 +278,7 @@ cudaError_t launch_base_prologue(const DevNet& net, const void* bases, int n_bas
                                  const void* levels_dev, BaseWS ws, cudaStream_t st) {
   int maxw = 0;
   for (int l = 0; l <= net.L; l++) maxw = maxw > net.sizes[l] ? maxw : net.sizes[l];
-  size_t smem = sizeof(float) * 2 * (size_t)maxw;
+  size_t smem = sizeof(double) * 2 * (size_t)maxw;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_base_prologue, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -211,7 +211,7 @@ extern "C" mlpv_status mlpv_create(const mlpv_net* net, const mlpv_quant* quant,
     cudaError_t pe = prepare_large(d, net->W, net->b, h->Wt, &per_cta, &h->large_why);
     if (pe != cudaSuccess) { mlpv_destroy(h); return fail(nullptr, MLPV_E_CUDA, "prepare_large: %s", cudaGetErrorString(pe)); }
     h->large_ready = h->large_why.empty();
-    for (int l = 0; l < L; l++) if (h->Wt[l]) h->allocs.push_back(h->Wt[l]);
+    for (int l = 0; l < kMaxL; l++) if (h->Wt[l]) h->allocs.push_back(h->Wt[l]);
     if (h->large_ready && per_cta > 0) {
       // the handle's own activation scratch (K padding zeroed once; the kernels never write it)
       const size_t bytes = per_cta * (size_t)h->num_sms;

@@ -344,6 +344,16 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a short suspend-time hint (the caller has other work to look at between tries)
+__device__ __forceinline__ bool mbar_try_ns(uint64_t* bar, uint32_t phase, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
 // two barriers polled together (their try_wait latencies overlap)
 __device__ __forceinline__ void mbar_wait2(uint64_t* b1, uint32_t ph1, uint64_t* b2, uint32_t ph2) {
   bool d1 = false, d2 = false;

@@ -180,7 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
   if (issuer) {
     if (MODE != 3) mbar_wait_cluster(&ready, 0); else mbar_wait(&ready, 0);
     fence_after();
-    const uint32_t N = MODE == 2 ? 128 : 256;
+    const uint32_t N = MODE == 2 ? 128 : (MODE == 29 ? 16 : (MODE == 30 ? 64 : 256));
     const uint32_t idesc = MODE == 3 ? idesc_f16(128, N, 1, 1) : (MODE == 20 ? idesc_f16(256, N, 0, 0) : idesc_f16(256, N, 1, 1));
     long long t0 = clock64();
     if (MODE == 21 || MODE == 22 || MODE == 23) {      // rings + per-stage readiness checks (k_fused3 issuer)
@@ -225,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
           const uint64_t ad = sdesc_sw128(smem_u32(sA + kb * 16384 + kk * 32));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + kb * 16384 + kk * 32));
           const uint32_t acc = (r | kb | kk) ? 1u : 0u;
-          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16) || MODE == 18 || MODE == 19 || MODE == 20 || MODE == 24 || MODE == 26 || MODE == 28) mma2_f16_ss(tb, ad, bd, idesc, acc);
+          if (MODE == 0 || MODE == 2 || (MODE >= 4 && MODE < 16) || MODE == 18 || MODE == 19 || MODE == 20 || MODE == 24 || MODE == 26 || MODE == 28 || MODE == 29 || MODE == 30) mma2_f16_ss(tb, ad, bd, idesc, acc);
           else if (MODE == 1) mma2_f16_ts(tb, tb + 256 + kb * 32 + kk * 8, bd, idesc, acc);
           else if (MODE == 16 || MODE == 17) mma2_f16_ts(tb + 256, tb + kb * 32 + kk * 8, bd, idesc_f16(256, 128, 1, 1), acc);
           else mma1_ss(tb, ad, bd, idesc, acc);
@@ -269,15 +269,21 @@ void run(const char* name) {
   cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long c = 0;
   cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
-  const double M = MODE == 3 ? 128 : 256, N = MODE == 2 ? 128 : 256;
+  const double M = MODE == 3 ? 128 : 256, N = MODE == 2 ? 128 : (MODE == 29 ? 16 : (MODE == 30 ? 64 : 256));
   const double groups = MODE == 3 ? 148 : 74;
-  const double flops = (MODE == 13 || MODE >= 21) ? 2.0 * M * N * 16 * 52 * (reps / 4) * groups : MODE == 13 ? 2.0 * M * N * 16 * 50 * (reps / 4) * groups : 2.0 * M * N * 16 * 16 * reps * groups;
+  const double flops = (MODE == 13 || (MODE >= 21 && MODE < 29)) ? 2.0 * M * N * 16 * 52 * (reps / 4) * groups : MODE == 13 ? 2.0 * M * N * 16 * 50 * (reps / 4) * groups : 2.0 * M * N * 16 * 16 * reps * groups;
   printf("%-28s err=%d  %.3f ms  %.1f TFLOP/s  cycles/MMA (cluster 0) %.1f\n", name, (int)e, ms, flops / (ms * 1e-3) / 1e12,
-         (double)c / (MODE >= 21 ? 52.0 * (reps / 4) : MODE == 13 ? 50.0 * (reps / 4) : 16.0 * reps));
+         (double)c / ((MODE >= 21 && MODE < 29) ? 52.0 * (reps / 4) : MODE == 13 ? 50.0 * (reps / 4) : 16.0 * reps));
 }
 
 int main() {
   run<0>("2CTA SS M256 N256 K16");
   run<3>("1CTA SS M128 N256 K16");
+  run<29>("2CTA SS M256 N16 K16");
+  run<30>("2CTA SS M256 N64 K16");
+  run<10>("SS + 8 warps Philox ALU");
+  run<11>("SS + 8 warps STS.128 stream");
+  run<12>("SS + 8 warps Philox+STS");
+  run<24>("SS + 8 warps TMEM ld/st epi");
   return 0;
 }

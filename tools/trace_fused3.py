@@ -1,6 +1,6 @@
 """Timeline of k_fused3 (debug build with -DMLPV_TRACE): per-tile clock64 stamps of cluster 0.
 
-    python tools/trace_fused3.py [n_samples_per_base]
+    python tools/trace_fused3.py [n_samples_per_base]      (MLPV_TRACE_CFG=cfg4_box: the unclamped box)
 """
 import ctypes as C
 import os
@@ -27,7 +27,7 @@ EV = {0: "iss.top", 1: "iss.kb0", 2: "iss.kblast", 3: "iss.h1rdy", 4: "iss.acc2f
       31: "prod.w0"}
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
-cfg = M.make_config("cfg4")
+cfg = M.make_config(os.environ.get("MLPV_TRACE_CFG", "cfg4"))
 cfg = cfg.subset(n_base=cfg.n_base, begin=0, end=S)
 chk = P.Checker(cfg.net)
 bases = to_device_bases(cfg)
@@ -130,3 +130,18 @@ for w in range(8):
         nxt = gp[w, i + 1, 0] if i < 7 else e[4]
         row.append(f"{e[1]-e[0]}/{e[2]-e[1]}/{e[3]-e[2]}/{e[4]-e[3]}/{nxt-e[4]}")
     print(f"  warp {w} (q{w & 3} h{w >> 2}): " + "  ".join(row))
+
+e1 = np.zeros((2, 8, 5, 4), np.uint64)
+assert P.lib().mlpv_f3_trace_e1p_read(e1.ctypes.data_as(C.c_void_p)) == 0
+e1 = e1.astype(np.int64)
+print("E1 per piece (tile 9): ld latency / compute / sign-off (st wait + fence + arrive) / gap to next piece")
+for rk in range(2):
+    for w in range(8):
+        row = []
+        for i in range(5):
+            e = e1[rk, w, i]
+            if not e[0]:
+                continue
+            nxt = e1[rk, w, i + 1, 0] if i < 4 and e1[rk, w, i + 1, 0] else e[3]
+            row.append(f"{e[1]-e[0]}/{e[2]-e[1]}/{e[3]-e[2]}/{nxt-e[3]}")
+        print(f"  rank {rk} warp {w}: " + "  ".join(row))
