@@ -41,10 +41,13 @@ def allgather_results(res: Dict, n_base: int, n_words: int, group=None) -> List[
     import torch
     import torch.distributed as dist
     flat = pack(res, n_base, n_words).contiguous()
+    dev = flat.device
+    if dist.get_backend(group) == "gloo" and flat.is_cuda:
+        flat = flat.cpu()                      # gloo: stage through host memory (tests, CPU-only boxes)
     world = dist.get_world_size(group)
     bufs = [torch.empty_like(flat) for _ in range(world)]
     dist.all_gather(bufs, flat, group=group)
-    return [unpack(b, n_base, n_words) for b in bufs]
+    return [unpack(b.to(dev), n_base, n_words) for b in bufs]
 
 
 def reduce_results(res: Dict, n_base: int, n_words: int, group=None, stream=None) -> Dict:
