@@ -149,7 +149,10 @@ typedef struct {
      * (not checked, no verdict, no coverage), so outside = range length - checked.  Fixed point:
      * sum of squared raw differences (int64) <= floor(restrict_l2^2 * S^2) in double, S = 4096 /
      * 255.  Float: sum over pixels, in pixel order, of (x' - x)^2 in double <= restrict_l2^2.
-     * Subset and tuple spaces only (MLPV_E_UNSUPPORTED for the Philox spaces).  0 = no restriction. */
+     * Every space: subset / tuple spaces filter inside the enumeration kernel (sum over the changed
+     * pixels); the Philox spaces run a mask pass that rebuilds each candidate and sums over all
+     * pixels in pixel order with separately rounded double operations (u8: exactly in integers).
+     * 0 = no restriction. */
     double restrict_l2;
 } mlpv_pert;
 

@@ -794,7 +794,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     for (uint64_t t = t_begin; t < t_end; t++, tl++) {
       const TileInfo ti = tile_info(a, t);
       const int grow = 128 * (int)rank + r;
-      const bool valid = grow < ti.nvalid;
+      // a row outside the restriction R (Philox spaces, k_restrict_mask) gets no verdict / coverage
+      const bool valid = grow < ti.nvalid && (eval || in_restriction(a.pert, ti.b, ti.start + (uint64_t)grow));
       const uint64_t cidx = eval ? (uint64_t)(ti.start + grow) : 0;
       if (ti.b != S.base_e) {                              // stage the base traces once per base input
         named_bar(2, 256);

@@ -380,8 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
       const TileInfo ti = tile_info(a, t);
       const int etl = (int)((t - blockIdx.x) / gridDim.x);
       (void)etl;
-      const bool valid = r < ti.nvalid;
       const uint64_t cidx = row_index(a, ti, r);
+      // a row outside the restriction R (Philox spaces, k_restrict_mask) gets no verdict / coverage
+      const bool valid = r < ti.nvalid && (eval || in_restriction(a.pert, ti.b, cidx));
       if (a.staged) {                              // this tile's base potentials (the previous tile's
         const uint32_t* tr = static_cast<const uint32_t*>(a.ws.trace) + (size_t)ti.b * T;   // reads ended
         for (int l = 1; l <= L; l++)                                                         // at its last

@@ -22,6 +22,84 @@ __global__ void k_init_result(DevResult r, int n_base, uint32_t n_words) {
   }
 }
 
+// ---------------------------------------------------------------- restriction R on the Philox spaces
+// (reading C27): one thread per candidate reconstructs the candidate
+// pixel by pixel (readings C14/C15) and sums (x'_p - x_p)^2 in pixel order with separately rounded
+// double operations (no contraction) -- the sum the definition states, so a candidate is inside R on
+// the GPU iff it is by that definition -- or exactly in int64 for u8 (against floor(b^2 255^2)).
+// One warp per 32 consecutive candidates of a base writes one mask word (ballot).
+__device__ __forceinline__ uint4 philox_r(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+// nearest bf16 value of v (8 significant bits, ties to even)
+__device__ __forceinline__ double rne_bf16_d(double v) {
+  if (v == 0.0) return v;
+  int e;
+  const double m = frexp(v, &e);
+  return ldexp(rint(ldexp(m, 8)), e - 8);
+}
+
+__global__ void k_restrict_mask(DevNet net, const void* bases, DevPert p, uint32_t* mask, uint64_t len) {
+  const int b = blockIdx.y;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n0 = net.sizes[0];
+  bool in = false;
+  if (i < len) {
+    const uint64_t c = p.begin + i;
+    const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
+    const bool u8 = net.numeric == MLPV_NUM_INT8;
+    double s2 = 0.0;
+    long long s2i = 0;
+    for (int j = 0; j < (n0 + 31) / 32; j++) {
+      const uint4 w = philox_r((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)b, (uint32_t)j, k0, k1);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      for (int q = 0; q < 32 && 32 * j + q < n0; q++) {
+        const int px = 32 * j + q;
+        const int l = (int)((ws[q >> 3] >> (4 * (q & 7))) & 15u);
+        if (u8) {
+          const int x = static_cast<const uint8_t*>(bases)[(size_t)b * n0 + px];
+          const int y = max(0, min(255, x + l * p.step_i + p.origin_i));
+          s2i += (long long)(y - x) * (y - x);
+          continue;
+        }
+        const double x = (double)__uint_as_float((uint32_t)static_cast<const uint16_t*>(bases)[(size_t)b * n0 + px] << 16);
+        double v;
+        if (p.kind == MLPV_PERT_PHILOX_LATTICE) {
+          const double off = rne_bf16_d(__dadd_rn(__dmul_rn((double)l, (double)p.step_f), (double)p.origin_f));
+          v = __dadd_rn(x, off);
+          v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+          v = rne_bf16_d(v);
+        } else {
+          v = __dadd_rn(x, __dadd_rn(p.origin_d, __dmul_rn((double)l, p.step_d)));
+          if (p.kind == MLPV_PERT_PHILOX_CLAMP) v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+        }
+        const double d = __dadd_rn(v, -x);
+        s2 = __dadd_rn(s2, __dmul_rn(d, d));
+      }
+    }
+    in = u8 ? s2i <= p.r2_raw : s2 <= p.r2_f;
+  }
+  const uint32_t word = __ballot_sync(0xffffffffu, in);
+  if ((threadIdx.x & 31) == 0 && i < len) mask[(size_t)b * p.rmask_wpb + (i >> 5)] = word;
+}
+
+cudaError_t launch_restrict_mask(const DevNet& net, const void* bases, int n_base, const DevPert& pert,
+                                 uint32_t* mask, cudaStream_t st) {
+  const uint64_t len = pert.end - pert.begin;
+  if (len == 0) return cudaSuccess;
+  dim3 grid((unsigned)((len + 127) / 128), (unsigned)n_base);
+  k_restrict_mask<<<grid, 128, 0, st>>>(net, bases, pert, mask, len);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_init_result(const DevResult& r, int n_base, uint32_t n_words, cudaStream_t st) {
   const int n = n_base > (int)n_words ? n_base : (int)n_words;
   const int blocks = (n + 255) / 256 > 0 ? ((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024) : 1;

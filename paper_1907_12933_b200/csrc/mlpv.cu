@@ -396,8 +396,7 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
   if (!std::isfinite(p->restrict_l2) || p->restrict_l2 < 0)
     return fail(h, MLPV_E_INVALID, "pert.restrict_l2 = %g (finite, >= 0)", p->restrict_l2);
   if (p->restrict_l2 > 0) {
-    if (is_philox(p->kind))
-      return fail(h, MLPV_E_UNSUPPORTED, "pert.restrict_l2 is built for the subset and tuple spaces");
+    // subset / tuple spaces: filtered inside k_small; Philox spaces: a mask pass (k_restrict_mask)
     dp->restrict_on = 1;
     const double b = p->restrict_l2;
     if (is_fixed(num)) {
@@ -675,7 +674,35 @@ static mlpv_status check_impl(mlpv_t h, const void* base_inputs, int32_t n_base,
   const bool fl = !is_fixed(h->net.numeric);
   if ((s = prepare(h, base_inputs, n_base, pert, dp, &dc, &plan, st, fl)) != MLPV_OK) return s;
   dc.tau_dev = (fl && !cov->tau) ? plan.tau_dev : nullptr;
-  if (pert->index_begin != pert->index_end) {
+  if (pert->index_begin != pert->index_end && is_philox(pert->kind) && dp.restrict_on) {
+    // restriction R on a Philox space: per chunk of the range, the mask pass marks the candidates
+    // inside R, then the enumeration kernel checks the marked ones (results accumulate over chunks)
+    const uint64_t len = pert->index_end - pert->index_begin;
+    uint64_t chunk = ((uint64_t)1 << 31) / (uint64_t)n_base;        // <= 256 MB of mask bits per pass
+    chunk = chunk < 32 ? 32 : chunk & ~(uint64_t)31;
+    if (chunk > len) chunk = len;
+    const uint32_t wpb = (uint32_t)((chunk + 31) / 32);
+    void* mask = nullptr;
+    CUDA_TRY(h, cudaMallocAsync(&mask, 4ull * wpb * n_base, st), "restriction mask");
+    mlpv_status rs = MLPV_OK;
+    for (uint64_t b0 = pert->index_begin; b0 < pert->index_end && rs == MLPV_OK; b0 += chunk) {
+      mlpv_pert pc = *pert;
+      pc.index_begin = b0;
+      pc.index_end = b0 + chunk < pert->index_end ? b0 + chunk : pert->index_end;
+      DevPert dpc = dp;
+      dpc.begin = pc.index_begin;
+      dpc.end = pc.index_end;
+      dpc.rmask = static_cast<const uint32_t*>(mask);
+      dpc.rmask_begin = pc.index_begin;
+      dpc.rmask_wpb = wpb;
+      cudaError_t e = launch_restrict_mask(h->net, base_inputs, n_base, dpc, static_cast<uint32_t*>(mask), st);
+      if (e != cudaSuccess) { rs = cuda_fail(h, e, "restriction mask"); break; }
+      h->launches++;
+      rs = run_kernel(h, base_inputs, n_base, &pc, dpc, dprop, dc, dr, plan, nullptr, 0, 0, nullptr, st);
+    }
+    cudaFreeAsync(mask, st);
+    if (rs != MLPV_OK) return rs;
+  } else if (pert->index_begin != pert->index_end) {
     if ((s = run_kernel(h, base_inputs, n_base, pert, dp, dprop, dc, dr, plan, nullptr, 0, 0, nullptr, st)) != MLPV_OK)
       return s;
   }

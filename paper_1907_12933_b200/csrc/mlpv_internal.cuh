@@ -61,6 +61,11 @@ struct DevPert {
   double r2_f;                // float: b^2
   long long r2_raw;           // fixed: floor(b^2 S^2), S = 4096 (Q4.12) / 255 (INT8)
   const void* levels;         // device copy of the levels (set by the plan; k_small's filter)
+  // restriction R on the Philox spaces: bit (b, c - rmask_begin) of rmask (words [n_base][rmask_wpb])
+  // is set iff candidate c of base b lies inside R (k_restrict_mask); nullptr = no restriction
+  const uint32_t* rmask;
+  uint64_t rmask_begin;
+  uint32_t rmask_wpb;
   // incremental bounds b_1 < .. < b_n (NEXT-2, reading C28): a violation's first_cex key is
   // (step << kStepShift) | index, step = smallest i with distance^2 <= r2 of b_i
   int n_steps;                // 0 = off
@@ -106,6 +111,14 @@ cudaError_t launch_neuron_cov(const DevNet& net, const DevCov& cov, const uint32
                               uint8_t* covered, uint32_t* counts, cudaStream_t st);
 cudaError_t launch_tau(const DevNet& net, const void* trace, int n_base, float* tau_out, cudaStream_t st);
 cudaError_t launch_split_steps(const DevResult& r, int n_base, int32_t* step, int32_t* step_u, cudaStream_t st);
+cudaError_t launch_restrict_mask(const DevNet& net, const void* bases, int n_base, const DevPert& pert,
+                                 uint32_t* mask, cudaStream_t st);
+// inside R? (Philox spaces with a restriction; always true otherwise)
+__device__ __forceinline__ bool in_restriction(const DevPert& p, int b, uint64_t c) {
+  if (!p.rmask) return true;
+  const uint64_t i = c - p.rmask_begin;
+  return (p.rmask[(size_t)b * p.rmask_wpb + (i >> 5)] >> (i & 31)) & 1u;
+}
 cudaError_t launch_pair_cov(const DevNet& net, const DevCov& cov, const void* trace, int n,
                             uint32_t* cov_all, uint32_t* cov_cert, cudaStream_t st);
 

@@ -549,6 +549,27 @@ def test_clamp_net_closed_form(oracle_mod):
     assert 2000 * 6 / 16 - 150 < len(hits) < 2000 * 6 / 16 + 150
 
 
+def test_restriction_on_philox_clamp_closed_form(oracle_mod):
+    """Restriction R on a Philox space (reading C27): base (0.5, 0.5), no clamping, so
+    delta^2 = step^2 ((l_0 - 7.5)^2 + (l_1 - 7.5)^2) with the two levels read straight off the Philox
+    stream; checked = #{c : that <= b^2}.  Also b -> large keeps all, and counts grow with b."""
+    O = oracle_mod
+    cfg = _clamp_net_cfg()
+    cfg.bases = M.f32_to_bf16_bits(np.array([[0.5, 0.5]], np.float32))
+    step = cfg.pert.lattice_step
+    key = [cfg.pert.seed & 0xFFFFFFFF, cfg.pert.seed >> 32]
+    lv = np.array([[int(O.philox([c, 0, 0, 0], key)[0]) >> (4 * n) & 15 for n in (0, 1)] for c in range(1000, 3000)])
+    r2 = ((lv - 7.5) ** 2).sum(axis=1) * step * step
+    prev = -1
+    for b in (0.01, 0.03, 0.05, 0.07, 1.0):
+        cfg.pert.restrict_l2 = b
+        n = int(O.check(cfg).checked[0])
+        assert n == int(np.sum(r2 <= b * b)), b
+        assert n >= prev
+        prev = n
+    assert prev == 2000
+
+
 def test_philox_is_counter_sensitive(oracle_mod):
     """Distinct counters / keys give distinct outputs; the same inputs give the same outputs."""
     O = oracle_mod

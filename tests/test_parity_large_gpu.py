@@ -241,3 +241,20 @@ def test_cfg5_bench_launch(P, oracle_mod, name):
         yb = oracle_mod.forward(cfg.net, cfg.bases[b])[-1]
         top = np.sort(y)[::-1]
         assert int(np.argmax(y)) != int(np.argmax(yb)) or (not fixed and top[0] - top[1] < 1e-5), (b, c)
+
+
+@pytest.mark.parametrize("name,b,nb,n", [("cfg4", 0.753, 3, 700), ("cfg4_box", 0.857, 2, 500), ("cfg5_bf16", 1.004, 2, 300),
+                                          ("cfg5_int8", 1.0, 2, 300)])
+def test_restriction_on_philox_spaces(P, oracle_mod, name, b, nb, n):
+    """Restriction R on the Philox spaces: the mask pass keeps the
+    candidates with delta <= b; checked (= inside R) is bit-exact against the oracle, verdicts and
+    coverage by the numeric's rules.  b is chosen to cut each slice roughly in half."""
+    cfg = M.make_config(name).subset(n_base=nb, begin=1000, end=1000 + n)
+    cfg.pert.restrict_l2 = b
+    o = oracle_mod.check(cfg)
+    assert 0 < int(o.checked.sum()) < nb * n
+    g = run_gpu(_checker(P, name) if name != "cfg4_box" else P.Checker(cfg.net), cfg)
+    if cfg.net.numeric == M.NUM_INT8:
+        assert_fixed_parity(g, o)
+    else:
+        assert_float_parity(g, o)
