@@ -2,14 +2,13 @@
 
 A Q4.12 net evaluates its sigmoid through the 129-knot piecewise-linear table of reading C17, so a
 reported counterexample may be an artefact of the table rather than of the network it stands for.
-`revalidate` re-evaluates each base input's first counterexample, and the base input itself, under
-that real-valued network -- weights raw / 4096 (exact in fp32), biases in accumulator units times
-the layer's scale (2^-24 for Q4.12), the exact logistic sigmoid -- on the library's FP32 path, and
-reports whether the property is still violated there.
-
-Everything runs through the public API (`Checker.eval`, `decode`): an arbitrary image x is the
-candidate of a two-pixel TUPLE_REPLACE space over the base x whose two levels are x_0 and x_1
-(index 1 replaces pixel 0 by x_0 and pixel 1 by x_1, i.e. reproduces x).
+`revalidate` re-checks each base input's first counterexample under that real-valued network --
+weights raw / 4096 (exact in fp32), biases in accumulator units times the layer's scale (2^-24 for
+Q4.12), the exact logistic sigmoid -- with the library's own check on the FP32 path: the base
+input is the real-valued base image and the perturbation space is a one-candidate SUBSET_REPLACE
+space that reproduces the counterexample (its changed pixels, each replaced by its own value).
+The verdict (violated / near-tie flagged) is mlpv_check's; this module only builds the arguments
+(no forward pass, argmax or property test here).
 """
 from __future__ import annotations
 
@@ -37,56 +36,51 @@ def exact_net(qnet):
                acc_scale=[1.0] * (len(qnet.sizes) - 1))
 
 
-def _logits(chk: Checker, x: np.ndarray, n_out: int) -> np.ndarray:
-    """Logits of the FP32 net for image x (see the module docstring)."""
-    import torch
+def one_candidate_space(base: np.ndarray, img: np.ndarray):
+    """A SUBSET_REPLACE space over `base` whose candidate `index` is `img` (float32 images): the
+    K <= 16 pixels where they differ, level k = img's value of the k-th of them, index digits 0..K-1
+    (pixel 0 most significant, reading C14).  K = 0 replaces pixel 0 by its own value."""
+    from mlpv_inputs import PERT_SUBSET_REPLACE
     from mlpv_inputs.configs import Pert
-    from mlpv_inputs import PERT_TUPLE_REPLACE
-    x = np.ascontiguousarray(x, np.float32)
-    pert = Pert(PERT_TUPLE_REPLACE, tuple=2, levels=np.array([x[0], x[1]], np.float32))
-    pert.index_end = pert.space_size(len(x))
-    base = torch.from_numpy(x[None, :]).cuda()
-    u = chk.eval(base, 0, pert, torch.tensor([1], dtype=torch.int64, device="cuda"))
-    return u[0, -n_out:].double().cpu().numpy()
-
-
-def _violated(prop, y: np.ndarray, base_cls: int) -> bool:
-    from mlpv_inputs import (PROP_ARGMAX_UNCHANGED, PROP_TARGET_NEVER, PROP_THRESHOLD_LITERAL,
-                             PROP_THRESHOLD_LITERAL_ALL)
-    cls = int(np.argmax(y))                        # lowest index on ties (reading C12)
-    if prop.kind == PROP_ARGMAX_UNCHANGED:
-        return cls != base_cls
-    if prop.kind == PROP_TARGET_NEVER:
-        return cls == prop.target
-    D = prop.target if prop.target >= 0 else base_cls
-    others = [y[i] > prop.V for i in range(len(y)) if i != D]
-    lit = all(others) if prop.kind == PROP_THRESHOLD_LITERAL_ALL else any(others)
-    assert prop.kind in (PROP_THRESHOLD_LITERAL, PROP_THRESHOLD_LITERAL_ALL)
-    return bool(y[D] < prop.V and lit)
+    px = np.nonzero(img != base)[0].astype(np.int32)
+    if len(px) == 0:
+        px = np.array([0], np.int32)
+    if len(px) > 16:
+        raise ValueError("counterexample differs from its base in more than 16 pixels")
+    K = len(px)
+    idx = 0
+    for k in range(K):
+        idx = idx * K + k
+    pert = Pert(PERT_SUBSET_REPLACE, pixels=px, levels=np.ascontiguousarray(img[px], np.float32),
+                index_begin=idx, index_end=idx + 1)
+    return pert, idx
 
 
 def revalidate(qnet, bases_q: np.ndarray, pert, prop, first_cex: np.ndarray, device: int = 0) -> List[Dict]:
-    """One record per base input with a counterexample: its index, the exact network's logits for
-    the counterexample and the base, whether the property is violated under the exact network,
-    and the top-2 margin there (a small margin means the verdict rests on rounding, not on the
-    table)."""
+    """One record per base input with a counterexample: its index, the exact network's potentials
+    for the counterexample (mlpv_eval) and the library's verdict under the exact network
+    (violated_exact, flagged_exact: the near-tie flag of reading C20).  violated_exact = False marks
+    a LUT artefact."""
+    import torch
+    from mlpv_inputs.configs import CovSpec
     net = exact_net(qnet)
     chk = Checker(net, device)
-    n_out = net.sizes[-1]
     out = []
     try:
         for b, c in enumerate(np.asarray(first_cex, np.uint64)):
             if c == UMAX:
                 continue
-            img = decode(NUM_Q4_12, pert, bases_q[b], b, int(c)).astype(np.float64) / 4096.0
-            base = np.asarray(bases_q[b], np.float64) / 4096.0
-            yb = _logits(chk, base, n_out)
-            y = _logits(chk, img, n_out)
-            top = np.sort(y)[::-1]
-            out.append({"base": b, "index": int(c), "logits": y, "base_logits": yb,
-                        "base_class": int(np.argmax(yb)), "class": int(np.argmax(y)),
-                        "violated_exact": _violated(prop, y, int(np.argmax(yb))),
-                        "margin": float(top[0] - top[1]) if len(top) > 1 else float("inf")})
+            img = (decode(NUM_Q4_12, pert, bases_q[b], b, int(c)).astype(np.float64) / 4096.0).astype(np.float32)
+            base = (np.asarray(bases_q[b], np.float64) / 4096.0).astype(np.float32)
+            sp, idx = one_candidate_space(base, img)
+            bt = torch.from_numpy(base[None, :]).cuda(device)
+            r = chk.check(bt, sp, prop, CovSpec([]))
+            u = chk.eval(bt, 0, sp, torch.tensor([idx], dtype=torch.int64, device=bt.device))
+            chk.sync()
+            out.append({"base": b, "index": int(c), "potentials": u[0].double().cpu().numpy(),
+                        "violated_exact": bool(int(r["violated"][0]) == 1),
+                        "flagged_exact": bool(int(r["flagged"][0]) == 1),
+                        "checked": int(r["checked"][0])})
     finally:
         chk.close()
     return out

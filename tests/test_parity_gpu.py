@@ -215,23 +215,30 @@ def test_literal_readings_gpu(P, oracle_mod):
 
 
 def test_lut_revalidation(P, oracle_mod):
-    """NEXT-4: the first counterexamples of the stress Q4.12 net re-evaluated under the real-valued
-    network it approximates (exact sigmoid, FP32 path) agree with the oracle's double forward of
-    that network (class, and the violation unless the margin is a near-tie)."""
-    from paper_1907_12933_b200.revalidate import exact_net, revalidate
+    """NEXT-4: the first counterexamples of the stress Q4.12 net re-checked by the library under the
+    real-valued network it approximates (exact sigmoid, FP32 path, a one-candidate space that
+    reproduces the counterexample): the candidate is the decoded image, its potentials agree with
+    the oracle's double forward of that network, and the library's verdict is the oracle's own
+    check of the same one-candidate space (C20 rules)."""
+    from paper_1907_12933_b200.revalidate import exact_net, one_candidate_space, revalidate
+    from mlpv_inputs.configs import CovSpec
     cfg = _stress_cfg2()
     g = run_gpu(P.Checker(cfg.net), cfg)
     recs = revalidate(cfg.net, cfg.bases, cfg.pert, cfg.prop, g["first_cex"])
     assert len(recs) == int(np.count_nonzero(g["first_cex"] != UMAX)) and len(recs) > 0
     en = exact_net(cfg.net)
     for r in recs:
-        img = oracle_mod.decode(cfg.net.numeric, cfg.pert, cfg.bases[r["base"]], r["base"], r["index"]).astype(np.float64) / 4096
-        yo = oracle_mod.forward(en, img.astype(np.float32))[-1]
-        yb = oracle_mod.forward(en, (cfg.bases[r["base"]].astype(np.float64) / 4096).astype(np.float32))[-1]
-        assert np.allclose(r["logits"], yo, rtol=1e-5, atol=1e-6)
-        if r["margin"] > 1e-5:
-            assert r["class"] == int(np.argmax(yo))
-            assert r["violated_exact"] == (int(np.argmax(yo)) != int(np.argmax(yb)))
+        assert r["checked"] == 1
+        img = (oracle_mod.decode(cfg.net.numeric, cfg.pert, cfg.bases[r["base"]], r["base"], r["index"]).astype(np.float64) / 4096).astype(np.float32)
+        base = (cfg.bases[r["base"]].astype(np.float64) / 4096).astype(np.float32)
+        sp, idx = one_candidate_space(base, img)
+        assert np.array_equal(oracle_mod.decode(M.NUM_FP32, sp, base, 0, idx), img)
+        yo = np.concatenate(oracle_mod.forward(en, img))
+        assert_logits_close(r["potentials"], yo)
+        c = M.Config("reval", "one candidate", en, base[None, :], sp, cfg.prop, CovSpec([]))
+        o = oracle_mod.check(c)
+        vo, fo = int(o.violated[0]), int(o.flagged[0])
+        assert int(r["violated_exact"]) == vo or (fo or r["flagged_exact"])
     print("LUT artefacts:", sum(not r["violated_exact"] for r in recs), "of", len(recs))
 
 
