@@ -130,10 +130,16 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
   const bool fixed = net.numeric == MLPV_NUM_Q4_12 || net.numeric == MLPV_NUM_INT8;
   const size_t in_sz = net.numeric == MLPV_NUM_FP32 ? 4 : (net.numeric == MLPV_NUM_INT8 ? 1 : 2);
   const char* x = static_cast<const char*>(bases) + in_sz * (size_t)n0 * b;
+  bool badq = false;
   for (int j = threadIdx.x; j < n0; j += blockDim.x) {
-    if (fixed) hi[j] = in_i(x, net.numeric, j);
-    else hf[j] = in_f(x, net.numeric, j);
+    if (fixed) {
+      hi[j] = in_i(x, net.numeric, j);
+      if (net.numeric == MLPV_NUM_Q4_12 && (hi[j] < 0 || hi[j] > 4096)) badq = true;   // reading C16
+    } else {
+      hf[j] = in_f(x, net.numeric, j);
+    }
   }
+  if (badq && ws.status) atomicOr(ws.status, kStatusQ412Base);
   __syncthreads();
   // dense layers: one warp per output neuron, lanes stride the fan-in (coalesced weight rows),
   // warp-shuffle sums

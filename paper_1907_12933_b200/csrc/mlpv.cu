@@ -140,8 +140,10 @@ extern "C" mlpv_status mlpv_create(const mlpv_net* net, const mlpv_quant* quant,
   // finiteness (float) and the fixed-point accumulator bound (reading C16/C18):
   // sum_j |w_ij| * x_max + |b_i| < 2^30 for every neuron, so every potential and every
   // base-vs-candidate difference fits in int32.
+  double hbound = 1.0;                       // BF16: bound on |input| of layer l (images in [0, 1])
   for (int l = 0; l < L; l++) {
     const int nl = net->sizes[l + 1], fan = net->sizes[l];
+    double nbound = 0.0;
     double xmax;
     // Q4.12 images are normalised: raw inputs in [0, 4096]
     if (num == MLPV_NUM_Q4_12) xmax = l == 0 ? 4096.0 : (act == MLPV_ACT_PL_SIGMOID ? 4096.0 : 32767.0);
@@ -160,6 +162,16 @@ extern "C" mlpv_status mlpv_create(const mlpv_net* net, const mlpv_quant* quant,
         if (!std::isfinite(w)) return fail(nullptr, MLPV_E_INVALID, "net.W[%d][%d][%d] is not finite", l, i, j);
         s += std::fabs(w);
       }
+      if (num == MLPV_NUM_BF16 && l + 1 < L) {
+        // hidden activations (and their base differences) travel as fp16 hi + lo into the next
+        // tensor-core layer: the worst case sum |w| x_max + |b| must stay below the fp16 range
+        // (inputs in [0, 1]; later layers bounded by this layer's bound, below)
+        const double bb = std::fabs((double)static_cast<const float*>(net->b[l])[i]);
+        if (s * hbound + bb >= 32768.0)
+          return fail(nullptr, MLPV_E_UNSUPPORTED, "BF16 layer %d neuron %d: worst-case |potential| %.0f exceeds the fp16 "
+                      "carrier range of the tensor-core path", l + 1, i, s * hbound + bb);
+        nbound = std::max(nbound, s * hbound + bb);
+      }
       if (is_fixed(num)) {
         const double bb = std::fabs((double)static_cast<const int32_t*>(net->b[l])[i]);
         if (s * xmax + bb >= 1073741824.0)
@@ -168,6 +180,7 @@ extern "C" mlpv_status mlpv_create(const mlpv_net* net, const mlpv_quant* quant,
         return fail(nullptr, MLPV_E_INVALID, "net.b[%d][%d] is not finite", l, i);
       }
     }
+    hbound = nbound;
   }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(nullptr, MLPV_E_CUDA, "no CUDA device");
@@ -317,6 +330,9 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
     case MLPV_PERT_TUPLE_REPLACE:
       if (p->tuple != 1 && p->tuple != 2) return fail(h, MLPV_E_INVALID, "pert.tuple = %d (1 or 2)", p->tuple);
       if (p->tuple == 2 && n.sizes[0] < 2) return fail(h, MLPV_E_SHAPE, "pert.tuple = 2 needs n_0 >= 2");
+      // the kernels rank pixel pairs in 32 bits
+      if (p->tuple == 2 && (uint64_t)n.sizes[0] * (uint64_t)(n.sizes[0] - 1) / 2 >= (1ull << 32))
+        return fail(h, MLPV_E_UNSUPPORTED, "pert.tuple = 2 with n_0 = %d: more than 2^32 pixel pairs", n.sizes[0]);
       if (num == MLPV_NUM_BF16) return fail(h, MLPV_E_UNSUPPORTED, "TUPLE_REPLACE with BF16 is not built (use PHILOX_LATTICE)");
       break;
     case MLPV_PERT_SUBSET_OFFSET:
@@ -415,7 +431,9 @@ static mlpv_status build_pert(mlpv_ctx* h, const mlpv_pert* p, DevPert* dp, bool
         if (!std::isfinite(v)) return fail(h, MLPV_E_INVALID, "pert.levels[%d] is not finite", q);
       } else if (p->kind != MLPV_PERT_SUBSET_OFFSET) {
         const int v = static_cast<const int16_t*>(p->levels)[q];
-        const int hi = num == MLPV_NUM_Q4_12 ? 32767 : 255, lo = num == MLPV_NUM_Q4_12 ? -32768 : 0;
+        // replacement values lie in the input domain: Q4.12 images are normalised (PAPER.md:412,
+        // reading C16: raw [0, 4096]; the create-time accumulator bound assumes it), u8 [0, 255]
+        const int hi = num == MLPV_NUM_Q4_12 ? 4096 : 255, lo = 0;
         if (v < lo || v > hi) return fail(h, MLPV_E_INVALID, "pert.levels[%d] = %d outside the input range", q, v);
       }
     }
@@ -869,6 +887,9 @@ extern "C" mlpv_status mlpv_sync(mlpv_t h, void* stream) {
   CUDA_TRY(h, cudaMemcpy(&st, h->dev_status, 4, cudaMemcpyDeviceToHost), "status read");
   if (st != 0) {
     CUDA_TRY(h, cudaMemset(h->dev_status, 0, 4), "status reset");
+    if (st & kStatusQ412Base)
+      return fail(h, MLPV_E_INVALID, "Q4_12: a base input pixel is outside the normalised raw range [0, 4096] "
+                                     "(reading C16; the accumulator bound of mlpv_create assumes it); results not exact");
     if (st & kStatusClampBase)
       return fail(h, MLPV_E_INVALID, "PHILOX_CLAMP: a base pixel is outside [0, 1] or its binding clamp bound is not "
                                      "exactly representable at the contraction scale (mlpv.h); those results are not exact");

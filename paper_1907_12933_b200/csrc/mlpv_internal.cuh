@@ -94,6 +94,7 @@ struct BaseWS {
 };
 // bits of the device status word (mlpv_sync reports them)
 constexpr uint32_t kStatusClampBase = 1u;      // a PHILOX_CLAMP base pixel outside [0, 1] or not fp16-exact
+constexpr uint32_t kStatusQ412Base = 2u;       // a Q4.12 base pixel outside [0, 4096]
 
 // Launchers (kernels in k_small.cu / k_large.cu / k_util.cu)
 cudaError_t launch_base_prologue(const DevNet& net, const void* bases, int n_base, const DevPert& pert,

@@ -66,6 +66,12 @@ def test_create_validation_is_synchronous(P):
     nan = M.configs.Net([2, 2], M.ACT_RELU, M.NUM_FP32, [np.array([[1, np.nan], [0, 0]], np.float32)], [np.zeros(2, np.float32)])
     s, msg = _create(P, nan)
     assert s == 1 and "finite" in msg
+    # BF16: hidden activations travel as fp16 hi / lo; a net whose worst case leaves that range
+    big = M.configs.Net([64, 8, 2], M.ACT_RELU, M.NUM_BF16,
+                        [M.f32_to_bf16_bits(np.full((8, 64), 600.0, np.float32)), np.zeros((2, 8), np.uint16)],
+                        [np.zeros(8, np.float32), np.zeros(2, np.float32)])
+    s, msg = _create(P, big)
+    assert s == 3 and "fp16" in msg
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg4_box", "cfg5_int8"])

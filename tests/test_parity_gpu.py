@@ -271,9 +271,40 @@ def test_restriction_gpu(P, oracle_mod):
     assert_fixed_parity(g, oracle_mod.check(cfg))
 
 
-def test_restriction_rejected_on_philox(P):
+def test_incremental_rejected_on_philox(P):
+    """Incremental bounds (NEXT-2) are built for the enumerated spaces; the Philox spaces say so."""
+    import torch
     cfg = M.make_config("cfg4").subset(n_base=1, begin=0, end=10)
-    cfg.pert.restrict_l2 = 0.5
     with pytest.raises(P.MlpvError) as e:
-        run_gpu(P.Checker(cfg.net), cfg)
+        P.Checker(cfg.net).check_incremental(to_device_bases(cfg), cfg.pert, cfg.prop, cfg.cov, gamma=0.5, max_bound=4)
     assert e.value.status == 3
+
+
+def test_device_found_input_errors(P):
+    """Input rules that hold for device-resident data are checked on the device and reported by
+    mlpv_sync (MLPV_E_INVALID): a Q4.12 base pixel outside [0, 4096] (reading C16), a PHILOX_CLAMP
+    base pixel that breaks the exact-contraction rule of mlpv.h.  Replace levels outside the input
+    domain are rejected synchronously."""
+    import torch
+    cfg = M.make_config("cfg2").subset(n_base=2, begin=0, end=1000)
+    chk = P.Checker(cfg.net)
+    bad = cfg.bases.copy()
+    bad[1, 3] = 5000
+    chk.check(torch.from_numpy(bad).cuda(), cfg.pert, cfg.prop, cfg.cov)
+    with pytest.raises(P.MlpvError) as ei:
+        chk.sync()
+    assert ei.value.status == 1 and "4096" in str(ei.value)
+    chk.check(torch.from_numpy(cfg.bases).cuda(), cfg.pert, cfg.prop, cfg.cov)
+    chk.sync()                                              # the status was cleared
+    rep = M.Pert(M.PERT_SUBSET_REPLACE, pixels=cfg.pert.pixels, levels=np.array([0, 4097], np.int16), index_end=2)
+    with pytest.raises(P.MlpvError) as ei:
+        chk.check(torch.from_numpy(cfg.bases).cuda(), rep, cfg.prop, cfg.cov)
+    assert ei.value.status == 1
+    c4 = M.make_config("cfg4").subset(n_base=1, begin=0, end=300)
+    chk4 = P.Checker(c4.net)
+    b4 = c4.bases.copy()
+    b4[0, 5] = M.f32_to_bf16_bits(np.array([1e-7], np.float32))[0]   # 0 < x < 2^-16: -x / 2 is not an fp16 value
+    chk4.check(to_device_bases(M.Config("x", "", c4.net, b4, c4.pert, c4.prop, c4.cov)), c4.pert, c4.prop, c4.cov)
+    with pytest.raises(P.MlpvError) as ei:
+        chk4.sync()
+    assert ei.value.status == 1 and "PHILOX_CLAMP" in str(ei.value)
