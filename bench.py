@@ -156,11 +156,51 @@ def cpu_baseline(cfg, budget_s=12.0):
     m = int(max(8, min(cfg.space, budget_s * rate / nb)))
     s = cfg.subset(n_base=nb, begin=0, end=m)
     t0 = time.perf_counter()
-    O.check(s, nthreads=cores)
+    ores = O.check(s, nthreads=cores)
     dt = time.perf_counter() - t0
     n = nb * m
-    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{cfg.name}: bases 0-{nb - 1} x indices [0, {m}) = {n} candidates in {dt:.1f} s"}
+    out = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{cfg.name}: bases 0-{nb - 1} x indices [0, {m}) = {n} candidates in {dt:.1f} s"}
+    return out, s, ores
+
+
+def sample_parity(chk, s, o):
+    """The GPU on exactly the oracle's timed sample, compared by the parity rules:
+    fixed point bit-exact (counts, counterexamples, every coverage bit); float by reading C20
+    (violation counts within the flagged counts, first counterexamples bracketing each other's
+    unflagged ones, certain coverage contained in the other side's coverage).  The oracle's tau
+    (C20) is the GPU's (both from the sample's base traces)."""
+    import numpy as np
+    import torch
+    import mlpv_inputs as M
+    import paper_1907_12933_b200 as P
+    bases = to_device(s.bases, "cuda")
+    r = chk.check(bases, s.pert, s.prop, s.cov)
+    chk.sync()
+    torch.cuda.synchronize()
+    g = P.result_to_numpy(r, s.n_base, r["n_words"])
+    bad = []
+    if s.net.numeric in (M.NUM_Q4_12, M.NUM_INT8):
+        for k in ("checked", "violated", "first_cex"):
+            if not np.array_equal(g[k], getattr(o, k)):
+                bad.append(k)
+        if not np.array_equal(g["cov_all"], o.cov_all):
+            bad.append("cov_all")
+        rule = "bit-exact"
+    else:
+        if not np.array_equal(g["checked"], o.checked):
+            bad.append("checked")
+        vg, vo = g["violated"].astype(np.int64), o.violated.astype(np.int64)
+        if not np.all(np.abs(vg - vo) <= np.minimum(g["flagged"], o.flagged).astype(np.int64)):
+            bad.append("violated")
+        if not (np.all(g["first_cex"] <= o.first_cex_unflagged) and np.all(o.first_cex <= g["first_cex_unflagged"])):
+            bad.append("first_cex")
+        if (o.cov_certain & ~g["cov_all"]).any() or (g["cov_certain"] & ~o.cov_all).any():
+            bad.append("coverage")
+        rule = "C20 float rules"
+    return {"status": "ok" if not bad else "FAILED", "rule": rule, "mismatch": bad,
+            "violated_gpu": int(g["violated"].sum()), "violated_oracle": int(o.violated.sum()),
+            "coverage_bits_gpu": int(np.unpackbits(g["cov_all"].view(np.uint8)).sum())}
 
 
 def run_reference(args):
@@ -174,7 +214,7 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     nb = min(16, cfg.n_base)
     # size each step to ~10 s of oracle work so the whole run stays within a few minutes
-    cal = cpu_baseline(cfg, budget_s=3.0)
+    cal, _, _ = cpu_baseline(cfg, budget_s=3.0)
     per_step = int(max(8, min(cfg.space, 10.0 * cal["value"] / nb)))
     times = []
     for k in range(args.warmup + args.steps):
@@ -348,9 +388,11 @@ def main():
                 "alg_ops_per_candidate": ops, "candidates_per_launch": per_launch}
 
     if rank == 0:
-        cpu = None
+        cpu = par = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cfg)
+            cpu, sample, ores = cpu_baseline(cfg)
+            par = sample_parity(chk, sample, ores)
+            par["sample"] = cpu["sample"]
         S = samples_for(cfg, args)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -362,7 +404,11 @@ def main():
                            "parallelism": f"dp{world} (index-space shards, one all-gather per step)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk}
+        if par is not None:
+            line["parity"] = par
         print(json.dumps(line), flush=True)
+        if par is not None and par["status"] != "ok":
+            raise SystemExit(f"bench: GPU / oracle parity FAILED on the timed sample: {par}")
     if world > 1:
         dist.destroy_process_group()
 
