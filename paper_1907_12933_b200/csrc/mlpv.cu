@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -565,8 +566,13 @@ static mlpv_status run_kernel(mlpv_ctx* h, const void* bases, int n_base, const 
     if (!supported) return fail(h, MLPV_E_UNSUPPORTED, "large-net kernel: %s", why.c_str());
   } else {
     dp.levels = plan.levels_dev;
-    e = launch_small(h->net, bases, n_base, dp, dprop, dc, dr, plan.ws, eval_idx, eval_n, eval_base, eval_out,
-                     h->num_sms, st, &supported);
+    supported = false;
+    e = cudaSuccess;
+    if (!eval_idx && !getenv("MLPV_NO_WARP3"))          // small int8 nets: one warp per candidate (k_warp)
+      e = launch_warp3(h->net, n_base, dp, dprop, dc, dr, plan.ws, h->num_sms, st, &supported);
+    if (!supported)
+      e = launch_small(h->net, bases, n_base, dp, dprop, dc, dr, plan.ws, eval_idx, eval_n, eval_base, eval_out,
+                       h->num_sms, st, &supported);
     if (!supported) return fail(h, MLPV_E_UNSUPPORTED, "no small-net kernel for this shape / numeric (L=%d, widths %d,%d,%d)",
                                 h->net.L, h->net.sizes[1], h->net.L > 1 ? h->net.sizes[2] : 0, h->net.L > 2 ? h->net.sizes[3] : 0);
   }

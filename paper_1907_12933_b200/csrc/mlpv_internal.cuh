@@ -103,6 +103,8 @@ cudaError_t launch_small(const DevNet& net, const void* bases, int n_base, const
                          const DevProp& prop, const DevCov& cov, const DevResult& res, BaseWS ws,
                          const uint64_t* eval_idx, int64_t eval_n, int eval_base, void* eval_out,
                          int num_sms, cudaStream_t st, bool* supported);
+cudaError_t launch_warp3(const DevNet& net, int n_base, const DevPert& pert, const DevProp& prop, const DevCov& cov,
+                         const DevResult& res, BaseWS ws, int num_sms, cudaStream_t st, bool* supported);
 cudaError_t launch_init_result(const DevResult& r, int n_base, uint32_t n_words, cudaStream_t st);
 constexpr int kMaxParts = 64;
 struct MergeParts { DevResult p[kMaxParts]; };
