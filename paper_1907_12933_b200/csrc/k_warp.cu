@@ -34,10 +34,6 @@ __device__ __forceinline__ int32_t dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, int
   asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_u8x4), "r"(b_s8x4), "r"(c));
   return d;
 }
-__device__ __forceinline__ int32_t requant(int32_t acc, int sh) {     // reading C18 (ReLU + requant)
-  const int32_t r = sh > 0 ? (1 << (sh - 1)) : 0;
-  return max(0, min(255, (acc + r) >> sh));
-}
 __device__ __forceinline__ uint32_t iabs_u(int32_t d) { return (uint32_t)(d < 0 ? -d : d); }
 
 struct Args {
@@ -49,7 +45,10 @@ struct Args {
   BaseWS ws;
 };
 
-__global__ void __launch_bounds__(32 * kWarps) k_warp3(const __grid_constant__ Args a) {
+// FULL: n1 = 64, n2 = 32 (config 3's shape): every lane owns real neurons in layers 1 and 2, no
+// per-lane predicates there
+template <bool FULL>
+__global__ void __launch_bounds__(32 * kWarps, 3) k_warp3(const __grid_constant__ Args a) {
   __shared__ uint32_t s_cov[256];
   __shared__ __align__(16) uint8_t s_h[kWarps][2][96];                // [warp][buffer] h1 (64) | h2 (32)
   __shared__ unsigned long long s_cnt[2], s_cex;
@@ -86,7 +85,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_warp3(const __grid_constant__ A
   const int32_t b2 = lane < n2 ? static_cast<const int32_t*>(net.b[1])[lane] : 0;
   const int32_t b3 = lane < n3 ? static_cast<const int32_t*>(net.b[2])[lane] : 0;
   const int32_t* tr = static_cast<const int32_t*>(a.ws.trace) + (size_t)b * T;
-  const bool in1a = lane < n1, in1b = lane + 32 < n1, in2 = lane < n2, in3 = lane < n3;
+  const bool in1a = FULL || lane < n1, in1b = FULL || lane + 32 < n1, in2 = FULL || lane < n2, in3 = lane < n3;
   const int32_t ub1a = in1a ? tr[net.loff[1] + lane] : 0, ub1b = in1b ? tr[net.loff[1] + lane + 32] : 0;
   const int32_t ub2 = in2 ? tr[net.loff[2] + lane] : 0, ub3 = in3 ? tr[net.loff[3] + lane] : 0;
   const uint32_t m1a = __ballot_sync(0xffffffffu, in1a), m1b = __ballot_sync(0xffffffffu, in1b);
@@ -102,6 +101,12 @@ __global__ void __launch_bounds__(32 * kWarps) k_warp3(const __grid_constant__ A
   const int32_t tg2 = (int32_t)a.cov.tg_i[1], tg3 = (int32_t)a.cov.tg_i[2];
   const uint32_t th1 = (uint32_t)a.cov.th_i[0], th2 = (uint32_t)a.cov.th_i[1];
   const int K = a.pert.n_pixels, q = a.pert.n_levels;
+  // the property, hoisted (kind 0: argmax unchanged, 1: target never, 2/3: the literal, C12)
+  const int pkind = a.prop.kind, ptarget = a.prop.target;
+  const int32_t pV = (int32_t)a.prop.V_i;
+  const int pD = ptarget >= 0 ? ptarget : base_cls;
+  const uint32_t pothers = m3 & ~(1u << (pD & 31));
+  const int32_t r1 = sh1 > 0 ? (1 << (sh1 - 1)) : 0, r2 = sh2 > 0 ? (1 << (sh2 - 1)) : 0;
   const int32_t* delta = static_cast<const int32_t*>(a.ws.delta) + (size_t)b * K * q * n1;
   __syncthreads();
 
@@ -127,62 +132,62 @@ __global__ void __launch_bounds__(32 * kWarps) k_warp3(const __grid_constant__ A
       }
     };
     prefix();
-    for (uint64_t c = c0; c < c1; c++) {
+    const int32_t* last = delta + (size_t)(K - 1) * q * n1;   // rows of the last digit
+    const int ncand = (int)(c1 - c0);
+    for (int i = 0; i < ncand; i++) {
       // ---- layer 1: one table row for the last digit
-      const int32_t* row = delta + ((size_t)(K - 1) * q + dl) * n1;
+      const int32_t* row = last + dl * n1;
       const int32_t u1a = in1a ? pa + __ldg(row + lane) : 0, u1b = in1b ? pb + __ldg(row + lane + 32) : 0;
-      if (++dl == q) { dl = 0; hi++; if (c + 1 < c1) prefix(); }
+      if (++dl == q) { dl = 0; hi++; if (i + 1 < ncand) prefix(); }
       const uint32_t sc1a = (__ballot_sync(0xffffffffu, u1a >= 0) & m1a) ^ sb1a;
       const uint32_t sc1b = (__ballot_sync(0xffffffffu, u1b >= 0) & m1b) ^ sb1b;
       const int nsc1 = __popc(sc1a) + __popc(sc1b);
       // ---- layer 2 (DP4A against the lane's W2 row; h1 broadcast through shared memory)
       uint8_t* hb = s_h[warp][buf];
       buf ^= 1;
-      hb[lane] = (uint8_t)(in1a ? requant(u1a, sh1) : 0);
-      hb[32 + lane] = (uint8_t)(in1b ? requant(u1b, sh1) : 0);
+      hb[lane] = (uint8_t)(in1a ? max(0, min(255, (u1a + r1) >> sh1)) : 0);      // requant, reading C18
+      hb[32 + lane] = (uint8_t)(in1b ? max(0, min(255, (u1b + r1) >> sh1)) : 0);
       __syncwarp();
       const uint4* h4 = reinterpret_cast<const uint4*>(hb);
-      int32_t u2 = b2;
+      int32_t acc2[4] = {b2, 0, 0, 0};                  // four independent DP4A chains
 #pragma unroll
       for (int m4 = 0; m4 < 4; m4++) {
         const uint4 w = h4[m4];
-        u2 = dp4a_us(w.x, W2r[4 * m4], u2);
-        u2 = dp4a_us(w.y, W2r[4 * m4 + 1], u2);
-        u2 = dp4a_us(w.z, W2r[4 * m4 + 2], u2);
-        u2 = dp4a_us(w.w, W2r[4 * m4 + 3], u2);
+        acc2[0] = dp4a_us(w.x, W2r[4 * m4], acc2[0]);
+        acc2[1] = dp4a_us(w.y, W2r[4 * m4 + 1], acc2[1]);
+        acc2[2] = dp4a_us(w.z, W2r[4 * m4 + 2], acc2[2]);
+        acc2[3] = dp4a_us(w.w, W2r[4 * m4 + 3], acc2[3]);
       }
+      int32_t u2 = (acc2[0] + acc2[1]) + (acc2[2] + acc2[3]);
       if (!in2) u2 = 0;
       const uint32_t sc2 = (__ballot_sync(0xffffffffu, u2 >= 0) & m2) ^ sb2;
       const int nsc2 = __popc(sc2);
       // ---- layer 3
-      hb[64 + lane] = (uint8_t)(in2 ? requant(u2, sh2) : 0);
+      hb[64 + lane] = (uint8_t)(in2 ? max(0, min(255, (u2 + r2) >> sh2)) : 0);
       __syncwarp();
-      int32_t u3 = b3;
+      int32_t acc3[4] = {b3, 0, 0, 0};
 #pragma unroll
       for (int m4 = 0; m4 < 2; m4++) {
         const uint4 w = h4[4 + m4];
-        u3 = dp4a_us(w.x, W3r[4 * m4], u3);
-        u3 = dp4a_us(w.y, W3r[4 * m4 + 1], u3);
-        u3 = dp4a_us(w.z, W3r[4 * m4 + 2], u3);
-        u3 = dp4a_us(w.w, W3r[4 * m4 + 3], u3);
+        acc3[0] = dp4a_us(w.x, W3r[4 * m4], acc3[0]);
+        acc3[1] = dp4a_us(w.y, W3r[4 * m4 + 1], acc3[1]);
+        acc3[2] = dp4a_us(w.z, W3r[4 * m4 + 2], acc3[2]);
+        acc3[3] = dp4a_us(w.w, W3r[4 * m4 + 3], acc3[3]);
       }
+      int32_t u3 = (acc3[0] + acc3[1]) + (acc3[2] + acc3[3]);
       if (!in3) u3 = 0;
       // ---- a7: argmax (lowest index on ties), property
       const int32_t top = __reduce_max_sync(0xffffffffu, in3 ? u3 : INT32_MIN);
       const int cls = __ffs(__ballot_sync(0xffffffffu, in3 && u3 == top)) - 1;
       bool viol;
-      if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
-        const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
-        const int32_t V = (int32_t)a.prop.V_i;
-        const int32_t yD = __shfl_sync(0xffffffffu, u3, D);
-        const uint32_t gt = __ballot_sync(0xffffffffu, in3 && lane != D && u3 > V);
-        const uint32_t others = m3 & ~(1u << D);
-        viol = yD < V && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? gt == others : gt != 0);
+      if (pkind == MLPV_PROP_THRESHOLD_LITERAL || pkind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
+        const int32_t yD = __shfl_sync(0xffffffffu, u3, pD);
+        const uint32_t gt = __ballot_sync(0xffffffffu, in3 && lane != pD && u3 > pV);
+        viol = yD < pV && (pkind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? gt == pothers : gt != 0);
       } else {
-        viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != base_cls;
+        viol = pkind == MLPV_PROP_TARGET_NEVER ? cls == ptarget : cls != base_cls;
       }
-      my_chk++;
-      if (viol) { my_v++; if (c < my_cex) my_cex = c; }
+      if (viol) { my_v++; if (c0 + (uint64_t)i < my_cex) my_cex = c0 + (uint64_t)i; }
       // ---- a8: covers of pairs (1, 2) and (2, 3) (reading C3-C8), rare, warp-uniform branches
       if (p12 >= 0 && nsc1 <= 1) {
         bool cond = nsc1 == 1;
@@ -227,6 +232,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_warp3(const __grid_constant__ A
         }
       }
     }
+    my_chk += (unsigned long long)ncand;
   }
   // ---- a9: block then global reductions (every lane of a warp holds the same counts)
   if (lane == 0) {
@@ -262,11 +268,13 @@ cudaError_t launch_warp3(const DevNet& net, int n_base, const DevPert& pert, con
   const uint64_t len = pert.end - pert.begin;
   const uint64_t nchunk = (len + kw::kChunk - 1) / kw::kChunk;
   // ~8 resident blocks per SM overall (registers: ~64 per thread)
-  uint64_t gx = (uint64_t)(8 * num_sms + n_base - 1) / (uint64_t)n_base;
+  uint64_t gx = (uint64_t)(12 * num_sms + n_base - 1) / (uint64_t)n_base;
   const uint64_t need = (nchunk + kw::kWarps - 1) / kw::kWarps;
   if (gx > need) gx = need;
   if (gx < 1) gx = 1;
-  kw::k_warp3<<<dim3((unsigned)gx, (unsigned)n_base), 32 * kw::kWarps, 0, st>>>(a);
+  // ~12 resident blocks per SM overall (3 per SM by the launch bounds)
+  if (net.sizes[1] == 64 && net.sizes[2] == 32) kw::k_warp3<true><<<dim3((unsigned)gx, (unsigned)n_base), 32 * kw::kWarps, 0, st>>>(a);
+  else kw::k_warp3<false><<<dim3((unsigned)gx, (unsigned)n_base), 32 * kw::kWarps, 0, st>>>(a);
   return cudaGetLastError();
 }
 
