@@ -110,7 +110,15 @@ constexpr int kMaxN0 = 1024;
 // (20 idle / trace observer, 21 weight producer, 23 MMA issuer for all three layers / TMEM owner),
 // 12-19 epilogue team (E1, E2, E3 -- on the tile's critical path; two warps per TMEM lane quadrant),
 // 0-11 generator (throughput work with a six-stage ring of slack; one warpgroup per stage group).
+#if MLPV_EXP == 31
+constexpr int kNGenGroups = 2, kWE = 12, kWIdle = 20, kWProd = 21, kWIss = 23;   // timing experiment: warps 8-11 idle
+#else
 constexpr int kNGenGroups = 3, kWE = 12, kWIdle = 20, kWProd = 21, kWIss = 23;   // warp 22: spare
+#endif
+// (Measured and kept: three generator groups.  Two groups keep up as well (MLPV_EXP 31, same tile
+// period); a 2-generator / 3-epilogue-warpgroup variant with 3-way row exchanges (E1 on three
+// warps per quadrant) ran 0.7 % slower: E1's pieces took proportionally longer per warp -- the step
+// is bound by the SMSPs' shared issue / TMEM traffic, not by the warp count.)
 __host__ __device__ constexpr int gen_index(int warp) { return warp; }
 // setmaxnreg only redistributes the CTA's launch allocation (768 threads x kRegLaunch, checked at
 // launch): 3 generator + 2 epilogue + 1 control warpgroups must fit in 6 x kRegLaunch per thread.
@@ -669,6 +677,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     // block of its 32 rows (two Philox calls) into registers before it waits for the slot.  The A
     // operand is the level l of every pixel (reading C14b: x' = x + origin + l * step, linear in l);
     // the base image enters through base1 in the epilogue.
+    if ((gen_index(warp) >> 2) < kNGenGroups) {          // (MLPV_EXP 31: fewer generator groups)
     const int gw = gen_index(warp), grp = gw >> 2;
     const int r = 32 * (gw & 3) + lane;                    // row of this CTA's A tile
     const int gt = 32 * gw + lane;                         // 0..383
@@ -769,6 +778,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         TRG(tl, kb, 4);
       }
       if (gt == 0) TR(tl, 7);
+    }
     }
   }
   } else {

@@ -107,19 +107,19 @@ for team, nm in ((0, "E1"), (1, "E2")):
         r = ep[team, k]
         print(f"{nm} tile {8 + k}: passA {r[1] - r[0]}  kb signals " + " ".join(str(r[2 + j] - r[0]) for j in range(4)))
 
-e2 = np.zeros((2, 8, 2, 8), np.uint64)
+e2 = np.zeros((2, 12, 2, 8), np.uint64)
 assert P.lib().mlpv_f3_trace_e2_read(e2.ctypes.data_as(C.c_void_p)) == 0
 e2 = e2.astype(np.int64)
 t0 = {team: e2[0, 0, team, 0] for team in (0, 1)}
 for team, nm in ((0, "E1"), (1, "E2")):
     print(f"{nm} tile 9 per warp (relative to rank 0 warp 0 start): start, signs, kb0..kb3 signals, end")
     for rk in range(2):
-        for w in range(8):
+        for w in range(12):
             r = e2[rk, w, team]
             rel = lambda x: str(int(x - t0[team])) if x else "-"
             print(f"  rank {rk} warp {w}: start {rel(r[0])} signs {rel(r[1])} kb " + " ".join(rel(r[2 + j]) for j in range(4)) + f" end {rel(r[6])}")
 
-gp = np.zeros((8, 8, 5), np.uint64)
+gp = np.zeros((12, 8, 5), np.uint64)
 assert P.lib().mlpv_f3_trace_grp_read(gp.ctypes.data_as(C.c_void_p)) == 0
 gp = gp.astype(np.int64)
 print("E2 pass B per group (rank 0, tile 9): stats / split / stores+signal / ld wait / to next top")
@@ -131,12 +131,12 @@ for w in range(8):
         row.append(f"{e[1]-e[0]}/{e[2]-e[1]}/{e[3]-e[2]}/{e[4]-e[3]}/{nxt-e[4]}")
     print(f"  warp {w} (q{w & 3} h{w >> 2}): " + "  ".join(row))
 
-e1 = np.zeros((2, 8, 5, 4), np.uint64)
+e1 = np.zeros((2, 12, 5, 4), np.uint64)
 assert P.lib().mlpv_f3_trace_e1p_read(e1.ctypes.data_as(C.c_void_p)) == 0
 e1 = e1.astype(np.int64)
 print("E1 per piece (tile 9): ld latency / compute / sign-off (st wait + fence + arrive) / gap to next piece")
 for rk in range(2):
-    for w in range(8):
+    for w in range(12):
         row = []
         for i in range(5):
             e = e1[rk, w, i]
