@@ -174,7 +174,7 @@ struct Args {
 struct alignas(16) Smem {
   uint64_t g_full[kSG], g_empty[kSG], w_full[kSW], w_empty[kSW];
   uint64_t acc1_full, acc2_full, acc3_full, acc2_free;
-  uint64_t h1_kb[kNkb2];
+  uint64_t h1_pc[2 * kNkb2];                 // E1 pieces (32 neurons) handed to layer 2
   uint64_t h2_kb[kNkb2];
   uint32_t tbase;
   int base_e;
@@ -438,7 +438,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     for (int i = 0; i < kSW; i++) { mbar_init(&S.w_full[i], two); mbar_init(&S.w_empty[i], 1); }
     mbar_init(&S.acc1_full, 1); mbar_init(&S.acc2_full, 1); mbar_init(&S.acc3_full, 1);
     mbar_init(&S.acc2_free, 8);
-    for (int i = 0; i < kNkb2; i++) mbar_init(&S.h1_kb[i], 16);
+    for (int i = 0; i < 2 * kNkb2; i++) mbar_init(&S.h1_pc[i], 8);    // 4 warps x 2 CTAs
     for (int i = 0; i < kNkb2; i++) mbar_init(&S.h2_kb[i], i ? 8 : 16);   // block 0 also waits for group 15's read
     S.base_e = -1;
     fence_mbar_init();
@@ -623,7 +623,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         TR(tl, 4);
         fence_after();                                      // the bias needs only R2, not H1
         if (el) mma2_f16_ss(R2, sdesc_none(smem_u32(sOnes), 128, 256), sdesc_none(smem_u32(sB2), 128, 256), id2, 0u);
-        mbar_wait_sleep(&S.h1_kb[0], tl & 1u, 32);
+        mbar_wait_sleep(&S.h1_pc[0], tl & 1u, 32);
         TR(tl, 3);
         mbar_wait(&S.w_full[wslot], wph);
         for (int kb = 0; kb < kNkb2; kb++) {
@@ -640,9 +640,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
               mma2_f16_ts(R2, R1 + col + 8u, bd, id2, 1u);
             }
             if (kk == 0) flush();
-            if (kk == 1) {
+            // H1 arrives in 32-neuron pieces (K steps 2 per piece): wait for each piece just before
+            // its K steps, so layer 2 starts one piece after E1 does
+            if (kk == 1) mbar_wait_sleep(&S.h1_pc[2 * kb + 1], tl & 1u, 32);
+            if (kk == 3) {
               if (kb + 1 < kNkb2) {
-                mbar_wait_sleep(&S.h1_kb[kb + 1], tl & 1u, 32);
+                mbar_wait_sleep(&S.h1_pc[2 * kb + 2], tl & 1u, 32);
                 mbar_wait(&S.w_full[wslot], wph);
               } else if (t + 1 < t_end) {
                 wait_l1();                                  // the next tile's first layer-1 stage
@@ -931,7 +934,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           tmem_st_wait();
           fence_before();
           __syncwarp();
-          if (lane == 0) arrive_leader(&S.h1_kb[kbs], rank);
+          if (lane == 0) arrive_leader(&S.h1_pc[p], rank);
           TRE(0, tl, 2 + kbs);
           TRE2(tl, 0, 2 + kbs);
         }
