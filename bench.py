@@ -58,6 +58,20 @@ def alg_ops_per_candidate(cfg):
     return 2 * (changed * s[1] + dense_rest)
 
 
+def kernel_name(cfg):
+    """The enumeration kernel mlpv_check launches for this config (the dominant kernel)."""
+    import mlpv_inputs as M
+    s = cfg.net.sizes
+    if cfg.pert.kind in (4, 5) and len(s) == 4 and s[1] == 256 and s[2] == 256 and s[0] % 2 == 0 and s[0] <= 1024:
+        return "k_fused3"
+    if cfg.pert.kind in (3, 4, 5):
+        return "k_large"
+    if (cfg.net.numeric == M.NUM_INT8 and len(s) == 4 and s[1] <= 64 and s[2] <= 32 and s[3] <= 32
+            and cfg.pert.kind in (1, 2) and len(cfg.pert.pixels) >= 2):
+        return "k_warp3"
+    return "k_small"
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -383,7 +397,7 @@ def main():
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get(cfg.name)
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                "traffic": traffic, "kernel": ("k_fused3" if cfg.pert.kind in (4, 5) else "k_large") if cfg.pert.kind in (3, 4, 5) else "k_small",
+                "traffic": traffic, "kernel": kernel_name(cfg),
                 "kernel_ms": 1e3 * kern_avg_s, "peak_source": peak_note,
                 "alg_ops_per_candidate": ops, "candidates_per_launch": per_launch}
 
