@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 METRIC = "perturbations verified/sec (whole box) at 1/2/4/8 B200; % of roofline"
 UNIT = "perturbations/s"
 DEFAULT_SAMPLES = {"cfg1": None, "cfg2": None, "cfg3": 1 << 20, "cfg4": 1 << 16, "cfg4_box": 1 << 16,
-                   "cfg5_bf16": 1 << 10, "cfg5_int8": 1 << 11}
+                   "cfg5_bf16": 1 << 12, "cfg5_int8": 1 << 12}
 DTYPE = {"cfg1": "fp32", "cfg2": "q4.12", "cfg3": "int8", "cfg4": "bf16", "cfg4_box": "bf16", "cfg5_bf16": "bf16",
          "cfg5_int8": "int8"}
 

@@ -219,7 +219,22 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
         }
       } else {
         double acc = 0.0;
-        for (int j = lane; j < fan; j += 32) acc += (double)wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hf[j];
+        if (net.numeric == MLPV_NUM_BF16 && (fan & 7) == 0) {        // 8 bf16 weights per 16-byte load
+          const uint4* wr = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(net.W[l - 1]) + (size_t)i * fan);
+          for (int qq = lane; qq < (fan >> 3); qq += 32) {
+            const uint4 w8 = __ldg(wr + qq);
+            const uint32_t wq[4] = {w8.x, w8.y, w8.z, w8.w};
+            const double2* h2 = reinterpret_cast<const double2*>(hf + 8 * qq);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const double2 hh = h2[k];
+              acc += (double)__uint_as_float(wq[k] << 16) * hh.x;
+              acc += (double)__uint_as_float(wq[k] & 0xFFFF0000u) * hh.y;
+            }
+          }
+        } else {
+          for (int j = lane; j < fan; j += 32) acc += (double)wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hf[j];
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
