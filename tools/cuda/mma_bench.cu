@@ -42,20 +42,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
     } else reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0, 0);
   }
   if (t == 0) {
-    mbar_init(&ready, (MODE != 3 && rank == 0) ? 2 : 1); mbar_init(&done, 1);
+    mbar_init(&ready, (!(MODE == 3 || MODE == 31) && rank == 0) ? 2 : 1); mbar_init(&done, 1);
     for (int i = 0; i < 4; i++) mbar_init(&scratch[i], 1);
     mbar_init(&pre, 1);
     fence_mbar_init();
   }
-  if (w == 0) { if (MODE == 3) { tmem_alloc(&tbase, 512); tmem_relinquish(); } else { tmem_alloc2(&tbase, 512); tmem_relinquish2(); } }
+  if (w == 0) { if ((MODE == 3 || MODE == 31)) { tmem_alloc(&tbase, 512); tmem_relinquish(); } else { tmem_alloc2(&tbase, 512); tmem_relinquish2(); } }
   fence_proxy_async();
   fence_before();
   cluster_sync();
   fence_after();
   const uint32_t tb = tbase;
-  if (t == 0) { if (rank == 0 || MODE == 3) mbar_arrive(&ready); else mbar_arrive_cluster(&ready, 0); }
+  if (t == 0) { if (rank == 0 || (MODE == 3 || MODE == 31)) mbar_arrive(&ready); else mbar_arrive_cluster(&ready, 0); }
   if (t == 0) mbar_arrive(&pre);                       // phase 0 of `pre` completes: waits on it are no-ops
-  const bool issuer = (MODE == 3) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15 && MODE != 25 && MODE != 27);
+  const bool issuer = ((MODE == 3 || MODE == 31)) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15 && MODE != 25 && MODE != 27);
   __shared__ volatile int stop;
   if (t == 0) stop = 0;
   __syncthreads();
@@ -178,10 +178,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
     if (acc == 0x12345u) g_sink = acc;
   }
   if (issuer) {
-    if (MODE != 3) mbar_wait_cluster(&ready, 0); else mbar_wait(&ready, 0);
+    if (!(MODE == 3 || MODE == 31)) mbar_wait_cluster(&ready, 0); else mbar_wait(&ready, 0);
     fence_after();
-    const uint32_t N = MODE == 2 ? 128 : (MODE == 29 ? 16 : (MODE == 30 ? 64 : 256));
-    const uint32_t idesc = MODE == 3 ? idesc_f16(128, N, 1, 1) : (MODE == 20 ? idesc_f16(256, N, 0, 0) : idesc_f16(256, N, 1, 1));
+    const uint32_t N = MODE == 2 ? 128 : ((MODE == 29 || MODE == 31) ? 16 : (MODE == 30 ? 64 : 256));
+    const uint32_t idesc = (MODE == 3 || MODE == 31) ? idesc_f16(128, N, 1, 1) : (MODE == 20 ? idesc_f16(256, N, 0, 0) : idesc_f16(256, N, 1, 1));
     long long t0 = clock64();
     if (MODE == 21 || MODE == 22 || MODE == 23) {      // rings + per-stage readiness checks (k_fused3 issuer)
       uint32_t gsl = 0, wsl = 0;
@@ -232,22 +232,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
         }
         if (MODE == 4 || MODE == 6) { mma2_commit(&scratch[0], 0x3); mma2_commit(&scratch[1], 0x3); }
       }
-    if (MODE == 3) mma_commit(&done); else mma2_commit(&done, 0x3);
+    if ((MODE == 3 || MODE == 31)) mma_commit(&done); else mma2_commit(&done, 0x3);
     mbar_wait(&done, 0);
     long long t1 = clock64();
     if (blockIdx.x == 0) *cyc = (unsigned long long)(t1 - t0);
   }
   if (t == 0) {                                        // stop the background warps of both CTAs
-    if (issuer || MODE == 3) stop = 1;
+    if (issuer || (MODE == 3 || MODE == 31)) stop = 1;
   }
-  if (MODE != 3) { if (t < 32 && !issuer) {} }
+  if (!(MODE == 3 || MODE == 31)) { if (t < 32 && !issuer) {} }
   __syncwarp();
-  if (!issuer && t == 0 && MODE != 3 && MODE != 15 && MODE != 25 && MODE != 27) { mbar_wait(&done, 0); stop = 1; }
+  if (!issuer && t == 0 && !(MODE == 3 || MODE == 31) && MODE != 15 && MODE != 25 && MODE != 27) { mbar_wait(&done, 0); stop = 1; }
   fence_before();
   __syncthreads();
   cluster_sync();
   fence_after();
-  if (w == 0) { if (MODE == 3) tmem_dealloc(tb, 512); else tmem_dealloc2(tb, 512); }
+  if (w == 0) { if ((MODE == 3 || MODE == 31)) tmem_dealloc(tb, 512); else tmem_dealloc2(tb, 512); }
 }
 
 template <int MODE>
@@ -269,8 +269,8 @@ void run(const char* name) {
   cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long c = 0;
   cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
-  const double M = MODE == 3 ? 128 : 256, N = MODE == 2 ? 128 : (MODE == 29 ? 16 : (MODE == 30 ? 64 : 256));
-  const double groups = MODE == 3 ? 148 : 74;
+  const double M = (MODE == 3 || MODE == 31) ? 128 : 256, N = MODE == 2 ? 128 : ((MODE == 29 || MODE == 31) ? 16 : (MODE == 30 ? 64 : 256));
+  const double groups = (MODE == 3 || MODE == 31) ? 148 : 74;
   const double flops = (MODE == 13 || (MODE >= 21 && MODE < 29)) ? 2.0 * M * N * 16 * 52 * (reps / 4) * groups : MODE == 13 ? 2.0 * M * N * 16 * 50 * (reps / 4) * groups : 2.0 * M * N * 16 * 16 * reps * groups;
   printf("%-28s err=%d  %.3f ms  %.1f TFLOP/s  cycles/MMA (cluster 0) %.1f\n", name, (int)e, ms, flops / (ms * 1e-3) / 1e12,
          (double)c / ((MODE >= 21 && MODE < 29) ? 52.0 * (reps / 4) : MODE == 13 ? 50.0 * (reps / 4) : 16.0 * reps));
@@ -281,9 +281,6 @@ int main() {
   run<3>("1CTA SS M128 N256 K16");
   run<29>("2CTA SS M256 N16 K16");
   run<30>("2CTA SS M256 N64 K16");
-  run<10>("SS + 8 warps Philox ALU");
-  run<11>("SS + 8 warps STS.128 stream");
-  run<12>("SS + 8 warps Philox+STS");
-  run<24>("SS + 8 warps TMEM ld/st epi");
+  run<31>("1CTA SS M128 N16 K16");
   return 0;
 }
