@@ -98,6 +98,7 @@ struct LargeArgs {
   float stepS;
   uint32_t cm2, cc2;
   const uint8_t* W1h;
+  uint32_t rk[20];                 // Philox round keys of pert.seed
 };
 
 struct TileInfo {
@@ -128,14 +129,15 @@ __device__ __forceinline__ uint64_t row_index(const LargeArgs& a, const TileInfo
 }
 
 // Philox4x32-10 (reading C15): counter (c_lo, c_hi, b, j), key (seed_lo, seed_hi)
-__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+// Philox4x32-10 (reading C15) with the launch's round keys precomputed on the host (parameter bank:
+// two IMAD.WIDE and two LOP3 per round, no per-call key schedule)
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const uint32_t (&rk)[20]) {
 #pragma unroll
   for (int r = 0; r < 10; r++) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
     const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r], n2 = hi0 ^ c3 ^ rk[2 * r + 1];
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
   }
   return make_uint4(c0, c1, c2, c3);
 }
@@ -209,7 +211,6 @@ __device__ __forceinline__ uint4 clamp_word(uint32_t w, uint4 nx, uint4 px, uint
 __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot) {
   const int n0 = a.net.sizes[0];
   const uint64_t c = row_index(a, ti, r);
-  const uint32_t k0 = (uint32_t)a.pert.seed, k1 = (uint32_t)(a.pert.seed >> 32);
   const bool valid = r < ti.nvalid;
   if (a.clamp) {
     const int nch = (n0 + 7) / 8;
@@ -218,7 +219,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
     for (int hb = 0; hb < 2; hb++) {
       const int j = 2 * kb + hb;
       uint4 w = make_uint4(0, 0, 0, 0);
-      if (32 * j < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, k0, k1);
+      if (32 * j < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, a.rk);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int ww = 0; ww < 4; ww++) {
@@ -237,7 +238,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
       const int j = 2 * kb + hb;
       const int p0 = 32 * j;
       uint4 w = make_uint4(0, 0, 0, 0);
-      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, k0, k1);
+      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, a.rk);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int ww = 0; ww < 4; ww++) {
@@ -275,7 +276,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
       const int j = 4 * kb + q;
       const int p0 = 32 * j;
       uint4 w = make_uint4(0, 0, 0, 0);
-      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, k0, k1);
+      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, a.rk);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
       if (p0 + 32 <= n0 && (n0 & 7) == 0 && s >= 0) {    // whole block in range: 16-bit-lane form
         const uint32_t c2 = (uint32_t)(256 + og) * 0x00010001u;
@@ -1150,6 +1151,15 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
   a.scratch_per_cta = g.scratch_per_cta;
   if (!scratch) return cudaErrorInvalidValue;     // the handle's scratch: num_sms x scratch_per_cta, K padding zero
   a.scratch = static_cast<uint8_t*>(scratch);
+  {
+    uint32_t k0 = (uint32_t)pert.seed, k1 = (uint32_t)(pert.seed >> 32);
+    for (int r = 0; r < 10; r++) {
+      a.rk[2 * r] = k0;
+      a.rk[2 * r + 1] = k1;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+  }
   if (pert.kind == MLPV_PERT_PHILOX_CLAMP) {
     a.clamp = 1;
     a.stepS = ldexpf(1.0f, -pert.clamp_s);
