@@ -34,7 +34,7 @@
 // MLPV_EXP = 201: the weight tiles are not streamed (128 B per stage); 202: the epilogue skips its
 // per-column work (barriers only); 203: the generators skip the candidate generation;
 // 204: all three; 205: layer-1 chunk pairs share one accumulator; 206: two of the four MMAs per
-// layer-1 stage
+// layer-1 stage; 207: no activation stores to the scratch; 209: discard.global.L2 of the dead scratch
 
 namespace mlpv {
 using namespace tc;
@@ -42,7 +42,11 @@ using namespace tc;
 #ifdef MLPV_TRACE
 __device__ unsigned long long g_kltrace[32][24];       // block 0, first 32 tiles, clock64 stamps
 #define KT(tl, ev) do { if (blockIdx.x == 0 && (tl) < 32) g_kltrace[(tl)][(ev)] = clock64(); } while (0)
+__device__ unsigned long long g_klstep[2][2][16][4];   // block 0, tile 2, quadrant 0: [half][chunk][step][event]
+#define KS(tl, l, ch, st, ev) do { if (blockIdx.x == 0 && (tl) == 2 && (l) == 1 && (ch) < 2 && quad == 0 && lane == 0 && (st) < 16) \
+    g_klstep[hh][(ch)][(st)][(ev)] = clock64(); } while (0)
 #else
+#define KS(tl, l, ch, st, ev) do { } while (0)
 #define KT(tl, ev) do { } while (0)
 #endif
 
@@ -91,6 +95,8 @@ struct LargeArgs {
   void* eval_out;
   int pair_of_lower[kMaxL + 1];    // pair index whose lower layer is k, or -1
   int soff[kMaxL + 2];             // staged bias / base potentials: layer l at [soff[l], soff[l+1]) (x4 aligned)
+  int goff[kMaxL + 2];             // staged per-16-neuron summaries of the base potentials: layer l at
+                                   // [goff[l], goff[l+1]) (sign word, min |u_base|)
   int staged;                      // 1: biases and the tile's base potentials live in shared memory
   // PHILOX_CLAMP (reading C14): layer 1 contracts A = d 2^s (fp16, d = x' - x exact) against the fp16
   // copy of W1 (W1h, the layer-1 tile layout) and forms u1 = base1 + 2^-s acc
@@ -205,6 +211,15 @@ __device__ __forceinline__ uint4 clamp_word(uint32_t w, uint4 nx, uint4 px, uint
     o[k] = *reinterpret_cast<const uint32_t*>(&d);
   }
   return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// 16 consecutive 32-bit words from shared memory (16-byte aligned address)
+__device__ __forceinline__ void lds16(uint32_t saddr, uint32_t (&w)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[4 * q]), "=r"(w[4 * q + 1]), "=r"(w[4 * q + 2]), "=r"(w[4 * q + 3])
+                 : "r"(saddr + 16u * q));
 }
 
 // ----------------------------------------------------------------------------- generator
@@ -330,6 +345,44 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
   }
 }
 
+// ----------------------------------------------------------------------------- verdict
+// Argmax (lowest index on ties), margin and the safety property of one candidate's logits
+// (readings C5/C6): lg holds the n_L <= 16 output potentials.
+template <typename TL>
+__device__ __forceinline__ void verdict(const LargeArgs& a, const TL (&lg)[16], int base_cls, bool& viol, bool& flag) {
+  const int nL = a.net.sizes[a.net.L];
+  int cls = 0;
+  viol = false;
+  flag = false;
+  TL top1 = lg[0];
+#pragma unroll
+  for (int i = 1; i < MLPV_MAX_CLASSES; i++) if (i < nL && lg[i] > top1) { top1 = lg[i]; cls = i; }
+  constexpr bool fl = sizeof(TL) == 4 && TL(0.5) != TL(0);
+  if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
+    const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
+    const TL V = fl ? (TL)a.prop.V_f : (TL)a.prop.V_i;
+    bool any = false, all = true;
+    TL yD = 0;
+#pragma unroll
+    for (int i = 0; i < MLPV_MAX_CLASSES; i++)
+      if (i < nL) {
+        if (i == D) yD = lg[i];
+        if (i != D && lg[i] > V) any = true;
+        if (i != D && !(lg[i] > V)) all = false;
+        if (fl && fabsf((float)lg[i] - a.prop.V_f) < a.cov.near_tie) flag = true;
+      }
+    viol = yD < V && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? all : any);
+  } else {
+    if (fl) {
+      float top2 = -3.0e38f;
+#pragma unroll
+      for (int i = 0; i < MLPV_MAX_CLASSES; i++) if (i < nL && i != cls && (float)lg[i] > top2) top2 = (float)lg[i];
+      flag = nL > 1 && (float)top1 - top2 < a.cov.near_tie;
+    }
+    viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != base_cls;
+  }
+}
+
 // ----------------------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ LargeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -358,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
   // biases of every layer (32-bit float or int) once; the base potentials per tile (epilogue)
   uint32_t* s_bias = s_xch + kXchWords;
   uint32_t* s_ub = s_bias + a.soff[a.net.L + 1];
+  uint2* s_g = reinterpret_cast<uint2*>(s_ub + a.soff[a.net.L + 1]);
   if (a.staged)
     for (int l = 1; l <= L; l++)
       for (int j = threadIdx.x; j < a.net.sizes[l]; j += blockDim.x)
@@ -395,14 +449,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         for (int l = 1; l <= L; l++)                                                         // at its last
           for (int j = e; j < a.net.sizes[l]; j += 256) s_ub[a.soff[l] + j] = tr[a.net.loff[l] + j];   // barrier)
         named_bar(2, 256);
+        // per 16 neurons: the base's sign word (bit k: neuron 16 g + k negative, reading C2) and
+        // min |u_base| (float nets), used by every candidate row of the tile
+        for (int l = 1; l <= L; l++) {
+          const int n = a.net.sizes[l];
+          for (int g = e; g < (n + 15) / 16; g += 256) {
+            uint32_t w = 0;
+            float m = 3.0e38f;
+            for (int k = 0; k < 16 && 16 * g + k < n; k++) {
+              const uint32_t x = s_ub[a.soff[l] + 16 * g + k];
+              const uint32_t sb = fl ? __float_as_uint(__uint_as_float(x) + 0.0f) >> 31 : x >> 31;
+              w |= sb << k;
+              if (fl) m = fminf(m, fabsf(__uint_as_float(x)));
+            }
+            s_g[a.goff[l] + g] = make_uint2(w, __float_as_uint(m));
+          }
+        }
+        named_bar(2, 256);
       }
       // per-layer summaries of the previous layer (lower layer of the pair being finished)
       int p_nsc = 0, p_istar = -1;
       bool p_cond = false, p_amb = false;
-      float lg_f[MLPV_MAX_CLASSES];
-      int32_t lg_i[MLPV_MAX_CLASSES];
-#pragma unroll
-      for (int i = 0; i < MLPV_MAX_CLASSES; i++) { lg_f[i] = 0.f; lg_i[i] = 0; }
+      bool t_viol = false, t_flag = false;         // the verdict, from the output layer's step
       for (int l = 1; l <= L; l++) {
         const LayerDesc& ld = a.lay[l];
         const int pidx = l >= 2 ? a.pair_of_lower[l - 1] : -1;
@@ -427,12 +495,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         if (l >= 2) bias_f = ub_f;
         const int32_t* ub_i = a.staged ? reinterpret_cast<const int32_t*>(s_ub + a.soff[l])
                                        : static_cast<const int32_t*>(a.ws.trace) + (size_t)ti.b * T + a.net.loff[l];
+        // staged: shared-memory addresses of the biases and the base potentials (explicit ld.shared;
+        // PHILOX_CLAMP layer 1 and float layers >= 2 take the base potentials as their offset)
+        const uint32_t sa_u = smem_u32(s_ub + a.soff[l]);
+        const bool off_is_ub = fl && (l >= 2 || a.clamp);
+        const uint32_t sa_b = off_is_ub ? sa_u : smem_u32(s_bias + a.soff[l]);
+        const uint2* s_gl = s_g + a.goff[l];
+        float lacc = 0.f;                            // delta layers: max |acc| (u - u_base = sS acc)
         uint8_t* hdst = scratch + a.h_off[l];
         const int sh = a.net.shift[l - 1];
         for (int ch = 0; ch < ld.nchunks; ch++) {
           const uint32_t buf = cseq & 1u, ph = (cseq >> 1) & 1u;
           mbar_wait(&acc_full[buf], ph);
           fence_after();
+          if (MLPV_EXP == 209 && l == L && ch == 0) {
+            // every layer's MMAs of this tile are complete: its activation scratch is dead
+            for (size_t o = (size_t)e * 128; o < a.scratch_per_cta; o += 256 * 128)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(scratch + o) : "memory");
+          }
           const int c_lo = ld.nc >= 64 ? hh * (ld.nc >> 1) : 0;
           const int c_hi = ld.nc >= 64 ? c_lo + (ld.nc >> 1) : (hh == 0 ? ld.nc : 0);
           for (int pc = c_lo; pc < ((MLPV_EXP == 202 || MLPV_EXP == 204) ? c_lo : c_hi); pc += 16) {
@@ -440,8 +520,107 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
             if (j0 >= ld.n && l == L) break;
             if (j0 >= ((ld.n + 63) & ~63) && l < L && fl) break;
             uint32_t v[16];
+            const int kst = (pc - c_lo) >> 4;
+            KS(etl, l, ch, kst, 0);
             tmem_ld16(tbase + buf * 256u + (uint32_t)pc + lane_off, v);
             tmem_ld_wait();
+#ifdef MLPV_TRACE
+            {   // (the stamp waits for the loaded registers: the ld wait is a scoreboard dependency)
+              uint32_t dep = 0;
+#pragma unroll
+              for (int i = 0; i < 16; i++) dep ^= v[i];
+              asm volatile("" ::"r"(dep));
+            }
+#endif
+            KS(etl, l, ch, kst, 1);
+            // ---- hot path (float net, staged base, delta layer (PHILOX_CLAMP layer 1 or l >= 2),
+            // hidden layer, a whole 16-neuron group, no pair-coverage words to record): short
+            // independent chains, no per-neuron guards
+            if (fl && a.staged && off_is_ub && l < L && !eval && !pair_on && j0 + 16 <= ld.n) {
+              uint32_t uw[16];
+              lds16(sa_u + 4u * (uint32_t)j0, uw);
+              const uint2 gw = s_gl[j0 >> 4];
+              float u[16];
+#pragma unroll
+              for (int i = 0; i < 16; i++) u[i] = fmaf(__uint_as_float(v[i]), sS, __uint_as_float(uw[i]));
+              uint32_t n0 = 0, n1 = 0;               // sign words (reading C2: -0.0 counts as >= 0)
+#pragma unroll
+              for (int i = 7; i >= 0; i--) {
+                n0 = __funnelshift_l(__float_as_uint(u[i] + 0.0f), n0, 1);
+                n1 = __funnelshift_l(__float_as_uint(u[i + 8] + 0.0f), n1, 1);
+              }
+              const uint32_t scw = (n0 | (n1 << 8)) ^ gw.x;
+              nsc += __popc(scw);
+              if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
+              float mn[4], mx[4];                    // min |u| and max |acc| in four chains
+#pragma unroll
+              for (int q = 0; q < 4; q++) { mn[q] = fabsf(u[q]); mx[q] = fabsf(__uint_as_float(v[q])); }
+#pragma unroll
+              for (int i = 4; i < 16; i++) { mn[i & 3] = fminf(mn[i & 3], fabsf(u[i])); mx[i & 3] = fmaxf(mx[i & 3], fabsf(__uint_as_float(v[i]))); }
+              minab = fminf(minab, fminf(fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3])), __uint_as_float(gw.y)));
+              lacc = fmaxf(lacc, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));
+              uint32_t hw[8], lw[8];
+#pragma unroll
+              for (int i = 0; i < 8; i++) {         // dh = ReLU(u) - ReLU(u_base) = hi + lo (reading C19)
+                const float h0 = fmaxf(u[2 * i], 0.f) - fmaxf(__uint_as_float(uw[2 * i]), 0.f);
+                const float h1 = fmaxf(u[2 * i + 1], 0.f) - fmaxf(__uint_as_float(uw[2 * i + 1]), 0.f);
+                const __half2 hi2 = __floats2half2_rn(h0, h1);
+                const float2 hf = __half22float2(hi2);
+                const __half2 lo2 = __floats2half2_rn(h0 - hf.x, h1 - hf.y);
+                hw[i] = *reinterpret_cast<const uint32_t*>(&hi2);
+                lw[i] = *reinterpret_cast<const uint32_t*>(&lo2);
+              }
+              if (MLPV_EXP != 207) {
+                const int kbh = j0 >> 6, byh = (2 * j0) & 127;
+                uint8_t* th = hdst + (size_t)kbh * kABytes;
+                uint8_t* tl = hdst + (size_t)(ld.lo_kb + kbh) * kABytes;
+#pragma unroll
+                for (int m = 0; m < 2; m++) {
+                  *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
+                  *reinterpret_cast<uint4*>(tl + sw128_off(r, byh + 16 * m)) = make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]);
+                }
+              }
+              continue;
+            }
+            // ---- hot path, int8 net (same conditions; reading C18: exact int32 potentials)
+            if (!fl && a.staged && l < L && !eval && !pair_on && j0 + 16 <= ld.n) {
+              uint32_t uw[16], bw[16];
+              lds16(sa_u + 4u * (uint32_t)j0, uw);
+              lds16(sa_b + 4u * (uint32_t)j0, bw);
+              const uint2 gw = s_gl[j0 >> 4];
+              int32_t u[16];
+#pragma unroll
+              for (int i = 0; i < 16; i++) u[i] = (int32_t)(v[i] + bw[i]);
+              uint32_t n0 = 0, n1 = 0;
+#pragma unroll
+              for (int i = 7; i >= 0; i--) {
+                n0 = __funnelshift_l((uint32_t)u[i], n0, 1);
+                n1 = __funnelshift_l((uint32_t)u[i + 8], n1, 1);
+              }
+              const uint32_t scw = (n0 | (n1 << 8)) ^ gw.x;
+              nsc += __popc(scw);
+              if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
+              int32_t mx[4];
+#pragma unroll
+              for (int q = 0; q < 4; q++) mx[q] = abs(u[q] - (int32_t)uw[q]);
+#pragma unroll
+              for (int i = 4; i < 16; i++) mx[i & 3] = max(mx[i & 3], abs(u[i] - (int32_t)uw[i]));
+              linf_i = max(linf_i, max(max(mx[0], mx[1]), max(mx[2], mx[3])));
+              const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
+              uint32_t hq[4];
+#pragma unroll
+              for (int q = 0; q < 4; q++) {         // y = clamp((u + rr) >> sh, 0, 255), packed
+                uint32_t hi2, w4;
+                asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi2) : "r"((u[4 * q + 3] + rr) >> sh), "r"((u[4 * q + 2] + rr) >> sh));
+                asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(w4) : "r"((u[4 * q + 1] + rr) >> sh), "r"((u[4 * q] + rr) >> sh), "r"(hi2));
+                hq[q] = w4;
+              }
+              if (MLPV_EXP != 207) {
+                const int kbh = j0 >> 7, byh = j0 & 127;
+                *reinterpret_cast<uint4*>(hdst + (size_t)kbh * kABytes + sw128_off(r, byh)) = make_uint4(hq[0], hq[1], hq[2], hq[3]);
+              }
+              continue;
+            }
             uint32_t hw[8];                          // fp16 hi pairs (float) or u8 quads (int8)
             uint32_t lw[8];
             if (fl) {
@@ -453,7 +632,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               // (the bias rows are 16-byte aligned; a base-trace row is 16- or 8-byte aligned
               // depending on its base index and the trace length)
               const uintptr_t ua = reinterpret_cast<uintptr_t>(ub_f + j0);
-              if (nin == 16 && ((reinterpret_cast<uintptr_t>(bias_f + j0) | (ua & 7u)) & 15u) == 0) {
+              if (a.staged) {
+                uint32_t uw[16];
+                lds16(sa_u + 4u * (uint32_t)j0, uw);
+                if (off_is_ub) {
+#pragma unroll
+                  for (int i = 0; i < 16; i++) { ubv[i] = __uint_as_float(uw[i]); u[i] = fmaf(__uint_as_float(v[i]), sS, ubv[i]); }
+                } else {
+                  uint32_t bw[16];
+                  lds16(sa_b + 4u * (uint32_t)j0, bw);
+#pragma unroll
+                  for (int i = 0; i < 16; i++) { ubv[i] = __uint_as_float(uw[i]); u[i] = fmaf(__uint_as_float(v[i]), sS, __uint_as_float(bw[i])); }
+                }
+                if (nin < 16) {
+#pragma unroll
+                  for (int i = 0; i < 16; i++) if (i >= nin) { u[i] = 0.f; ubv[i] = 0.f; }
+                }
+              } else if (nin == 16 && ((reinterpret_cast<uintptr_t>(bias_f + j0) | (ua & 7u)) & 15u) == 0) {
 #pragma unroll
                 for (int q4 = 0; q4 < 4; q4++) {
                   const float4 b4 = reinterpret_cast<const float4*>(bias_f + j0)[q4];
@@ -485,26 +680,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               }
               // sign words (reading C2: sign(u) = 1 iff u >= 0, so -0.0 counts as >= 0: + 0.0f)
               uint32_t nu = 0, nb = 0, ng = 0;
+              const bool fast = a.staged && nin == 16;
+              if (fast) {
+                // whole 16-neuron group, staged base: the base's sign word and min |u_base| come
+                // from the tile's table; delta layers take L-inf from max |acc| (scaled once per layer)
+                const uint2 gw = s_gl[j0 >> 4];
+                nb = gw.x;
 #pragma unroll
-              for (int i = 15; i >= 0; i--) {
-                nu = __funnelshift_l(__float_as_uint(u[i] + 0.0f), nu, 1);
-                nb = __funnelshift_l(__float_as_uint(ubv[i] + 0.0f), nb, 1);
+                for (int i = 15; i >= 0; i--) nu = __funnelshift_l(__float_as_uint(u[i] + 0.0f), nu, 1);
+                float m0 = __uint_as_float(gw.y), m1 = fabsf(u[0]);
+#pragma unroll
+                for (int i = 1; i < 16; i += 2) { m0 = fminf(m0, fabsf(u[i])); if (i + 1 < 16) m1 = fminf(m1, fabsf(u[i + 1])); }
+                minab = fminf(minab, fminf(m0, m1));
+                if (off_is_ub) {
+                  float x0 = fabsf(__uint_as_float(v[0])), x1 = fabsf(__uint_as_float(v[1]));
+#pragma unroll
+                  for (int i = 2; i < 16; i += 2) { x0 = fmaxf(x0, fabsf(__uint_as_float(v[i]))); x1 = fmaxf(x1, fabsf(__uint_as_float(v[i + 1]))); }
+                  lacc = fmaxf(lacc, fmaxf(x0, x1));
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 16; i++) linf_f = fmaxf(linf_f, fabsf(u[i] - ubv[i]));
+                }
+              } else {
+#pragma unroll
+                for (int i = 15; i >= 0; i--) {
+                  nu = __funnelshift_l(__float_as_uint(u[i] + 0.0f), nu, 1);
+                  nb = __funnelshift_l(__float_as_uint(ubv[i] + 0.0f), nb, 1);
+                }
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                  if (i < nin) {
+                    linf_f = fmaxf(linf_f, fabsf(u[i] - ubv[i]));
+                    minab = fminf(minab, fminf(fabsf(u[i]), fabsf(ubv[i])));
+                  }
+                }
               }
               const uint32_t scw = (nu ^ nb) & inmask;
               nsc += __popc(scw);
               if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
-              float dt[16];
-#pragma unroll
-              for (int i = 0; i < 16; i++) {
-                const bool in = i < nin;
-                const float d = fabsf(u[i] - ubv[i]);
-                if (in) {
-                  linf_f = fmaxf(linf_f, d);
-                  minab = fminf(minab, fminf(fabsf(u[i]), fabsf(ubv[i])));
-                }
-                dt[i] = d - tg_f;                      // value change <=> sign bit clear
-              }
               if (pair_on) {
+                float dt[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) dt[i] = fabsf(u[i] - ubv[i]) - tg_f;   // value change <=> sign bit clear
 #pragma unroll
                 for (int i = 15; i >= 0; i--) {
                   ng = __funnelshift_l(__float_as_uint(dt[i]), ng, 1);
@@ -519,10 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
                 for (int i = 0; i < 16; i++)
                   if (i < nin) static_cast<float*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j0 + i] = u[i];
               }
-              if (l == L && j0 == 0) {
-#pragma unroll
-                for (int i = 0; i < MLPV_MAX_CLASSES; i++) if (i < nin) lg_f[i] = u[i];
-              }
+              if (l == L && j0 == 0 && !eval) verdict(a, u, a.ws.cls[ti.b], t_viol, t_flag);
               if (l < L) {
                 // h = hi + lo, two fp16 (RN), reading C19
 #pragma unroll
@@ -543,7 +757,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               const uint32_t inmask = nin >= 16 ? 0xFFFFu : ((1u << nin) - 1u);
               int32_t u[16], ubv[16];
               const uintptr_t ua = reinterpret_cast<uintptr_t>(ub_i + j0), ba = reinterpret_cast<uintptr_t>(bias_i + j0);
-              if (nin == 16 && ((ua | ba) & 15u) == 0) {
+              if (a.staged) {
+                uint32_t uw[16], bw[16];
+                lds16(sa_u + 4u * (uint32_t)j0, uw);
+                lds16(sa_b + 4u * (uint32_t)j0, bw);
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                  const bool in = i < nin;
+                  u[i] = in ? (int32_t)v[i] + (int32_t)bw[i] : 0;
+                  ubv[i] = in ? (int32_t)uw[i] : 0;
+                }
+              } else if (nin == 16 && ((ua | ba) & 15u) == 0) {
 #pragma unroll
                 for (int q4 = 0; q4 < 4; q4++) {
                   const int4 b4 = reinterpret_cast<const int4*>(bias_i + j0)[q4];
@@ -563,10 +787,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
                 }
               }
               uint32_t nu = 0, nb = 0, ng = 0;
+              if (a.staged && nin == 16) {
+                nb = s_gl[j0 >> 4].x;
 #pragma unroll
-              for (int i = 15; i >= 0; i--) {
-                nu = __funnelshift_l((uint32_t)u[i], nu, 1);
-                nb = __funnelshift_l((uint32_t)ubv[i], nb, 1);
+                for (int i = 15; i >= 0; i--) nu = __funnelshift_l((uint32_t)u[i], nu, 1);
+              } else {
+#pragma unroll
+                for (int i = 15; i >= 0; i--) {
+                  nu = __funnelshift_l((uint32_t)u[i], nu, 1);
+                  nb = __funnelshift_l((uint32_t)ubv[i], nb, 1);
+                }
               }
               const uint32_t scw = (nu ^ nb) & inmask;
               nsc += __popc(scw);
@@ -590,10 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
                 for (int i = 0; i < 16; i++)
                   if (i < nin) static_cast<int32_t*>(a.eval_out)[(size_t)(ti.start + r) * T + a.net.loff[l] + j0 + i] = u[i];
               }
-              if (l == L && j0 == 0) {
-#pragma unroll
-                for (int i = 0; i < MLPV_MAX_CLASSES; i++) if (i < nin) lg_i[i] = u[i];
-              }
+              if (l == L && j0 == 0 && !eval) verdict(a, u, a.ws.cls[ti.b], t_viol, t_flag);
               if (l < L) {
                 const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
                 // y = clamp((u + rr) >> sh, 0, 255) (reading C18): cvt.pack.sat saturates two s32
@@ -610,7 +837,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
                 }
               }
             }
-            if (l < L) {
+            KS(etl, l, ch, kst, 2);
+            if (l < L && MLPV_EXP != 207) {
               if (fl) {
                 // 16 fp16 values = 32 bytes at K element j0 (hi) and lo_kb*64 + j0 (lo)
                 const int kbh = j0 >> 6, byh = (2 * j0) & 127;
@@ -630,6 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
               }
             }
           }
+          KS(etl, l, ch, 15, 3);
           fence_before();
           named_bar(2, 256);
           if (e == 0) mbar_arrive(&acc_empty[buf]);
@@ -638,6 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         }
         // ---- the two halves' partial results of layer l (count, lowest changed neuron, L-inf,
         // min |u|, value-change margin), exchanged through shared memory (64 threads per quadrant)
+        if (fl && off_is_ub) linf_f = fmaxf(linf_f, lacc * sS);
         {
           uint32_t* mine = s_xch + (size_t)hh * 4 * kM;
           const uint32_t* other = s_xch + (size_t)(hh ^ 1) * 4 * kM;
@@ -700,56 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
         }
       }
       if (eval || hh == 1) continue;                 // the logits (and so the verdict) live in half 0
-      // ---- argmax (lowest index on ties), margin, property
-      const int nL = a.net.sizes[L];
-      int cls = 0;
-      bool viol = false, flag = false;
-      const int base_cls = a.ws.cls[ti.b];
-      if (fl) {
-        float top1 = lg_f[0];
-#pragma unroll
-        for (int i = 1; i < MLPV_MAX_CLASSES; i++) if (i < nL && lg_f[i] > top1) { top1 = lg_f[i]; cls = i; }
-        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
-          const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
-          bool any = false, all = true;
-          float yD = 0.f;
-#pragma unroll
-          for (int i = 0; i < MLPV_MAX_CLASSES; i++)
-            if (i < nL) {
-              if (i == D) yD = lg_f[i];
-              if (i != D && lg_f[i] > a.prop.V_f) any = true;
-              if (i != D && !(lg_f[i] > a.prop.V_f)) all = false;
-              if (fabsf(lg_f[i] - a.prop.V_f) < a.cov.near_tie) flag = true;
-            }
-          viol = yD < a.prop.V_f && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? all : any);
-        } else {
-          float top2 = -3.0e38f;
-#pragma unroll
-          for (int i = 0; i < MLPV_MAX_CLASSES; i++) if (i < nL && i != cls && lg_f[i] > top2) top2 = lg_f[i];
-          flag = nL > 1 && top1 - top2 < a.cov.near_tie;
-          viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != base_cls;
-        }
-      } else {
-        int32_t top1 = lg_i[0];
-#pragma unroll
-        for (int i = 1; i < MLPV_MAX_CLASSES; i++) if (i < nL && lg_i[i] > top1) { top1 = lg_i[i]; cls = i; }
-        if (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL || a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL) {
-          const int D = a.prop.target >= 0 ? a.prop.target : base_cls;
-          const int32_t V = (int32_t)a.prop.V_i;
-          bool any = false, all = true;
-          int32_t yD = 0;
-#pragma unroll
-          for (int i = 0; i < MLPV_MAX_CLASSES; i++)
-            if (i < nL) {
-              if (i == D) yD = lg_i[i];
-              if (i != D && lg_i[i] > V) any = true;
-              if (i != D && !(lg_i[i] > V)) all = false;
-            }
-          viol = yD < V && (a.prop.kind == MLPV_PROP_THRESHOLD_LITERAL_ALL ? all : any);
-        } else {
-          viol = a.prop.kind == MLPV_PROP_TARGET_NEVER ? cls == a.prop.target : cls != base_cls;
-        }
-      }
+      bool viol = t_viol, flag = t_flag;
       if (!valid) { viol = false; flag = false; }
       // ---- per-tile reduction (a9): warp reduce, one atomic per warp and counter
       const uint32_t nv = __reduce_add_sync(0xffffffffu, viol ? 1u : 0u);
@@ -958,6 +1139,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
 #ifdef MLPV_TRACE
 extern "C" int mlpv_kl_trace_read(void* host) {
   return (int)cudaMemcpyFromSymbol(host, g_kltrace, sizeof g_kltrace);
+}
+extern "C" int mlpv_kl_step_read(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_klstep, sizeof g_klstep);
 }
 #endif
 
@@ -1169,7 +1353,10 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
   }
   a.soff[1] = 0;
   for (int l = 1; l <= net.L; l++) a.soff[l + 1] = a.soff[l] + ((net.sizes[l] + 3) & ~3);
-  const size_t stage_bytes = (size_t)2 * a.soff[net.L + 1] * 4;
+  a.goff[1] = 0;
+  for (int l = 1; l <= net.L; l++) a.goff[l + 1] = a.goff[l] + (net.sizes[l] + 15) / 16;
+  // biases + base potentials, the per-group table, + 16 words read past the end (masked)
+  const size_t stage_bytes = (size_t)2 * a.soff[net.L + 1] * 4 + (size_t)a.goff[net.L + 1] * 8 + 64;
   a.staged = kSmemBytes + stage_bytes <= (size_t)227 * 1024 ? 1 : 0;
   const size_t smem = kSmemBytes + (a.staged ? stage_bytes : 0);
   cudaError_t e = cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

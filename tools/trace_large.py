@@ -42,3 +42,14 @@ for tl in range(1, 4):
     print(f"tile {tl}: issuer waits (cycles) pair0 gfull {int(buf[tl, 20])} pfull {int(buf[tl, 21])}; pair1 gfull {int(buf[tl, 22])} pfull {int(buf[tl, 23])}")
 per = [int(buf[tl + 1, 0]) - int(buf[tl, 0]) for tl in range(1, 10) if buf[tl + 1, 0]]
 print("tile period (cycles):", per)
+
+st = np.zeros((2, 2, 16, 4), np.uint64)
+if hasattr(P.lib(), "mlpv_kl_step_read") and P.lib().mlpv_kl_step_read(st.ctypes.data_as(C.c_void_p)) == 0:
+    for hh in range(2):
+        for ch in range(2):
+            t0s = int(st[hh, ch, 0, 0])
+            if not t0s:
+                continue
+            steps = [(int(st[hh, ch, k, 0]) - t0s, int(st[hh, ch, k, 1]) - int(st[hh, ch, k, 0]),
+                      int(st[hh, ch, k, 2]) - int(st[hh, ch, k, 1])) for k in range(16) if st[hh, ch, k, 0]]
+            print(f"E1 tile 2 quad 0 half {hh} chunk {ch}: (start, ld, compute) per step {steps}; end {int(st[hh, ch, 15, 3]) - t0s}")
