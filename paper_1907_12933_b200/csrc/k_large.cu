@@ -45,29 +45,48 @@ __device__ unsigned long long g_kltrace[32][24];       // block 0, first 32 tile
 __device__ unsigned long long g_klstep[2][2][16][4];   // block 0, tile 2, quadrant 0: [half][chunk][step][event]
 #define KS(tl, l, ch, st, ev) do { if (blockIdx.x == 0 && (tl) == 2 && (l) == 1 && (ch) < 2 && quad == 0 && lane == 0 && (st) < 16) \
     g_klstep[hh][(ch)][(st)][(ev)] = clock64(); } while (0)
+__device__ unsigned long long g_klgen[2][48][4];       // block 0, tile 2, pass 1: [group][stage][event]
+#define KG(tl, pass, kb, ev) do { if (blockIdx.x == 0 && (tl) == 2 && (pass) == 1 && (kb) < 48 && (warp & 3) == 0 && lane == 0) \
+    g_klgen[ggrp][(kb)][(ev)] = clock64(); } while (0)
+// W ring of layer 1, block 0 (leader), tile 2: [sub-stage 0..191][0 producer wait start, 1 copy
+// issued, 2 issuer wait start, 3 issuer wait done]
+__device__ unsigned long long g_klw[192][4];
+#define KW(tl, i, ev) do { if (blockIdx.x == 0 && (tl) == 2 && (i) < 192) g_klw[(i)][(ev)] = clock64(); } while (0)
 #else
+#define KG(tl, pass, kb, ev) do { } while (0)
+#define KW(tl, i, ev) do { } while (0)
 #define KS(tl, l, ch, st, ev) do { } while (0)
 #define KT(tl, ev) do { } while (0)
 #endif
 
 constexpr int kM = 128;                   // candidates per tile = TMEM lanes
+// CTA pairs (clusters of 2): a tile is 256 candidates, rows 0-127 in the leader (rank 0), 128-255
+// in the peer; the leader issues every MMA with cta_group::2 (M = 256), each CTA holding its own A
+// rows and half of every W tile (N / 2 rows), so each SM streams half the weight bytes per
+// candidate of the one-CTA design.
 constexpr int kSG = 3;                    // generator ring stages
-constexpr int kSP = 3;                    // producer ring stages, layers >= 2 (W tile + A tile)
-constexpr int kSPA = 4;                   // producer ring stages, layer 1 (W tile only; the same bytes)
+constexpr int kSP = 4;                    // producer ring stages, layers >= 2 (W half tile + A tile)
+constexpr int kSPA = 8;                   // producer ring stages, layer 1 (W half tiles; the same bytes)
 constexpr uint32_t kABytes = 128u * 128u; // A tile: 128 rows x 128 B
-constexpr uint32_t kWBytes = 256u * 128u; // W tile: up to 256 rows x 128 B
+constexpr uint32_t kWBytes = 128u * 128u; // W half tile: up to 128 rows x 128 B
 constexpr int kThreads = 640;                // 5 warpgroups: 2 x generator, 2 x epilogue (halves), control
 // The SMSP arbiter favours the highest warp id: the MMA issuer and the weight producer get the top
 // ids (a low-id issuer lost issue slots to the generators: 260 cycles per 128-cycle MMA, trace),
 // then the epilogue, then the generators.
 constexpr int kWProd = 18, kWIss = 19;
+// a second producer (warp 17) takes every other ring stage, and the peer relays with warps 16 and
+// 19: one thread's chain of mbarrier operations per stage (wait, expect_tx, copy) takes ~850
+// cycles, more than the 512-cycle MMA time of a W stage (trace)
+constexpr int kWProd2 = 17, kWRel2 = 16;
 // setmaxnreg budget: 2 x 80 (generators) + 56 (control) + 2 x 128 (epilogue halves) <= 5 x 96
 constexpr int kRegLaunchL = 96, kRegGenL = 80, kRegCtlL = 56, kRegEpiL = 128;
 static_assert(2 * kRegGenL + kRegCtlL + 2 * kRegEpiL <= 5 * kRegLaunchL, "setmaxnreg budget");
 constexpr uint32_t kTmemCols = 512;       // two 256-column accumulator buffers
 constexpr int kPendWords = 32;            // per candidate: 16 sc + 16 vc words (upper width <= 512)
 constexpr int kXchWords = 2 * 4 * kM;     // epilogue halves' per-row partial results (4 words per row)
-constexpr size_t kSmemBytes = 1024 + kSG * kABytes + kSP * (kABytes + kWBytes) + (size_t)kM * kPendWords * 4 + 4 * kXchWords;
+constexpr size_t kRing = kSP * (kABytes + kWBytes);   // layer 1: kSPA W slots; layers >= 2: kSP (A, W) stages
+static_assert(kSPA * kWBytes <= kRing, "ring region");
+constexpr size_t kSmemBytes = 1024 + kSG * kABytes + kRing + (size_t)kM * kPendWords * 4 + 4 * kXchWords;
 
 struct LayerDesc {
   int n, npad, nc, nchunks, nkb;   // neurons, padded, rows per W tile, chunks, 128-byte K blocks of A
@@ -101,6 +120,8 @@ struct LargeArgs {
   // PHILOX_CLAMP (reading C14): layer 1 contracts A = d 2^s (fp16, d = x' - x exact) against the fp16
   // copy of W1 (W1h, the layer-1 tile layout) and forms u1 = base1 + 2^-s acc
   int clamp;
+  int gtab;                        // bytes of the generators' per-base table staged in shared memory
+                                   // (PHILOX_CLAMP bounds / base pixels), 0: read from global
   float stepS;
   uint32_t cm2, cc2;
   const uint8_t* W1h;
@@ -113,20 +134,34 @@ struct TileInfo {
   int nvalid;
 };
 
-__device__ __forceinline__ TileInfo tile_info(const LargeArgs& a, uint64_t t) {
+// the CTA's half of pair tile t: rows 128 rank .. + 127 of the tile's 256 candidates
+__device__ __forceinline__ TileInfo tile_info(const LargeArgs& a, uint64_t t, uint32_t rank) {
   TileInfo ti;
+  int64_t rem;
   if (a.eval_idx) {
     ti.b = a.eval_base;
-    ti.start = t * kM;
-    const int64_t rem = a.eval_n - (int64_t)(t * kM);
-    ti.nvalid = rem < kM ? (int)rem : kM;
+    ti.start = t * (2 * kM) + kM * rank;
+    rem = a.eval_n - (int64_t)ti.start;
   } else {
     ti.b = (int)(t / a.tiles_per_base);
-    ti.start = a.pert.begin + (t % a.tiles_per_base) * kM;
-    const uint64_t rem = a.pert.end - ti.start;
-    ti.nvalid = rem < (uint64_t)kM ? (int)rem : kM;
+    ti.start = a.pert.begin + (t % a.tiles_per_base) * (2 * kM) + kM * rank;
+    rem = ti.start < a.pert.end ? (int64_t)(a.pert.end - ti.start) : 0;
   }
+  ti.nvalid = rem <= 0 ? 0 : (rem < kM ? (int)rem : kM);
   return ti;
+}
+
+// contiguous range of pair tiles owned by cluster c: consecutive tiles share a base input, so the
+// generators restage their per-base table rarely
+__device__ __forceinline__ void cluster_range(uint64_t n, uint64_t c, uint64_t nc, uint64_t& t0, uint64_t& t1) {
+  const uint64_t q = n / nc, r = n % nc;
+  t0 = c * q + (c < r ? c : r);
+  t1 = t0 + q + (c < r ? 1 : 0);
+}
+
+__device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t rank) {
+  if (rank == 0) mbar_arrive(bar);
+  else mbar_arrive_cluster(bar, 0);
 }
 
 __device__ __forceinline__ uint64_t row_index(const LargeArgs& a, const TileInfo& ti, int r) {
@@ -222,8 +257,21 @@ __device__ __forceinline__ void lds16(uint32_t saddr, uint32_t (&w)[16]) {
                  : "r"(saddr + 16u * q));
 }
 
+__device__ __forceinline__ uint4 lds_u4(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t saddr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(saddr));
+  return v;
+}
+
 // ----------------------------------------------------------------------------- generator
-__device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot) {
+// gt: shared-memory address of the base's staged table (PHILOX_CLAMP bounds, or the base pixels),
+// 0 when the table is read from global memory
+__device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot, uint32_t gt) {
   const int n0 = a.net.sizes[0];
   const uint64_t c = row_index(a, ti, r);
   const bool valid = r < ti.nvalid;
@@ -240,7 +288,11 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
       for (int ww = 0; ww < 4; ww++) {
         const int ch = 4 * j + ww;                       // 8-pixel chunk; beyond n_0: bounds 0, d = 0
         const uint4 z = make_uint4(0, 0, 0, 0);
-        const uint4 nx = ch < nch ? __ldg(tab + 2 * ch) : z, px = ch < nch ? __ldg(tab + 2 * ch + 1) : z;
+        uint4 nx = z, px = z;
+        if (ch < nch) {
+          if (gt) { nx = lds_u4(gt + 32u * ch); px = lds_u4(gt + 32u * ch + 16u); }
+          else { nx = __ldg(tab + 2 * ch); px = __ldg(tab + 2 * ch + 1); }
+        }
         *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (4 * hb + ww))) = clamp_word(ws[ww], nx, px, a.cm2, a.cc2);
       }
     }
@@ -262,7 +314,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
         uint32_t xv[4] = {0, 0, 0, 0};
         const int pw = p0 + 8 * ww;
         if (pw + 8 <= n0 && ((n0 & 7) == 0)) {
-          const uint4 x8 = __ldg(reinterpret_cast<const uint4*>(x + pw));
+          const uint4 x8 = gt ? lds_u4(gt + 2u * pw) : __ldg(reinterpret_cast<const uint4*>(x + pw));
           xv[0] = x8.x; xv[1] = x8.y; xv[2] = x8.z; xv[3] = x8.w;
         } else {
 #pragma unroll
@@ -297,8 +349,8 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
         const uint32_t c2 = (uint32_t)(256 + og) * 0x00010001u;
 #pragma unroll
         for (int half = 0; half < 2; half++) {
-          const uint2 xa = __ldg(reinterpret_cast<const uint2*>(x + p0 + 16 * half));
-          const uint2 xb2 = __ldg(reinterpret_cast<const uint2*>(x + p0 + 16 * half + 8));
+          const uint2 xa = gt ? lds_u2(gt + p0 + 16 * half) : __ldg(reinterpret_cast<const uint2*>(x + p0 + 16 * half));
+          const uint2 xb2 = gt ? lds_u2(gt + p0 + 16 * half + 8) : __ldg(reinterpret_cast<const uint2*>(x + p0 + 16 * half + 8));
           const uint2 ya = lattice8_u8(ws[2 * half], xa, (uint32_t)s, c2);
           const uint2 yb = lattice8_u8(ws[2 * half + 1], xb2, (uint32_t)s, c2);
           *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * (2 * q + half))) = make_uint4(ya.x, ya.y, yb.x, yb.y);
@@ -384,40 +436,49 @@ __device__ __forceinline__ void verdict(const LargeArgs& a, const TL (&lg)[16], 
 }
 
 // ----------------------------------------------------------------------------- the kernel
-__global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ LargeArgs a) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ LargeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sG = smem;                                        // [kSG][kABytes]
-  uint8_t* sPA = sG + kSG * kABytes;                         // [kSP][kABytes]
-  uint8_t* sPW = sPA + kSP * kABytes;                        // [kSP][kWBytes]
-  uint32_t* s_pend = reinterpret_cast<uint32_t*>(sPW + kSP * kWBytes);   // [kM][kPendWords]
+  uint8_t* sR = sG + kSG * kABytes;                          // ring region: layer 1 [kSPA][kWBytes];
+                                                             // layers >= 2 [kSP][A kABytes | W kWBytes]
+  uint32_t* s_pend = reinterpret_cast<uint32_t*>(sR + kRing);   // [kM][kPendWords]
   __shared__ uint64_t gfull[kSG], gempty[kSG], pfull[kSP], pempty[kSP], pfullA[kSPA], pemptyA[kSPA], acc_full[2],
       acc_empty[2], h_ready[kMaxL + 1];
   __shared__ uint32_t s_tbase;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = a.net.L;
+  const uint32_t rank = cluster_ctarank();
+  const uint64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  uint64_t t_begin, t_end;
+  cluster_range(a.n_tiles, cluster, nclusters, t_begin, t_end);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kSG; i++) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
-    for (int i = 0; i < kSP; i++) { mbar_init(&pfull[i], 1); mbar_init(&pempty[i], 1); }
-    for (int i = 0; i < kSPA; i++) { mbar_init(&pfullA[i], 1); mbar_init(&pemptyA[i], 1); }
-    for (int i = 0; i < 2; i++) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 1); }
+    // the leader's full / acc_empty barriers count both CTAs (the peer arrives remotely; its
+    // producer's stages are relayed by its issuer warp); the empty / acc_full barriers of both CTAs
+    // take the leader's multicast commits
+    const uint32_t two = rank == 0 ? 2u : 1u;
+    for (int i = 0; i < kSG; i++) { mbar_init(&gfull[i], two); mbar_init(&gempty[i], 1); }
+    for (int i = 0; i < kSP; i++) { mbar_init(&pfull[i], two); mbar_init(&pempty[i], 1); }
+    for (int i = 0; i < kSPA; i++) { mbar_init(&pfullA[i], two); mbar_init(&pemptyA[i], 1); }
+    for (int i = 0; i < 2; i++) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], two); }
     for (int i = 0; i <= kMaxL; i++) mbar_init(&h_ready[i], 1);
     fence_mbar_init();
   }
-  if (warp == kWIss) { tmem_alloc(&s_tbase, kTmemCols); tmem_relinquish(); }
+  if (warp == kWIss) { tmem_alloc2(&s_tbase, kTmemCols); tmem_relinquish2(); }
   for (int i = threadIdx.x; i < kM * kPendWords; i += blockDim.x) s_pend[i] = 0;
   uint32_t* s_xch = s_pend + kM * kPendWords;                // [half][4][kM]
   // biases of every layer (32-bit float or int) once; the base potentials per tile (epilogue)
   uint32_t* s_bias = s_xch + kXchWords;
   uint32_t* s_ub = s_bias + a.soff[a.net.L + 1];
   uint2* s_g = reinterpret_cast<uint2*>(s_ub + a.soff[a.net.L + 1]);
+  uint8_t* s_gt = reinterpret_cast<uint8_t*>(s_g + ((a.goff[a.net.L + 1] + 1) & ~1)) + 64;   // 16-byte aligned
   if (a.staged)
     for (int l = 1; l <= L; l++)
       for (int j = threadIdx.x; j < a.net.sizes[l]; j += blockDim.x)
         s_bias[a.soff[l] + j] = static_cast<const uint32_t*>(a.net.b[l - 1])[j];
   fence_before();
-  __syncthreads();
+  cluster_sync();
   fence_after();
   const uint32_t tbase = s_tbase;
   uint8_t* scratch = a.scratch + (size_t)blockIdx.x * a.scratch_per_cta;
@@ -437,9 +498,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
     const bool eval = a.eval_idx != nullptr;
     uint32_t cseq = 0;
     uint32_t* pend = s_pend + r * kPendWords;
-    for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-      const TileInfo ti = tile_info(a, t);
-      const int etl = (int)((t - blockIdx.x) / gridDim.x);
+    for (uint64_t t = t_begin; t < t_end; t++) {
+      const TileInfo ti = tile_info(a, t, rank);
+      const int etl = (int)(t - t_begin);
       (void)etl;
       const uint64_t cidx = row_index(a, ti, r);
       // a row outside the restriction R (Philox spaces, k_restrict_mask) gets no verdict / coverage
@@ -861,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           KS(etl, l, ch, 15, 3);
           fence_before();
           named_bar(2, 256);
-          if (e == 0) mbar_arrive(&acc_empty[buf]);
+          if (e == 0) arrive_leader(&acc_empty[buf], rank);
           if (e == 0) KT(etl, 11 + (l == 1 ? ch : (l == 2 ? 4 + ch : 6)));
           cseq++;
         }
@@ -951,16 +1012,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
     }
     } else if (warp >= 16) {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtlL));
-  if (warp == kWProd) {
+  if (warp == kWProd || warp == kWProd2) {
+    const uint32_t pid = warp == kWProd ? 0u : 1u;
     // ------------------------------------------------------------------- producer
     if (lane == 0) {
-      // Layer 1 streams W tiles alone through kSPA slots of kWBytes laid over the whole
-      // [sPA, sPW) region; layers >= 2 stream (W, A) pairs through kSP slots (sPW, sPA).  The two
-      // layouts overlap, so a switch first drains the other layout's last stage (MMAs complete
-      // in order).
-      uint32_t ps = 0, psA = 0, hph[kMaxL + 1] = {0};
+      // Layer 1 streams W half tiles alone through kSPA slots of the ring region; layers >= 2
+      // stream (A, W half) stages through kSP slots.  The two layouts overlap, so a switch first
+      // drains the other layout's last stage (MMAs complete in order).  Each CTA loads the rows
+      // rank * nc/2 .. of every W tile (contiguous: whole 128-byte rows, 8-row swizzle groups).
+      uint32_t ps = 0, psA = 0, hph[kMaxL + 1] = {0}, q = 0;
       int lay_prev = -1;
-      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+      for (uint64_t t = t_begin; t < t_end; t++) {
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
           const uint32_t wbytes = (uint32_t)ld.nc * 128u;
@@ -977,28 +1039,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           for (int i = 0; i < ld.nchunks * ld.nkb; i++) {
             const int ch = paired ? 2 * (i / (2 * ld.nkb)) + (i & 1) : i / ld.nkb;
             const int kb = paired ? (i / 2) % ld.nkb : i % ld.nkb;
-            const uint32_t wb = (MLPV_EXP == 201 || MLPV_EXP == 204) ? 128u : wbytes;
+            const uint32_t wb = (MLPV_EXP == 201 || MLPV_EXP == 204) ? 128u : wbytes / 2;
+            const size_t woff = ((size_t)ch * ld.nkb + kb) * wbytes + rank * (wbytes / 2);
+            if ((q++ & 1u) != pid) { if (lay == 0) psA++; else ps++; continue; }   // the other producer's
             if (lay == 0) {
               const uint32_t st = psA % kSPA, ph = (psA / kSPA) & 1u;
+              KW((int)(t - t_begin), i, 0);
               mbar_wait(&pemptyA[st], ph ^ 1u);
               mbar_expect_tx(&pfullA[st], wb);
               const uint8_t* W = a.clamp ? a.W1h : ld.W;     // PHILOX_CLAMP: the fp16 copy of W1
-              bulk_g2s(sPA + st * kWBytes, W + ((size_t)ch * ld.nkb + kb) * wbytes, wb, &pfullA[st]);
+              bulk_g2s(sR + st * kWBytes, W + woff, wb, &pfullA[st]);
+              KW((int)(t - t_begin), i, 1);
               psA++;
             } else {
               const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
+              uint8_t* sa = sR + st * (kABytes + kWBytes);
               mbar_wait(&pempty[st], ph ^ 1u);
-              mbar_expect_tx(&pfull[st], wb + (l >= 2 ? kABytes : 0u));
-              bulk_g2s(sPW + st * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes, wb, &pfull[st]);
-              if (l >= 2) bulk_g2s(sPA + st * kABytes, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
+              mbar_expect_tx(&pfull[st], wb + kABytes);
+              bulk_g2s(sa + kABytes, ld.W + woff, wb, &pfull[st]);
+              bulk_g2s(sa, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
               ps++;
             }
           }
         }
       }
     }
+  } else if ((warp == kWIss || warp == kWRel2) && rank == 1) {
+    // ------------------------------------------------------------------- peer: relay its stages
+    // (its producer's bulk copies complete on the peer's own full barriers; the leader's issuer
+    // waits on the leader's, which count this arrive as the second of two); two relay threads take
+    // the stages in turn, like the two producers
+    if (lane == 0) {
+      const uint32_t pid = warp == kWIss ? 0u : 1u;
+      uint32_t ps = 0, psA = 0, q = 0;
+      for (uint64_t t = t_begin; t < t_end; t++)
+        for (int l = 1; l <= L; l++) {
+          const LayerDesc& ld = a.lay[l];
+          for (int i = 0; i < ld.nchunks * ld.nkb; i++) {
+            if ((q++ & 1u) != pid) { if (l == 1) psA++; else ps++; continue; }
+            if (l == 1) {
+              const uint32_t st = psA % kSPA, ph = (psA / kSPA) & 1u;
+              mbar_wait(&pfullA[st], ph);
+              mbar_arrive_cluster(&pfullA[st], 0);
+              psA++;
+            } else {
+              const uint32_t st = ps % kSP, ph = (ps / kSP) & 1u;
+              mbar_wait(&pfull[st], ph);
+              mbar_arrive_cluster(&pfull[st], 0);
+              ps++;
+            }
+          }
+        }
+    }
   } else if (warp == kWIss) {
-    // ------------------------------------------------------------------- MMA issuer
+    // ------------------------------------------------------------------- MMA issuer (leader)
     {
       // the whole warp runs the loop (descriptors stay warp-uniform, in uniform registers); one
       // elected lane issues the MMAs and commits.  A lane-0-only issuer spent ~900 cycles per
@@ -1006,13 +1100,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
       const bool el = elect_one();
       uint32_t gs = 0, ps = 0, psA = 0, cseq = 0;
       const bool i8 = a.net.numeric == MLPV_NUM_INT8;
-      for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-        const int tl = (int)((t - blockIdx.x) / gridDim.x);
+      for (uint64_t t = t_begin; t < t_end; t++) {
+        const int tl = (int)(t - t_begin);
         KT(tl, 0);
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
           const uint32_t bf1 = (l == 1 && !a.clamp) ? 1u : 0u;          // layer 1: bf16 x bf16, or f16 (clamp)
-          const uint32_t idesc = i8 ? idesc_i8(kM, ld.nc, 0, 1) : idesc_f16(kM, ld.nc, bf1, bf1);
+          const uint32_t idesc = i8 ? idesc_i8(2 * kM, ld.nc, 0, 1) : idesc_f16(2 * kM, ld.nc, bf1, bf1);
           if (l == 1 && (ld.nchunks & 1) == 0) {
             // chunk pairs: both accumulators, one generated A stage per K block (half the Philox work)
             for (int cp = 0; cp < ld.nchunks / 2; cp++) {
@@ -1023,44 +1117,62 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
 #ifdef MLPV_TRACE
               long long wg = 0, wp = 0;
 #endif
+              // Every cycle the issuing thread spends between two MMAs is a pipe bubble (the pipe
+              // takes a new MMA about when the previous one is under way), and a blocking mbarrier
+              // wait costs ~200 cycles even when the phase completed long ago (trace).  So the next
+              // stage's barriers are tested (non-blocking) between this stage's MMAs, and only a
+              // stage found not ready is waited for.
+              const uint32_t d0 = tbase + ((cseq & 1u) ? 256u : 0u), d1 = tbase + (((cseq + 1) & 1u) ? 256u : 0u);
+              bool rg = mbar_test(&gfull[gs % kSG], (gs / kSG) & 1u);
+              bool rp0 = mbar_test(&pfullA[psA % kSPA], (psA / kSPA) & 1u);
+              bool rp1 = mbar_test(&pfullA[(psA + 1) % kSPA], ((psA + 1) / kSPA) & 1u);
               for (int kb = 0; kb < ld.nkb; kb++) {
-                const uint32_t gst = gs % kSG;
+                const uint32_t gst = gs % kSG, p0 = psA % kSPA, p1 = (psA + 1) % kSPA;
 #ifdef MLPV_TRACE
                 const long long tw0 = clock64();
 #endif
-                mbar_wait(&gfull[gst], (gs / kSG) & 1u);
+                if (!rg) mbar_wait(&gfull[gst], (gs / kSG) & 1u);
 #ifdef MLPV_TRACE
                 wg += clock64() - tw0;
+                const long long tw1 = clock64();
 #endif
-#pragma unroll 1
-                for (int c = 0; c < 2; c++) {
-                  const uint32_t pst = psA % kSPA;
+                KW(tl, (int)(2 * ld.nkb * cp + 2 * kb), 2);
+                if (!rp0) mbar_wait(&pfullA[p0], (psA / kSPA) & 1u);
+                KW(tl, (int)(2 * ld.nkb * cp + 2 * kb), 3);
 #ifdef MLPV_TRACE
-                  const long long tw1 = clock64();
+                wp += clock64() - tw1;
 #endif
-                  mbar_wait(&pfullA[pst], (psA / kSPA) & 1u);
-#ifdef MLPV_TRACE
-                  wp += clock64() - tw1;
-#endif
-                  // (no tcgen05.fence::after_thread_sync per stage: the operands arrive through the
-                  // async proxy / proxy-fenced stores behind the mbarrier; a fence here stalled the
-                  // issue until the queued MMAs drained -- ~900 cycles per 4-MMA stage, trace)
-                  const uint32_t d = tbase + (MLPV_EXP == 205 ? 0u : ((cseq + c) & 1u) * 256u);
-                  const uint32_t abase = smem_u32(sG + gst * kABytes), bbase = smem_u32(sPA + pst * kWBytes);
+                // (no tcgen05.fence::after_thread_sync per stage: the operands arrive through the
+                // async proxy / proxy-fenced stores behind the mbarrier; a fence here stalled the
+                // issue until the queued MMAs drained -- ~900 cycles per 4-MMA stage, trace)
+                const uint32_t abase = smem_u32(sG + gst * kABytes);
+                const uint32_t b0 = smem_u32(sR + p0 * kWBytes), b1 = smem_u32(sR + p1 * kWBytes);
+                const bool more = kb + 1 < ld.nkb;
 #pragma unroll
-                  for (int kk = 0; kk < (MLPV_EXP == 206 ? 2 : 4); kk++) {
-                    const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
-                    const uint32_t acc = (kb | kk) ? 1u : 0u;
-                    if (el) { if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc); }
+                for (int kk = 0; kk < 4; kk++) {
+                  const uint32_t acc = (kb | kk) ? 1u : 0u;
+                  if (el) { if (i8) mma2_i8_ss(d0, sdesc_sw128(abase + 32u * kk), sdesc_sw128(b0 + 32u * kk), idesc, acc);
+                            else mma2_f16_ss(d0, sdesc_sw128(abase + 32u * kk), sdesc_sw128(b0 + 32u * kk), idesc, acc); }
+                  if (kk == 1) {                      // test ahead: this stage's second W tile, the next stage
+                    if (!rp1) rp1 = mbar_test(&pfullA[p1], ((psA + 1) / kSPA) & 1u);
+                    rg = more && mbar_test(&gfull[(gs + 1) % kSG], ((gs + 1) / kSG) & 1u);
+                    rp0 = more && mbar_test(&pfullA[(psA + 2) % kSPA], ((psA + 2) / kSPA) & 1u);
                   }
-                  if (el) mma_commit(&pemptyA[pst]);
-                  psA++;
                 }
-                if (el) mma_commit(&gempty[gst]);
+                if (!rp1) mbar_wait(&pfullA[p1], ((psA + 1) / kSPA) & 1u);
+#pragma unroll
+                for (int kk = 0; kk < (MLPV_EXP == 206 ? 2 : 4); kk++) {
+                  const uint32_t acc = (kb | kk) ? 1u : 0u;
+                  if (el) { if (i8) mma2_i8_ss(d1, sdesc_sw128(abase + 32u * kk), sdesc_sw128(b1 + 32u * kk), idesc, acc);
+                            else mma2_f16_ss(d1, sdesc_sw128(abase + 32u * kk), sdesc_sw128(b1 + 32u * kk), idesc, acc); }
+                  if (kk == 1) rp1 = more && mbar_test(&pfullA[(psA + 3) % kSPA], ((psA + 3) / kSPA) & 1u);
+                }
+                if (el) { mma2_commit(&pemptyA[p0], 0x3); mma2_commit(&pemptyA[p1], 0x3); mma2_commit(&gempty[gst], 0x3); }
+                psA += 2;
                 gs++;
               }
-              if (el) mma_commit(&acc_full[cseq & 1u]);
-              if (el) mma_commit(&acc_full[(cseq + 1) & 1u]);
+              if (el) mma2_commit(&acc_full[cseq & 1u], 0x3);
+              if (el) mma2_commit(&acc_full[(cseq + 1) & 1u], 0x3);
               KT(tl, 2 + 2 * (cp & 1));
 #ifdef MLPV_TRACE
               if (blockIdx.x == 0 && tl < 32) { g_kltrace[tl][20 + 2 * (cp & 1)] = wg; g_kltrace[tl][21 + 2 * (cp & 1)] = wp; }
@@ -1075,25 +1187,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
             if (ch == 0) KT(tl, 5 + 3 * (l - 2));
             fence_after();
             const uint32_t d = tbase + buf * 256u;
+            // (early non-blocking tests of the next stage, as in the chunk-pair loop above)
+            bool rp = l == 1 ? mbar_test(&pfullA[psA % kSPA], (psA / kSPA) & 1u) : mbar_test(&pfull[ps % kSP], (ps / kSP) & 1u);
+            bool rg = l == 1 && mbar_test(&gfull[gs % kSG], (gs / kSG) & 1u);
             for (int kb = 0; kb < ld.nkb; kb++) {
               const uint32_t pst = l == 1 ? psA % kSPA : ps % kSP;
-              if (l == 1) mbar_wait(&pfullA[pst], (psA / kSPA) & 1u);
-              else mbar_wait(&pfull[pst], (ps / kSP) & 1u);
+              if (!rp) { if (l == 1) mbar_wait(&pfullA[pst], (psA / kSPA) & 1u); else mbar_wait(&pfull[pst], (ps / kSP) & 1u); }
               if (ch == 0 && kb == 0) KT(tl, 6 + 3 * (l - 2));
               uint32_t gst = 0;
-              if (l == 1) { gst = gs % kSG; mbar_wait(&gfull[gst], (gs / kSG) & 1u); }
-              const uint32_t abase = smem_u32(l == 1 ? sG + gst * kABytes : sPA + pst * kABytes);
-              const uint32_t bbase = smem_u32(l == 1 ? sPA + pst * kWBytes : sPW + pst * kWBytes);
+              if (l == 1) { gst = gs % kSG; if (!rg) mbar_wait(&gfull[gst], (gs / kSG) & 1u); }
+              const uint32_t abase = smem_u32(l == 1 ? sG + gst * kABytes : sR + pst * (kABytes + kWBytes));
+              const uint32_t bbase = smem_u32(l == 1 ? sR + pst * kWBytes : sR + pst * (kABytes + kWBytes) + kABytes);
+              const bool more = kb + 1 < ld.nkb;
 #pragma unroll
               for (int kk = 0; kk < 4; kk++) {
                 const uint64_t ad = sdesc_sw128(abase + 32u * kk), bd = sdesc_sw128(bbase + 32u * kk);
                 const uint32_t acc = (kb | kk) ? 1u : 0u;
-                if (el) { if (i8) mma_i8_ss(d, ad, bd, idesc, acc); else mma_f16_ss(d, ad, bd, idesc, acc); }
+                if (el) { if (i8) mma2_i8_ss(d, ad, bd, idesc, acc); else mma2_f16_ss(d, ad, bd, idesc, acc); }
+                if (kk == 1) {
+                  if (l == 1) {
+                    rp = more && mbar_test(&pfullA[(psA + 1) % kSPA], ((psA + 1) / kSPA) & 1u);
+                    rg = more && mbar_test(&gfull[(gs + 1) % kSG], ((gs + 1) / kSG) & 1u);
+                  } else {
+                    rp = more && mbar_test(&pfull[(ps + 1) % kSP], ((ps + 1) / kSP) & 1u);
+                  }
+                }
               }
-              if (l == 1) { if (el) mma_commit(&pemptyA[pst]); if (el) mma_commit(&gempty[gst]); gs++; psA++; }
-              else { if (el) mma_commit(&pempty[pst]); ps++; }
+              if (l == 1) { if (el) mma2_commit(&pemptyA[pst], 0x3); if (el) mma2_commit(&gempty[gst], 0x3); gs++; psA++; }
+              else { if (el) mma2_commit(&pempty[pst], 0x3); ps++; }
             }
-            if (el) mma_commit(&acc_full[buf]);
+            if (el) mma2_commit(&acc_full[buf], 0x3);
             if (ch == ld.nchunks - 1) KT(tl, 7 + 3 * (l - 2));
             cseq++;
           }
@@ -1110,8 +1233,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
     const int r = threadIdx.x - 128 * ggrp;
     uint32_t gs = 0;
     const LayerDesc& l1 = a.lay[1];
-    for (uint64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-      const TileInfo ti = tile_info(a, t);
+    int gt_b = -1;
+    const uint32_t gt_addr = a.gtab ? smem_u32(s_gt) : 0u;
+    for (uint64_t t = t_begin; t < t_end; t++) {
+      const TileInfo ti = tile_info(a, t, rank);
+      if (a.gtab && ti.b != gt_b) {
+        // a new base: both groups have finished every stage of the previous one at the first
+        // barrier; the 256 generator threads then copy the base's table (16-byte words)
+        named_bar(10, 256);
+        const uint4* src = a.clamp ? a.ws.clampc + (size_t)ti.b * (a.gtab / 16)
+                                   : reinterpret_cast<const uint4*>(a.bases + (size_t)ti.b * a.gtab);
+        for (int i = threadIdx.x; i < a.gtab / 16; i += 256) reinterpret_cast<uint4*>(s_gt)[i] = __ldg(src + i);
+        named_bar(10, 256);
+        gt_b = ti.b;
+      }
+      const int gtl = (int)(t - t_begin);
+      (void)gtl;
       const int passes = (l1.nchunks & 1) == 0 ? l1.nchunks / 2 : l1.nchunks;   // chunk pairs share A
       for (int ch = 0; ch < passes; ch++)
         for (int kb = 0; kb < l1.nkb; kb++) {
@@ -1119,21 +1256,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_large(const __grid_constant__ L
           const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
           // one poller warp per group (with a short sleep between polls), the others wait in a
           // named barrier: spinning generators would take issue slots from the epilogue warps
+          KG(gtl, ch, kb, 0);
           if ((warp & 3) == 0) mbar_wait_sleep(&gempty[st], ph ^ 1u, 32);
           named_bar(ggrp ? 5 : 4, 128);
-          if (MLPV_EXP != 203 && MLPV_EXP != 204) gen_block(a, ti, r, kb, sG + st * kABytes);
+          KG(gtl, ch, kb, 1);
+          if (MLPV_EXP != 203 && MLPV_EXP != 204) gen_block(a, ti, r, kb, sG + st * kABytes, gt_addr);
+          KG(gtl, ch, kb, 2);
           fence_proxy_async();
           named_bar(ggrp ? 3 : 1, 128);
-          if (r == 0) mbar_arrive(&gfull[st]);
+          if (r == 0) arrive_leader(&gfull[st], rank);
+          KG(gtl, ch, kb, 3);
           gs++;
         }
     }
   }
   }
   fence_before();
-  __syncthreads();
+  cluster_sync();                     // the pair's MMAs, commits and remote arrives are all done
   fence_after();
-  if (warp == kWIss) tmem_dealloc(tbase, kTmemCols);
+  if (warp == kWIss) tmem_dealloc2(tbase, kTmemCols);
 }
 
 #ifdef MLPV_TRACE
@@ -1142,6 +1283,12 @@ extern "C" int mlpv_kl_trace_read(void* host) {
 }
 extern "C" int mlpv_kl_step_read(void* host) {
   return (int)cudaMemcpyFromSymbol(host, g_klstep, sizeof g_klstep);
+}
+extern "C" int mlpv_kl_w_read(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_klw, sizeof g_klw);
+}
+extern "C" int mlpv_kl_gen_read(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_klgen, sizeof g_klgen);
 }
 #endif
 
@@ -1324,14 +1471,15 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
   for (int k = 0; k <= kMaxL; k++) a.pair_of_lower[k] = -1;
   for (int p = 0; p < cov.n_pairs; p++) a.pair_of_lower[cov.lower[p]] = p;
   if (eval_idx) {
-    a.tiles_per_base = (uint64_t)((eval_n + kM - 1) / kM);
+    a.tiles_per_base = (uint64_t)((eval_n + 2 * kM - 1) / (2 * kM));
     a.n_tiles = a.tiles_per_base;
   } else {
-    a.tiles_per_base = (pert.end - pert.begin + kM - 1) / kM;
+    a.tiles_per_base = (pert.end - pert.begin + 2 * kM - 1) / (2 * kM);
     a.n_tiles = a.tiles_per_base * (uint64_t)n_base;
   }
   if (a.n_tiles == 0) return cudaSuccess;
-  const int grid = (int)(a.n_tiles < (uint64_t)num_sms ? a.n_tiles : (uint64_t)num_sms);
+  const uint64_t ncl = (uint64_t)(num_sms >= 4 ? num_sms / 2 : 1);     // CTA pairs (one CTA per SM)
+  const int grid = 2 * (int)(a.n_tiles < ncl ? a.n_tiles : ncl);
   a.scratch_per_cta = g.scratch_per_cta;
   if (!scratch) return cudaErrorInvalidValue;     // the handle's scratch: num_sms x scratch_per_cta, K padding zero
   a.scratch = static_cast<uint8_t*>(scratch);
@@ -1356,9 +1504,18 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
   a.goff[1] = 0;
   for (int l = 1; l <= net.L; l++) a.goff[l + 1] = a.goff[l] + (net.sizes[l] + 15) / 16;
   // biases + base potentials, the per-group table, + 16 words read past the end (masked)
-  const size_t stage_bytes = (size_t)2 * a.soff[net.L + 1] * 4 + (size_t)a.goff[net.L + 1] * 8 + 64;
+  const size_t stage_bytes = (size_t)2 * a.soff[net.L + 1] * 4 + (size_t)((a.goff[net.L + 1] + 1) & ~1) * 8 + 64;
   a.staged = kSmemBytes + stage_bytes <= (size_t)227 * 1024 ? 1 : 0;
-  const size_t smem = kSmemBytes + (a.staged ? stage_bytes : 0);
+  // the generators' per-base table (16-byte words; the base rows must be 16-byte aligned)
+  {
+    const int n0 = net.sizes[0];
+    int gt = 0;
+    if (a.clamp) gt = 32 * ((n0 + 7) / 8);
+    else if (net.numeric == MLPV_NUM_BF16) gt = (2 * n0) % 16 == 0 ? 2 * n0 : 0;
+    else gt = n0 % 16 == 0 ? n0 : 0;
+    if (a.staged && kSmemBytes + stage_bytes + gt <= (size_t)227 * 1024) a.gtab = gt;
+  }
+  const size_t smem = kSmemBytes + (a.staged ? stage_bytes + a.gtab : 0);
   cudaError_t e = cudaFuncSetAttribute(k_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_large<<<grid, kThreads, smem, st>>>(a);

@@ -10,8 +10,11 @@ using namespace mlpv::tc;
 __device__ __forceinline__ void mma1_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) { mma_f16_ss(d, a, b, idesc, acc); }
 
 __device__ unsigned int g_sink;
+__device__ uint4 g_src[2048];                       // 32 KB bulk-copy source (L2-resident)
+__device__ uint4 g_src2[1 << 19];                   // 8 MB bulk-copy source (mode 35)
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int reps, unsigned long long* cyc) {
+  constexpr bool ONE = MODE == 3 || MODE == 31 || MODE == 32 || MODE == 33 || MODE == 34 || MODE == 35;   // cta_group::1 M128 N256 (N16 for 31)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t ready, done, scratch[4], pre;
@@ -42,20 +45,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
     } else reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0, 0);
   }
   if (t == 0) {
-    mbar_init(&ready, (!(MODE == 3 || MODE == 31) && rank == 0) ? 2 : 1); mbar_init(&done, 1);
+    mbar_init(&ready, (!ONE && rank == 0) ? 2 : 1); mbar_init(&done, 1);
     for (int i = 0; i < 4; i++) mbar_init(&scratch[i], 1);
     mbar_init(&pre, 1);
     fence_mbar_init();
   }
-  if (w == 0) { if ((MODE == 3 || MODE == 31)) { tmem_alloc(&tbase, 512); tmem_relinquish(); } else { tmem_alloc2(&tbase, 512); tmem_relinquish2(); } }
+  if (w == 0) { if (ONE) { tmem_alloc(&tbase, 512); tmem_relinquish(); } else { tmem_alloc2(&tbase, 512); tmem_relinquish2(); } }
   fence_proxy_async();
   fence_before();
   cluster_sync();
   fence_after();
   const uint32_t tb = tbase;
-  if (t == 0) { if (rank == 0 || (MODE == 3 || MODE == 31)) mbar_arrive(&ready); else mbar_arrive_cluster(&ready, 0); }
+  if (t == 0) { if (rank == 0 || ONE) mbar_arrive(&ready); else mbar_arrive_cluster(&ready, 0); }
   if (t == 0) mbar_arrive(&pre);                       // phase 0 of `pre` completes: waits on it are no-ops
-  const bool issuer = ((MODE == 3 || MODE == 31)) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15 && MODE != 25 && MODE != 27);
+  const bool issuer = (ONE) ? (t == 0) : (rank == 0 && t == 0 && MODE != 15 && MODE != 25 && MODE != 27);
   __shared__ volatile int stop;
   if (t == 0) stop = 0;
   __syncthreads();
@@ -153,7 +156,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
     if ((t & 31) == 0 && w == 4 && blockIdx.x == 0) printf("  ld16 rate: %.1f cycles per ld16+wait (warp), %.1f B/clk/SM (4 warps)\n",
         (double)(t1 - t0) / n, 4.0 * n * 32 * 16 * 4 / (double)(t1 - t0));
     if (acc == 0x1234567u) g_sink = acc;
-  } else if ((w >= 4 && MODE >= 10 && MODE < 14) || (MODE == 28 && w >= 12)) {
+  } else if (MODE == 35 && w == 12) {
+    // background: a ring of 2 x 16 KB bulk copies in flight (from an 8 MB L2-resident source,
+    // block-dependent offsets), into a 32 KB smem scratch
+    __shared__ uint64_t rbar[2];
+    uint8_t* scratch = smem + 8 * 16384;
+    if (t == 384) { mbar_init(&rbar[0], 1); mbar_init(&rbar[1], 1); fence_mbar_init(); }
+    __syncwarp();
+    long long n = 0;
+    const long long t0 = clock64();
+    uint32_t ph[2] = {0, 0};
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(g_src2);
+    if (t == 384)
+      for (int i = 0; i < 2; i++) { mbar_expect_tx(&rbar[i], 16384); bulk_g2s(scratch + i * 16384, src + ((blockIdx.x * 7 + i) & 511) * 16384, 16384, &rbar[i]); }
+    while (!stop) {
+      const int i = (int)(n & 1);
+      mbar_wait(&rbar[i], ph[i]);
+      ph[i] ^= 1u;
+      n++;
+      if (t == 384) { mbar_expect_tx(&rbar[i], 16384); bulk_g2s(scratch + i * 16384, src + ((blockIdx.x * 7 + n + 1) & 511) * 16384, 16384, &rbar[i]); }
+      __syncwarp();
+    }
+    for (int i = 0; i < 2; i++) mbar_wait(&rbar[(n + i) & 1], ph[(n + i) & 1]);
+    const long long t1 = clock64();
+    if (t == 384 && blockIdx.x == 0) printf("  2 x 16 KB ring beside the MMAs: %.1f B/clk/SM\n", 16384.0 * n / (double)(t1 - t0));
+  } else if ((MODE == 33 || MODE == 34) && w == 12) {
+    // background: bulk copies of 32 KB from global (L2) into a smem scratch, back to back
+    __shared__ uint64_t cbar;
+    uint8_t* scratch = smem + 8 * 16384;
+    if (t == 384) { mbar_init(&cbar, 1); fence_mbar_init(); }
+    __syncwarp();
+    uint32_t ph = 0;
+    long long n = 0;
+    const long long t0 = clock64();
+    while (!stop) {
+      if (t == 384) {
+        mbar_expect_tx(&cbar, 32768);
+        bulk_g2s(scratch, reinterpret_cast<const uint8_t*>(g_src), 32768, &cbar);
+      }
+      __syncwarp();
+      mbar_wait(&cbar, ph);
+      ph ^= 1u;
+      n++;
+    }
+    const long long t1 = clock64();
+    if (t == 384 && blockIdx.x == 0) printf("  bulk g2s beside the MMAs: %.1f B/clk/SM\n", 32768.0 * n / (double)(t1 - t0));
+  } else if ((w >= 4 && MODE >= 10 && MODE < 14) || (MODE == 28 && w >= 12) || ((MODE == 32 || MODE == 34) && w >= 4 && w < 12)) {
     // background load while the MMAs run (warps 4..11)
     uint32_t c0 = t, c1 = t * 7, c2 = t * 13, c3 = t * 31, acc = 0;
     uint8_t* scratch = smem + 8 * 16384;                 // 32 KB scratch
@@ -168,7 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
         }
         acc += c0 ^ c2;
       }
-      if (MODE == 11 || MODE == 12 || MODE == 28) {
+      if (MODE == 11 || MODE == 12 || MODE == 28 || MODE == 32 || MODE == 34) {
 #pragma unroll
         for (int k = 0; k < 4; k++)
           *reinterpret_cast<uint4*>(scratch + ((t * 16 + (it * 4 + k) * 4096) & 32767)) = make_uint4(c0, c1, acc, it);
@@ -178,10 +226,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
     if (acc == 0x12345u) g_sink = acc;
   }
   if (issuer) {
-    if (!(MODE == 3 || MODE == 31)) mbar_wait_cluster(&ready, 0); else mbar_wait(&ready, 0);
+    if (!ONE) mbar_wait_cluster(&ready, 0); else mbar_wait(&ready, 0);
     fence_after();
     const uint32_t N = MODE == 2 ? 128 : ((MODE == 29 || MODE == 31) ? 16 : (MODE == 30 ? 64 : 256));
-    const uint32_t idesc = (MODE == 3 || MODE == 31) ? idesc_f16(128, N, 1, 1) : (MODE == 20 ? idesc_f16(256, N, 0, 0) : idesc_f16(256, N, 1, 1));
+    const uint32_t idesc = ONE ? idesc_f16(128, N, 1, 1) : (MODE == 20 ? idesc_f16(256, N, 0, 0) : idesc_f16(256, N, 1, 1));
     long long t0 = clock64();
     if (MODE == 21 || MODE == 22 || MODE == 23) {      // rings + per-stage readiness checks (k_fused3 issuer)
       uint32_t gsl = 0, wsl = 0;
@@ -232,26 +280,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768) k_bench(int rep
         }
         if (MODE == 4 || MODE == 6) { mma2_commit(&scratch[0], 0x3); mma2_commit(&scratch[1], 0x3); }
       }
-    if ((MODE == 3 || MODE == 31)) mma_commit(&done); else mma2_commit(&done, 0x3);
+    if (ONE) mma_commit(&done); else mma2_commit(&done, 0x3);
     mbar_wait(&done, 0);
     long long t1 = clock64();
     if (blockIdx.x == 0) *cyc = (unsigned long long)(t1 - t0);
   }
   if (t == 0) {                                        // stop the background warps of both CTAs
-    if (issuer || (MODE == 3 || MODE == 31)) stop = 1;
+    if (issuer || ONE) stop = 1;
   }
-  if (!(MODE == 3 || MODE == 31)) { if (t < 32 && !issuer) {} }
+  if (!ONE) { if (t < 32 && !issuer) {} }
   __syncwarp();
-  if (!issuer && t == 0 && !(MODE == 3 || MODE == 31) && MODE != 15 && MODE != 25 && MODE != 27) { mbar_wait(&done, 0); stop = 1; }
+  if (!issuer && t == 0 && !ONE && MODE != 15 && MODE != 25 && MODE != 27) { mbar_wait(&done, 0); stop = 1; }
   fence_before();
   __syncthreads();
   cluster_sync();
   fence_after();
-  if (w == 0) { if ((MODE == 3 || MODE == 31)) tmem_dealloc(tb, 512); else tmem_dealloc2(tb, 512); }
+  if (w == 0) { if (ONE) tmem_dealloc(tb, 512); else tmem_dealloc2(tb, 512); }
 }
 
 template <int MODE>
 void run(const char* name) {
+  constexpr bool ONE = MODE == 3 || MODE == 31 || MODE == 32 || MODE == 33 || MODE == 34 || MODE == 35;
   const size_t smem = (MODE == 13 || MODE >= 21 ? 13 : 10) * 16384 + 1024;
   cudaFuncSetAttribute(k_bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   unsigned long long* cyc;
@@ -259,7 +308,7 @@ void run(const char* name) {
   const int reps = 2000;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int nt = MODE == 28 ? 768 : (MODE >= 10 ? 384 : 128);
+  const int nt = (MODE == 28 || MODE >= 32) ? 768 : (MODE >= 10 ? 384 : 128);
   k_bench<MODE><<<148, nt, smem>>>(10, cyc);
   cudaEventRecord(e0);
   k_bench<MODE><<<148, nt, smem>>>(reps, cyc);
@@ -269,8 +318,8 @@ void run(const char* name) {
   cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long c = 0;
   cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
-  const double M = (MODE == 3 || MODE == 31) ? 128 : 256, N = MODE == 2 ? 128 : ((MODE == 29 || MODE == 31) ? 16 : (MODE == 30 ? 64 : 256));
-  const double groups = (MODE == 3 || MODE == 31) ? 148 : 74;
+  const double M = ONE ? 128 : 256, N = MODE == 2 ? 128 : ((MODE == 29 || MODE == 31) ? 16 : (MODE == 30 ? 64 : 256));
+  const double groups = ONE ? 148 : 74;
   const double flops = (MODE == 13 || (MODE >= 21 && MODE < 29)) ? 2.0 * M * N * 16 * 52 * (reps / 4) * groups : MODE == 13 ? 2.0 * M * N * 16 * 50 * (reps / 4) * groups : 2.0 * M * N * 16 * 16 * reps * groups;
   printf("%-28s err=%d  %.3f ms  %.1f TFLOP/s  cycles/MMA (cluster 0) %.1f\n", name, (int)e, ms, flops / (ms * 1e-3) / 1e12,
          (double)c / ((MODE >= 21 && MODE < 29) ? 52.0 * (reps / 4) : MODE == 13 ? 50.0 * (reps / 4) : 16.0 * reps));
@@ -282,5 +331,9 @@ int main() {
   run<29>("2CTA SS M256 N16 K16");
   run<30>("2CTA SS M256 N64 K16");
   run<31>("1CTA SS M128 N16 K16");
+  run<32>("1CTA M128 N256 + 8w STS");
+  run<33>("1CTA M128 N256 + bulk g2s");
+  run<34>("1CTA M128 N256 + STS + bulk");
+  run<35>("1CTA M128 N256 + 2x16KB ring");
   return 0;
 }

@@ -53,3 +53,29 @@ if hasattr(P.lib(), "mlpv_kl_step_read") and P.lib().mlpv_kl_step_read(st.ctypes
             steps = [(int(st[hh, ch, k, 0]) - t0s, int(st[hh, ch, k, 1]) - int(st[hh, ch, k, 0]),
                       int(st[hh, ch, k, 2]) - int(st[hh, ch, k, 1])) for k in range(16) if st[hh, ch, k, 0]]
             print(f"E1 tile 2 quad 0 half {hh} chunk {ch}: (start, ld, compute) per step {steps}; end {int(st[hh, ch, 15, 3]) - t0s}")
+
+gn = np.zeros((2, 48, 4), np.uint64)
+if hasattr(P.lib(), "mlpv_kl_gen_read") and P.lib().mlpv_kl_gen_read(gn.ctypes.data_as(C.c_void_p)) == 0:
+    for g in range(2):
+        ks = [k for k in range(48) if gn[g, k, 0]]
+        if not ks:
+            continue
+        w = [int(gn[g, k, 1]) - int(gn[g, k, 0]) for k in ks]
+        c = [int(gn[g, k, 2]) - int(gn[g, k, 1]) for k in ks]
+        f = [int(gn[g, k, 3]) - int(gn[g, k, 2]) for k in ks]
+        per = [int(gn[g, ks[i + 1], 0]) - int(gn[g, ks[i], 0]) for i in range(len(ks) - 1)]
+        med = lambda x: sorted(x)[len(x) // 2]
+        print(f"gen group {g} tile 2 pass 1: {len(ks)} stages; median wait {med(w)} compute {med(c)} fence+arrive {med(f)} stage-to-stage {med(per)}")
+        print(f"   waits {w[:24]}")
+
+wr = np.zeros((192, 4), np.uint64)
+if hasattr(P.lib(), "mlpv_kl_w_read") and P.lib().mlpv_kl_w_read(wr.ctypes.data_as(C.c_void_p)) == 0:
+    med = lambda x: sorted(x)[len(x) // 2] if x else None
+    ok = [i for i in range(192) if all(wr[i, e] for e in range(4))]
+    emp = [int(wr[i, 1]) - int(wr[i, 0]) for i in ok]
+    lat = [int(wr[i, 3]) - int(wr[i, 1]) for i in ok]
+    iw = [int(wr[i, 3]) - int(wr[i, 2]) for i in ok]
+    ahead = [int(wr[i, 2]) - int(wr[i, 1]) for i in ok]
+    print(f"W ring tile 2 (leader): {len(ok)} sub-stages; median producer empty-wait {med(emp)}, copy issue -> issuer sees full {med(lat)}, issuer wait {med(iw)}, copy issued before the issuer wanted it {med(ahead)}")
+    print("   issue->full", lat[:40])
+    print("   issuer wait", iw[:40])
