@@ -85,7 +85,11 @@ constexpr uint32_t kTmemCols = 512;       // two 256-column accumulator buffers
 constexpr int kPendWords = 32;            // per candidate: 16 sc + 16 vc words (upper width <= 512)
 constexpr int kXchWords = 2 * 4 * kM;     // epilogue halves' per-row partial results (4 words per row)
 constexpr size_t kRing = kSP * (kABytes + kWBytes);   // layer 1: kSPA W slots; layers >= 2: kSP (A, W) stages
-static_assert(kSPA * kWBytes <= kRing, "ring region");
+// float layers >= 2: stages [A_hi | A_lo | W chunk c | W chunk c+1] (the hi and lo halves of the
+// activations share one W tile: no duplicated [W | W] K rows, and a chunk pair shares both A tiles)
+constexpr int kSP2 = 2;
+constexpr uint32_t kStage2 = 2 * kABytes + 2 * kWBytes;
+static_assert(kSPA * kWBytes <= kRing && kSP2 * kStage2 <= kRing, "ring region");
 constexpr size_t kSmemBytes = 1024 + kSG * kABytes + kRing + (size_t)kM * kPendWords * 4 + 4 * kXchWords;
 
 struct LayerDesc {
@@ -443,6 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
   uint8_t* sR = sG + kSG * kABytes;                          // ring region: layer 1 [kSPA][kWBytes];
                                                              // layers >= 2 [kSP][A kABytes | W kWBytes]
   uint32_t* s_pend = reinterpret_cast<uint32_t*>(sR + kRing);   // [kM][kPendWords]
+  __shared__ uint64_t pfull2[kSP2], pempty2[kSP2];
   __shared__ uint64_t gfull[kSG], gempty[kSG], pfull[kSP], pempty[kSP], pfullA[kSPA], pemptyA[kSPA], acc_full[2],
       acc_empty[2], h_ready[kMaxL + 1];
   __shared__ uint32_t s_tbase;
@@ -461,6 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
     for (int i = 0; i < kSG; i++) { mbar_init(&gfull[i], two); mbar_init(&gempty[i], 1); }
     for (int i = 0; i < kSP; i++) { mbar_init(&pfull[i], two); mbar_init(&pempty[i], 1); }
     for (int i = 0; i < kSPA; i++) { mbar_init(&pfullA[i], two); mbar_init(&pemptyA[i], 1); }
+    for (int i = 0; i < kSP2; i++) { mbar_init(&pfull2[i], two); mbar_init(&pempty2[i], 1); }
     for (int i = 0; i < 2; i++) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], two); }
     for (int i = 0; i <= kMaxL; i++) mbar_init(&h_ready[i], 1);
     fence_mbar_init();
@@ -1020,19 +1026,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
       // stream (A, W half) stages through kSP slots.  The two layouts overlap, so a switch first
       // drains the other layout's last stage (MMAs complete in order).  Each CTA loads the rows
       // rank * nc/2 .. of every W tile (contiguous: whole 128-byte rows, 8-row swizzle groups).
-      uint32_t ps = 0, psA = 0, hph[kMaxL + 1] = {0}, q = 0;
+      uint32_t ps = 0, psA = 0, ps2 = 0, hph[kMaxL + 1] = {0}, q = 0;
       int lay_prev = -1;
+      const bool fl = a.net.numeric == MLPV_NUM_BF16;
       for (uint64_t t = t_begin; t < t_end; t++) {
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
           const uint32_t wbytes = (uint32_t)ld.nc * 128u;
-          const int lay = l == 1 ? 0 : 1;
+          const int lay = l == 1 ? 0 : (fl ? 2 : 1);
           if (lay != lay_prev) {
             if (lay_prev == 0 && psA > 0) mbar_wait(&pemptyA[(psA - 1) % kSPA], ((psA - 1) / kSPA) & 1u);
             if (lay_prev == 1 && ps > 0) mbar_wait(&pempty[(ps - 1) % kSP], ((ps - 1) / kSP) & 1u);
+            if (lay_prev == 2 && ps2 > 0) mbar_wait(&pempty2[(ps2 - 1) % kSP2], ((ps2 - 1) / kSP2) & 1u);
             lay_prev = lay;
           }
           if (l >= 2) { mbar_wait(&h_ready[l - 1], hph[l - 1]); hph[l - 1] ^= 1u; }
+          if (lay == 2) {
+            // float layer >= 2: per W K block one stage of A_hi, A_lo (this CTA's rows of the
+            // previous layer's [hi | lo] activations) and the W half tiles of one or two chunks
+            const int pr = (ld.nchunks & 1) == 0 ? 2 : 1;
+            const uint32_t wb = (MLPV_EXP == 201 || MLPV_EXP == 204) ? 128u : wbytes / 2;
+            const uint8_t* hsrc = scratch + a.h_off[l - 1];
+            for (int cp = 0; cp < ld.nchunks / pr; cp++)
+              for (int kb = 0; kb < ld.nkb; kb++) {
+                if ((q++ & 1u) != pid) { ps2++; continue; }
+                const uint32_t st = ps2 % kSP2, ph = (ps2 / kSP2) & 1u;
+                uint8_t* sb = sR + st * kStage2;
+                mbar_wait(&pempty2[st], ph ^ 1u);
+                mbar_expect_tx(&pfull2[st], 2 * kABytes + pr * wb);
+                bulk_g2s(sb, hsrc + (size_t)kb * kABytes, kABytes, &pfull2[st]);
+                bulk_g2s(sb + kABytes, hsrc + (size_t)(ld.nkb + kb) * kABytes, kABytes, &pfull2[st]);
+                for (int c = 0; c < pr; c++) {
+                  const int ch = pr * cp + c;
+                  bulk_g2s(sb + 2 * kABytes + c * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes + rank * (wbytes / 2), wb, &pfull2[st]);
+                }
+                ps2++;
+              }
+            continue;
+          }
           // layer 1 with an even chunk count runs the chunks in pairs on one generated A stage:
           // W stages in the order (pair, kb, chunk of the pair)
           const bool paired = l == 1 && (ld.nchunks & 1) == 0;
@@ -1071,10 +1102,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
     // the stages in turn, like the two producers
     if (lane == 0) {
       const uint32_t pid = warp == kWIss ? 0u : 1u;
-      uint32_t ps = 0, psA = 0, q = 0;
+      const bool fl = a.net.numeric == MLPV_NUM_BF16;
+      uint32_t ps = 0, psA = 0, ps2 = 0, q = 0;
       for (uint64_t t = t_begin; t < t_end; t++)
         for (int l = 1; l <= L; l++) {
           const LayerDesc& ld = a.lay[l];
+          if (l >= 2 && fl) {
+            const int pr = (ld.nchunks & 1) == 0 ? 2 : 1;
+            for (int i = 0; i < (ld.nchunks / pr) * ld.nkb; i++) {
+              if ((q++ & 1u) != pid) { ps2++; continue; }
+              const uint32_t st = ps2 % kSP2, ph = (ps2 / kSP2) & 1u;
+              mbar_wait(&pfull2[st], ph);
+              mbar_arrive_cluster(&pfull2[st], 0);
+              ps2++;
+            }
+            continue;
+          }
           for (int i = 0; i < ld.nchunks * ld.nkb; i++) {
             if ((q++ & 1u) != pid) { if (l == 1) psA++; else ps++; continue; }
             if (l == 1) {
@@ -1098,7 +1141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
       // elected lane issues the MMAs and commits.  A lane-0-only issuer spent ~900 cycles per
       // 4-MMA stage moving per-lane operands into uniform registers (trace).
       const bool el = elect_one();
-      uint32_t gs = 0, ps = 0, psA = 0, cseq = 0;
+      uint32_t gs = 0, ps = 0, psA = 0, ps2 = 0, cseq = 0;
       const bool i8 = a.net.numeric == MLPV_NUM_INT8;
       for (uint64_t t = t_begin; t < t_end; t++) {
         const int tl = (int)(t - t_begin);
@@ -1178,6 +1221,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
               if (blockIdx.x == 0 && tl < 32) { g_kltrace[tl][20 + 2 * (cp & 1)] = wg; g_kltrace[tl][21 + 2 * (cp & 1)] = wp; }
 #endif
               cseq += 2;
+            }
+            continue;
+          }
+          if (l >= 2 && !i8) {
+            // float layer >= 2: per stage and chunk, 4 MMAs on A_hi then 4 on A_lo against the
+            // same W half tiles (u = u_base + W (hi + lo)); chunk pairs share the A tiles
+            const int pr = (ld.nchunks & 1) == 0 ? 2 : 1;
+            for (int cp = 0; cp < ld.nchunks / pr; cp++) {
+              for (int c = 0; c < pr; c++) mbar_wait(&acc_empty[(cseq + c) & 1u], (((cseq + c) >> 1) & 1u) ^ 1u);
+              if (cp == 0) KT(tl, 5 + 3 * (l - 2));
+              fence_after();
+              bool rp = mbar_test(&pfull2[ps2 % kSP2], (ps2 / kSP2) & 1u);
+              for (int kb = 0; kb < ld.nkb; kb++) {
+                const uint32_t st = ps2 % kSP2;
+                if (!rp) mbar_wait(&pfull2[st], (ps2 / kSP2) & 1u);
+                if (cp == 0 && kb == 0) KT(tl, 6 + 3 * (l - 2));
+                const uint32_t sb = smem_u32(sR + st * kStage2);
+                const bool more = kb + 1 < ld.nkb;
+                for (int c = 0; c < pr; c++) {
+                  const uint32_t d = tbase + (((cseq + c) & 1u) ? 256u : 0u);
+                  const uint32_t wbase = sb + 2 * kABytes + c * kWBytes;
+#pragma unroll
+                  for (int h = 0; h < 2; h++)
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                      const uint32_t acc = (kb | h | kk) ? 1u : 0u;
+                      if (el) mma2_f16_ss(d, sdesc_sw128(sb + h * kABytes + 32u * kk), sdesc_sw128(wbase + 32u * kk), idesc, acc);
+                      if (c == 0 && h == 0 && kk == 1) rp = more && mbar_test(&pfull2[(ps2 + 1) % kSP2], ((ps2 + 1) / kSP2) & 1u);
+                    }
+                }
+                if (el) mma2_commit(&pempty2[st], 0x3);
+                ps2++;
+              }
+              for (int c = 0; c < pr; c++) if (el) mma2_commit(&acc_full[(cseq + c) & 1u], 0x3);
+              if (cp == ld.nchunks / pr - 1) KT(tl, 7 + 3 * (l - 2));
+              cseq += pr;
             }
             continue;
           }
@@ -1316,7 +1395,7 @@ static bool geometry(const DevNet& net, LargeGeom* g, std::string* why) {
     d.nchunks = d.npad / d.nc;
     const int kin = net.sizes[l - 1];
     int kbytes;
-    if (fl) kbytes = l == 1 ? 2 * kin : 4 * pad_to(kin, 64);   // [hi | lo] fp16 for l >= 2
+    if (fl) kbytes = 2 * (l == 1 ? kin : pad_to(kin, 64));   // fp16 (l >= 2: the A operand is [hi | lo])
     else kbytes = kin;
     d.nkb = (kbytes + 127) / 128;
     d.lo_kb = fl ? pad_to(d.n, 64) / 64 : 0;
@@ -1327,7 +1406,7 @@ static bool geometry(const DevNet& net, LargeGeom* g, std::string* why) {
   }
   for (int l = 1; l < L; l++) {
     g->h_off[l] = off;
-    off += (size_t)g->lay[l + 1].nkb * kABytes;
+    off += (size_t)(fl ? 2 : 1) * g->lay[l + 1].nkb * kABytes;   // float: hi blocks, then lo blocks
   }
   g->scratch_per_cta = (off + 1023) & ~size_t(1023);
   g->w_total = wo;
@@ -1401,7 +1480,6 @@ cudaError_t prepare_large(const DevNet& net, const void* const* W_host, const vo
           memcpy(&f, &u, 4);
           const uint16_t h = host_f2h(f);          // exact for |w| >= 2^-17 (C19)
           put(2 * k, reinterpret_cast<const uint8_t*>(&h), 2);
-          put(2 * (pad_to(kin, 64) + k), reinterpret_cast<const uint8_t*>(&h), 2);
         }
       }
     }
