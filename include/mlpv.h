@@ -243,6 +243,12 @@ typedef struct {
     double gamma;          /* radius of the outer ball, finite > 0 (real pixel units as restrict_l2) */
     int32_t max_bound;     /* >= 1 */
     int32_t granularity;   /* >= 1 */
+    int32_t early_exit;    /* 0: one enumeration of the gamma ball, keys (step, index);
+                            * 1: the loop's own order with early exit: pass i
+                            *    checks only the shell b_(i-1) < delta <= b_i of every base input not
+                            *    yet decided (a base is decided once an unflagged violation is found),
+                            *    so a base input's work stops at its counterexample's iteration */
+    int32_t reserved;      /* 0 */
 } mlpv_incremental;
 
 /* n_steps of the schedule (0 if inc is NULL or invalid). */
@@ -256,7 +262,10 @@ double mlpv_incremental_bound(const mlpv_incremental *inc, int32_t i);
  * safe after n_steps iterations), first_cex[b] = the lowest index among the violating candidates
  * inside b_step -- what the loop reports at that iteration.  step_unflagged / first_cex_unflagged:
  * the same over unflagged violations (float numerics, reading C20).  The other result fields are
- * those of mlpv_check with restrict_l2 = gamma (pert->restrict_l2 is ignored).  Subset / tuple
+ * those of mlpv_check with restrict_l2 = gamma (pert->restrict_l2 is ignored) -- with early_exit = 1,
+ * those of mlpv_check with restrict_l2 = b_(s_b) for each base input b, s_b = step_unflagged[b] if
+ * nonzero else n_steps: the ball the paper's loop had checked when it stopped for b;
+ * step / first_cex / step_unflagged / first_cex_unflagged are the same in both modes.  Subset / tuple
  * spaces with index_end <= 2^48 and n_steps <= 2048; MLPV_E_UNSUPPORTED otherwise.  Errors as
  * mlpv_check, plus MLPV_E_INVALID for a NULL / invalid inc or NULL step arrays. */
 mlpv_status mlpv_check_incremental(mlpv_t h, const void *base_inputs, int32_t n_base, const mlpv_pert *pert,

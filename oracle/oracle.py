@@ -273,6 +273,9 @@ def incremental_verify(cfg, gamma: float, max_bound: int, granularity: int = 1, 
     first = np.full(n, none, np.uint64)
     first_u = np.full(n, none, np.uint64)
     it = 0
+    # counts of the last ball checked for each base input: the ball of its deciding iteration, or
+    # of the last iteration run (the early-exit mode of the library reports these)
+    fin = {k: np.zeros(n, np.uint64) for k in ("checked", "violated", "flagged")}
     for i, b in enumerate(bounds, 1):
         it = i
         c = copy.copy(cfg)
@@ -284,10 +287,13 @@ def incremental_verify(cfg, gamma: float, max_bound: int, granularity: int = 1, 
                 step[j], first[j] = i, r.first_cex[j]
             if step_u[j] == 0 and r.first_cex_unflagged[j] != none:
                 step_u[j], first_u[j] = i, r.first_cex_unflagged[j]
+            if step_u[j] in (0, i):
+                for k in fin:
+                    fin[k][j] = getattr(r, k)[j]
         if np.all(step_u > 0):
             break                                   # every base input decided
     return {"step": step, "first_cex": first, "step_unflagged": step_u, "first_cex_unflagged": first_u,
-            "bounds": bounds, "iterations": it}
+            "bounds": bounds, "iterations": it, "final": fin}
 
 
 def pair_coverage(net, images, pairs, d_value: float, d_distance: float,

@@ -61,7 +61,8 @@ class _Cov(C.Structure):
 
 
 class _Inc(C.Structure):
-    _fields_ = [("gamma", C.c_double), ("max_bound", C.c_int32), ("granularity", C.c_int32)]
+    _fields_ = [("gamma", C.c_double), ("max_bound", C.c_int32), ("granularity", C.c_int32),
+                ("early_exit", C.c_int32), ("reserved", C.c_int32)]
 
 
 class _Res(C.Structure):
@@ -273,9 +274,11 @@ class Checker:
         return r
 
     def check_incremental(self, bases, pert, prop, cov, gamma: float, max_bound: int, granularity: int = 1,
-                          tau=None, stream=None) -> Dict:
+                          tau=None, stream=None, early_exit: bool = False) -> Dict:
         """mlpv_check_incremental: the check's result dict plus "step" / "step_unflagged" (CUDA
-        int32 [n_base]; 1-based iteration of the incremental loop, 0 = none in the gamma ball)."""
+        int32 [n_base]; 1-based iteration of the incremental loop, 0 = none in the gamma ball).
+        early_exit: the loop's own order, one shell per pass, a base input's work ending at its
+        counterexample's iteration (the counts / coverage are then those of that ball)."""
         import torch
         n_base = int(bases.shape[0])
         nw, _ = self.coverage_layout(cov)
@@ -286,7 +289,7 @@ class Checker:
         p = _mk_pert(pert, keep)
         pr = _Prop(prop.kind, prop.target, float(prop.V))
         c = _mk_cov(cov, keep, tau)
-        inc = _Inc(float(gamma), int(max_bound), int(granularity))
+        inc = _Inc(float(gamma), int(max_bound), int(granularity), 1 if early_exit else 0, 0)
         rs = _res_struct(r)
         if nw == 0:
             rs.cov_all = None

@@ -519,6 +519,11 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
   __shared__ unsigned long long s_cnt[3];
   __shared__ unsigned long long s_cex[2];
 
+  // early-exit pass (NEXT-2): a base input decided at an earlier step has nothing left to check
+  if (a.pert.shell > 0 && !eval) {
+    const unsigned long long k = a.pert.decided[b];
+    if (k != kNone && (int)(k >> kStepShift) < a.pert.shell) return;      // uniform over the block
+  }
   // ---- stage per-base data
   for (int t = threadIdx.x; t < T; t += blockDim.x) s_base[t] = static_cast<const P*>(a.ws.trace)[(size_t)b * T + t];
   {
@@ -694,6 +699,14 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
       }
       if (!inside) continue;                           // outside R: no verdict, no coverage
     }
+    // incremental bounds (NEXT-2): the step of the smallest ball b_i holding the candidate
+    int cstep = 0;
+    if (a.pert.n_steps > 0 && !eval) {
+      cstep = 1;
+      if constexpr (FL) { while (cstep < a.pert.n_steps && rs2_f > a.pert.step_r2_f[cstep - 1]) cstep++; }
+      else { while (cstep < a.pert.n_steps && rs2_i > a.pert.step_r2_raw[cstep - 1]) cstep++; }
+      if (a.pert.shell > 0 && cstep != a.pert.shell) continue;   // early-exit pass: this shell only
+    }
     // ---- a5/a6: hidden activations and dense layers
     {
       float h1f[M1]; int32_t h1i[M1]; uint32_t h1p[(M1 + 3) / 4];
@@ -754,12 +767,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
     if (viol) {
       my_v++;
       unsigned long long key = c;
-      if (a.pert.n_steps > 0) {                       // incremental bounds (NEXT-2): key = (step, index)
-        int st = 1;
-        if constexpr (FL) { while (st < a.pert.n_steps && rs2_f > a.pert.step_r2_f[st - 1]) st++; }
-        else { while (st < a.pert.n_steps && rs2_i > a.pert.step_r2_raw[st - 1]) st++; }
-        key |= (unsigned long long)st << kStepShift;
-      }
+      if (a.pert.n_steps > 0) key |= (unsigned long long)cstep << kStepShift;   // key = (step, index)
       if (key < my_cex) my_cex = key;
       if (!flag && key < my_cexu) my_cexu = key;
     }

@@ -666,6 +666,8 @@ static mlpv_status check_impl(mlpv_t h, const void* base_inputs, int32_t n_base,
   if (inc) {
     if (!(inc->gamma > 0) || !std::isfinite(inc->gamma)) return fail(h, MLPV_E_INVALID, "inc.gamma = %g (finite, > 0)", inc->gamma);
     if (inc->max_bound < 1 || inc->granularity < 1) return fail(h, MLPV_E_INVALID, "inc.max_bound / granularity must be >= 1");
+    if ((inc->early_exit != 0 && inc->early_exit != 1) || inc->reserved != 0)
+      return fail(h, MLPV_E_INVALID, "inc.early_exit = %d (0 or 1), inc.reserved = %d (0)", inc->early_exit, inc->reserved);
     const int n_steps = mlpv_incremental_steps(inc);
     if (n_steps > kMaxSteps) return fail(h, MLPV_E_INVALID, "inc: %d steps (max %d)", n_steps, kMaxSteps);
     if (is_philox(pert->kind))
@@ -726,6 +728,20 @@ static mlpv_status check_impl(mlpv_t h, const void* base_inputs, int32_t n_base,
     }
     cudaFreeAsync(mask, st);
     if (rs != MLPV_OK) return rs;
+  } else if (pert->index_begin != pert->index_end && inc && inc->early_exit) {
+    // the loop's own order (NEXT-2 early exit): pass i checks the shell
+    // b_(i-1) < delta <= b_i of the base inputs not decided by passes 1 .. i-1 (the unflagged keys
+    // in first_cex_unflagged, stream-ordered); a decided base's blocks return at once, so the
+    // passes after the last decision cost a launch each and no host synchronisation is needed
+    dp.decided = reinterpret_cast<const unsigned long long*>(dr.first_cex_unflagged);
+    const cudaEvent_t ev0 = h->ev_begin;              // mlpv_profile brackets all the passes
+    for (int i = 1; i <= dp.n_steps && s == MLPV_OK; i++) {
+      dp.shell = i;
+      s = run_kernel(h, base_inputs, n_base, pert, dp, dprop, dc, dr, plan, nullptr, 0, 0, nullptr, st);
+      h->ev_begin = nullptr;
+    }
+    h->ev_begin = ev0;
+    if (s != MLPV_OK) return s;
   } else if (pert->index_begin != pert->index_end) {
     if ((s = run_kernel(h, base_inputs, n_base, pert, dp, dprop, dc, dr, plan, nullptr, 0, 0, nullptr, st)) != MLPV_OK)
       return s;

@@ -71,6 +71,11 @@ struct DevPert {
   int n_steps;                // 0 = off
   const double* step_r2_f;    // device [n_steps] b_i^2 (float numerics)
   const long long* step_r2_raw;  // device [n_steps] floor(b_i^2 S^2) (fixed point)
+  // early-exit passes (mlpv_incremental.early_exit): this pass checks only the candidates of step
+  // `shell` (b_(shell-1) < delta <= b_shell) of the base inputs whose unflagged key in `decided`
+  // (the result's first_cex_unflagged) is not from an earlier step; 0 = off
+  int shell;
+  const unsigned long long* decided;
 };
 constexpr int kStepShift = 48;   // candidate indices < 2^48 in incremental mode
 constexpr int kMaxSteps = 2048;

@@ -25,13 +25,16 @@ def P():
     return P
 
 
-def _gpu(P, cfg, gamma, mb, g):
+def _gpu(P, cfg, gamma, mb, g, early_exit=False):
     chk = P.Checker(cfg.net)
     try:
-        r = chk.check_incremental(to_device_bases(cfg), cfg.pert, cfg.prop, cfg.cov, gamma, mb, g)
+        r = chk.check_incremental(to_device_bases(cfg), cfg.pert, cfg.prop, cfg.cov, gamma, mb, g,
+                                  early_exit=early_exit)
         out = {k: r[k][:cfg.n_base].cpu().numpy() for k in ("step", "step_unflagged")}
-        for k in ("first_cex", "first_cex_unflagged", "checked", "violated"):
+        for k in ("first_cex", "first_cex_unflagged", "checked", "violated", "flagged"):
             out[k] = r[k][:cfg.n_base].cpu().numpy().view(np.uint64)
+        nw = r["n_words"]
+        out["cov_all"] = r["cov_all"][:nw].cpu().numpy().view(np.uint32) if nw else np.zeros(0, np.uint32)
         return out
     finally:
         chk.close()
@@ -112,3 +115,57 @@ def test_rejections(P):
         _gpu(P, c4, 0.5, 4, 1)
     assert e.value.status == 3
     torch.cuda.synchronize()
+
+
+def _final_cov(oracle_mod, cfg, o):
+    """OR over the base inputs of the coverage of the ball each one stopped at (oracle only)."""
+    import copy
+    acc = None
+    for j in range(cfg.n_base):
+        s = int(o["step_unflagged"][j]) or len(o["bounds"])
+        c = cfg.subset(n_base=1, base_start=j, begin=cfg.pert.index_begin, end=cfg.pert.index_end)
+        c.pert = copy.copy(c.pert)
+        c.pert.restrict_l2 = o["bounds"][s - 1]
+        w = np.asarray(oracle_mod.check(c).cov_all, np.uint32)
+        acc = w if acc is None else acc | w
+    return acc
+
+
+@pytest.mark.parametrize("g", [1, 3])
+def test_early_exit_gamma_workload_q412(P, oracle_mod, g):
+    """NEXT-2 early exit (the loop's own order, one shell per pass): the (step, index) results equal
+    the one-enumeration keys and the oracle's loop bit for bit; checked / violated per base input and
+    the coverage words are those of the ball each base's loop stopped at (oracle: restricted checks
+    at b_(s_b))."""
+    cfg = M.gamma_config(50)
+    r = _gpu(P, cfg, 3.0, 12, g, early_exit=True)
+    o = oracle_mod.incremental_verify(cfg, 3.0, 12, g)
+    _exact(r, o)
+    one = _gpu(P, cfg, 3.0, 12, g)
+    _exact(r, one)
+    assert np.array_equal(r["checked"], o["final"]["checked"]), (r["checked"], o["final"]["checked"])
+    assert np.array_equal(r["violated"], o["final"]["violated"])
+    decided = r["step"] > 0
+    assert decided.any() and (r["checked"][decided] < one["checked"][decided]).any()   # work saved
+    assert np.array_equal(r["cov_all"], _final_cov(oracle_mod, cfg, o))
+
+
+def test_early_exit_threshold_and_int8(P, oracle_mod):
+    from tests.test_oracle_pins import _flip_cfg
+    cfg = _flip_cfg()
+    r = _gpu(P, cfg, 0.5, 10, 1, early_exit=True)
+    assert (int(r["step"][0]), int(r["first_cex"][0]), int(r["checked"][0]), int(r["violated"][0])) == (4, 18, 9, 1)
+    cfg = M.make_config("cfg3").subset(n_base=3, begin=0, end=60_000)
+    r = _gpu(P, cfg, 1.0, 5, 1, early_exit=True)
+    o = oracle_mod.incremental_verify(cfg, 1.0, 5, 1)
+    _exact(r, o)
+    assert np.array_equal(r["checked"], o["final"]["checked"]) and np.array_equal(r["violated"], o["final"]["violated"])
+
+
+def test_early_exit_fp32_cfg1(P, oracle_mod):
+    cfg = M.make_config("cfg1")
+    r = _gpu(P, cfg, 1.4, 7, 1, early_exit=True)
+    o = oracle_mod.incremental_verify(cfg, 1.4, 7, 1)
+    _float_rule(r, o)
+    same = r["step_unflagged"] == o["step_unflagged"]
+    assert np.array_equal(r["checked"][same], o["final"]["checked"][same])

@@ -918,3 +918,27 @@ def test_incremental_threshold_net(oracle_mod):
     assert int(r["step"][0]) == 0 and r["iterations"] == 10
     r = O.incremental_verify(_flip_cfg((0.4, 0.4)), 0.5, 10, 1)
     assert int(r["step"][0]) == 0
+
+
+def test_incremental_final_ball_counts(oracle_mod):
+    """The counts of the ball the loop stopped at (what the early-exit mode reports): brute force
+    over the 25 grid points of the threshold net.  g = 1 stops at b_4 = 0.2: the points with
+    offsets a^2 + b^2 <= 0.04 are (0,0), the four (+-0.125, 0) / (0, +-0.125) and the four
+    (+-0.125, +-0.125) = 9, of which only (0.525, 0.525) (c = 18) flips; gamma = 0.17 never
+    decides and stops at b_10 = 0.17: the same 9 points minus the diagonal ones (0.177 > 0.17) = 5,
+    none violated."""
+    O = oracle_mod
+    cfg = _flip_cfg()
+    lv = np.array(cfg.pert.levels, np.float32).astype(np.float64)
+    x = float(np.float32(0.4))
+
+    def brute(bound):
+        pts = [(i, j) for i in range(5) for j in range(5) if (lv[i] - x) ** 2 + (lv[j] - x) ** 2 <= bound * bound]
+        return len(pts), sum(1 for i, j in pts if np.float32(lv[i]) + np.float32(lv[j]) > 1)
+
+    r = O.incremental_verify(cfg, 0.5, 10, 1)
+    assert brute(0.2) == (9, 1)
+    assert (int(r["final"]["checked"][0]), int(r["final"]["violated"][0])) == (9, 1)
+    r = O.incremental_verify(cfg, 0.17, 10, 1)
+    assert brute(0.17) == (5, 0)
+    assert (int(r["final"]["checked"][0]), int(r["final"]["violated"][0])) == (5, 0)

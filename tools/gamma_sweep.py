@@ -66,6 +66,17 @@ def main():
     for i, b in enumerate(sched, 1):
         print(f"  step {i:3d}  b = {b:6.3f}  bases {int((st == i).sum()):4d}")
     print(f"  safe over the grid: {int((st == 0).sum())}")
+    # the same loop in its own order with early exit (one shell per pass, decided bases stop)
+    for ee in (False, True):
+        chk.check_incremental(bases, cfg.pert, cfg.prop, cfg.cov, max(gs), mb, 1, early_exit=ee)   # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r2 = chk.check_incremental(bases, cfg.pert, cfg.prop, cfg.cov, max(gs), mb, 1, early_exit=ee)
+        st2 = r2["step"].cpu().numpy()
+        dt = (time.perf_counter() - t0) * 1e3
+        assert np.array_equal(st2, st)
+        print(f"incremental early_exit={int(ee)}: {dt:.2f} ms, candidates checked "
+              f"{int(r2['checked'][:cfg.n_base].cpu().numpy().view(np.uint64).sum())}")
 
 
 if __name__ == "__main__":
