@@ -59,20 +59,65 @@ __device__ __forceinline__ float row_dot_f(const void* W, int numeric, int row, 
 }
 __device__ __forceinline__ int32_t row_dot_i(const void* W, int numeric, int row, int fan, const int32_t* h, int lane) {
   int32_t acc = 0;
-  if (numeric == MLPV_NUM_INT8 && (fan & 15) == 0) {
-    const uint4* wr = reinterpret_cast<const uint4*>(static_cast<const int8_t*>(W) + (size_t)row * fan);
-    for (int q = lane; q < (fan >> 4); q += 32) {
-      const uint4 w16 = __ldg(wr + q);
-      const uint32_t ws[4] = {w16.x, w16.y, w16.z, w16.w};
-#pragma unroll
-      for (int k = 0; k < 4; k++)
-#pragma unroll
-        for (int b = 0; b < 4; b++) acc += (int32_t)(int8_t)(ws[k] >> (8 * b)) * h[16 * q + 4 * k + b];
-    }
-    return acc;
-  }
   for (int j = lane; j < fan; j += 32) acc += wload_i(W, numeric, (size_t)row * fan + j) * h[j];
   return acc;
+}
+// Base-prologue dots, four weight rows per warp at once: lane-contiguous 32-bit weight words (one
+// 128-byte load per row and warp), so the shared-memory reads of the input vector are conflict-free
+// and each of them serves four rows (a 16-byte-per-lane row layout made the reads 16-way bank
+// conflicted and the prologue shared-memory bound).  Rows >= nrows contribute nothing.
+// bf16 rows (fan even) x double h (+ org): fp64 sums, two chains per row.
+__device__ __forceinline__ void rows4_bf16_d(const uint16_t* W, int fan, int r0, int nrows, const double* h, double org,
+                                             int lane, double (&acc)[4]) {
+  const int nw2 = fan >> 1;
+  const uint32_t* wr[4];
+  bool ok[4];
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    ok[r] = r0 + r < nrows;
+    wr[r] = reinterpret_cast<const uint32_t*>(W + (size_t)(ok[r] ? r0 + r : r0) * fan);
+  }
+  double a[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  const double2* h2 = reinterpret_cast<const double2*>(h);
+#pragma unroll 4
+  for (int w = lane; w < nw2; w += 32) {
+    const double2 hh = h2[w];
+    const double x0 = hh.x + org, x1 = hh.y + org;
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+      if (ok[r]) {
+        const uint32_t q = __ldg(wr[r] + w);
+        a[r][0] = fma((double)__uint_as_float(q << 16), x0, a[r][0]);
+        a[r][1] = fma((double)__uint_as_float(q & 0xFFFF0000u), x1, a[r][1]);
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; r++) acc[r] = a[r][0] + a[r][1];
+}
+// int8 rows (fan % 4 == 0) x int32 h (u8 values): exact int32 sums
+__device__ __forceinline__ void rows4_i8(const int8_t* W, int fan, int r0, int nrows, const int32_t* h, int lane,
+                                         int32_t (&acc)[4]) {
+  const int nw4 = fan >> 2;
+  const uint32_t* wr[4];
+  bool ok[4];
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    ok[r] = r0 + r < nrows;
+    wr[r] = reinterpret_cast<const uint32_t*>(W + (size_t)(ok[r] ? r0 + r : r0) * fan);
+    acc[r] = 0;
+  }
+  const int4* h4 = reinterpret_cast<const int4*>(h);
+#pragma unroll 4
+  for (int w = lane; w < nw4; w += 32) {
+    const int4 hh = h4[w];
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+      if (ok[r]) {
+        const uint32_t q = __ldg(wr[r] + w);
+        acc[r] += (int32_t)(int8_t)q * hh.x + (int32_t)(int8_t)(q >> 8) * hh.y + (int32_t)(int8_t)(q >> 16) * hh.z +
+                  (int32_t)(int8_t)(q >> 24) * hh.w;
+      }
+  }
 }
 __device__ __forceinline__ float in_f(const void* x, int numeric, size_t i) {
   if (numeric == MLPV_NUM_FP32) return static_cast<const float*>(x)[i];
@@ -116,7 +161,7 @@ __device__ __forceinline__ float act_float(int act, float u) {
 // the fixed-point numerics, fp32 for the float numerics), base class, and the layer-1 delta
 // tables Delta[s][l][i] = W1[i, p_s] * (x'_{p_s}(l) - x_{p_s}) of subset / tuple spaces.
 __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, const void* levels, BaseWS ws) {
-  extern __shared__ double sm_d[];
+  extern __shared__ __align__(16) double sm_d[];
   const int b = blockIdx.x;
   const int n0 = net.sizes[0];
   int maxw = 0;
@@ -144,29 +189,36 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
   // dense layers: one warp per output neuron, lanes stride the fan-in (coalesced weight rows),
   // warp-shuffle sums
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool l1_clamp = ws.base1 != nullptr && pert.kind == MLPV_PERT_PHILOX_CLAMP && !fixed;
   if (ws.base1 != nullptr) {                        // PHILOX_BOX: W1 x + b1 + origin W1 1 (fp64 sum)
     const int n1 = net.sizes[1];                    // PHILOX_CLAMP: W1 x + b1 (origin enters via d)
     const double org = pert.kind == MLPV_PERT_PHILOX_BOX ? pert.origin_d : 0.0;
-    for (int i = wid; i < n1; i += nw) {
-      double acc = 0.0;
-      if (net.numeric == MLPV_NUM_BF16 && (n0 & 7) == 0) {          // 8 bf16 weights per 16-byte load
-        const uint4* wr = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(net.W[0]) + (size_t)i * n0);
-        for (int qq = lane; qq < (n0 >> 3); qq += 32) {
-          const uint4 w8 = __ldg(wr + qq);
-          const uint32_t ws[4] = {w8.x, w8.y, w8.z, w8.w};
-#pragma unroll
-          for (int k = 0; k < 4; k++) {
-            acc += (double)__uint_as_float(ws[k] << 16) * ((double)hf[8 * qq + 2 * k] + org);
-            acc += (double)__uint_as_float(ws[k] & 0xFFFF0000u) * ((double)hf[8 * qq + 2 * k + 1] + org);
-          }
-        }
+    for (int i0 = 4 * wid; i0 < n1; i0 += 4 * nw) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      if (net.numeric == MLPV_NUM_BF16 && (n0 & 1) == 0) {
+        rows4_bf16_d(static_cast<const uint16_t*>(net.W[0]), n0, i0, n1, hf, org, lane, acc);
       } else {
-        for (int j = lane; j < n0; j += 32)
-          acc += (double)wload_f(net.W[0], net.numeric, (size_t)i * n0 + j) * ((double)hf[j] + org);
+        for (int r = 0; r < 4 && i0 + r < n1; r++)
+          for (int j = lane; j < n0; j += 32)
+            acc[r] += (double)wload_f(net.W[0], net.numeric, (size_t)(i0 + r) * n0 + j) * ((double)hf[j] + org);
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) ws.base1[(size_t)b * n1 + i] = (float)(acc + (double)static_cast<const float*>(net.b[0])[i]);
+      for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+      if (lane < 4 && i0 + lane < n1) {
+        const int i = i0 + lane;
+        const double v = (lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3]) +
+                         (double)static_cast<const float*>(net.b[0])[i];
+        const float u = (float)v;
+        ws.base1[(size_t)b * n1 + i] = u;
+        if (l1_clamp) {
+          // PHILOX_CLAMP: this sum is the base's layer-1 potential itself (reading C23), so the
+          // dense loop below starts at layer 2
+          static_cast<float*>(ws.trace)[(size_t)b * net.trace_len + net.loff[1] + i] = u;
+          if (net.L > 1) hn[i] = net.act == MLPV_ACT_SIGMOID ? 1.0 / (1.0 + exp(-v)) : (v > 0.0 ? v : 0.0);
+        }
+      }
     }
   }
   if (ws.clampc != nullptr) {
@@ -206,45 +258,51 @@ __global__ void k_base_prologue(DevNet net, const void* bases, DevPert pert, con
     if (bad) atomicOr(ws.status, kStatusClampBase);
   }
   const int T = net.trace_len;
-  for (int l = 1; l <= net.L; l++) {
+  if (l1_clamp) {                                   // layer 1 done above (hn holds its activations)
+    __syncthreads();
+    if (net.L > 1) {
+      for (int i = threadIdx.x; i < net.sizes[1]; i += blockDim.x) hf[i] = hn[i];
+      __syncthreads();
+    }
+  }
+  for (int l = l1_clamp ? 2 : 1; l <= net.L; l++) {
     const int nl = net.sizes[l], fan = net.sizes[l - 1];
-    for (int i = wid; i < nl; i += nw) {
+    for (int i0 = 4 * wid; i0 < nl; i0 += 4 * nw) {
       if (fixed) {
-        int32_t acc = row_dot_i(net.W[l - 1], net.numeric, i, fan, hi, lane);
-        acc = __reduce_add_sync(0xffffffffu, acc);
-        if (lane == 0) {
-          acc += static_cast<const int32_t*>(net.b[l - 1])[i];
-          static_cast<int32_t*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = acc;
-          if (l < net.L) hin[i] = act_fixed(net.numeric, net.act, acc, net.shift[l - 1], net.knots);
+        int32_t acc[4] = {0, 0, 0, 0};
+        if (net.numeric == MLPV_NUM_INT8 && (fan & 3) == 0) {
+          rows4_i8(static_cast<const int8_t*>(net.W[l - 1]), fan, i0, nl, hi, lane, acc);
+        } else {
+          for (int r = 0; r < 4 && i0 + r < nl; r++) acc[r] = row_dot_i(net.W[l - 1], net.numeric, i0 + r, fan, hi, lane);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; r++) acc[r] = __reduce_add_sync(0xffffffffu, acc[r]);
+        if (lane < 4 && i0 + lane < nl) {
+          const int i = i0 + lane;
+          const int32_t v = (lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3]) +
+                            static_cast<const int32_t*>(net.b[l - 1])[i];
+          static_cast<int32_t*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = v;
+          if (l < net.L) hin[i] = act_fixed(net.numeric, net.act, v, net.shift[l - 1], net.knots);
         }
       } else {
-        double acc = 0.0;
-        if (net.numeric == MLPV_NUM_BF16 && (fan & 7) == 0) {        // 8 bf16 weights per 16-byte load
-          const uint4* wr = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(net.W[l - 1]) + (size_t)i * fan);
-          for (int qq = lane; qq < (fan >> 3); qq += 32) {
-            const uint4 w8 = __ldg(wr + qq);
-            const uint32_t wq[4] = {w8.x, w8.y, w8.z, w8.w};
-            const double2* h2 = reinterpret_cast<const double2*>(hf + 8 * qq);
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-              const double2 hh = h2[k];
-              acc += (double)__uint_as_float(wq[k] << 16) * hh.x;
-              acc += (double)__uint_as_float(wq[k] & 0xFFFF0000u) * hh.y;
-            }
-          }
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (net.numeric == MLPV_NUM_BF16 && (fan & 1) == 0) {
+          rows4_bf16_d(static_cast<const uint16_t*>(net.W[l - 1]), fan, i0, nl, hf, 0.0, lane, acc);
         } else {
-          for (int j = lane; j < fan; j += 32) acc += (double)wload_f(net.W[l - 1], net.numeric, (size_t)i * fan + j) * hf[j];
+          for (int r = 0; r < 4 && i0 + r < nl; r++)
+            for (int j = lane; j < fan; j += 32)
+              acc[r] += (double)wload_f(net.W[l - 1], net.numeric, (size_t)(i0 + r) * fan + j) * hf[j];
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-          acc += (double)static_cast<const float*>(net.b[l - 1])[i];
-          float u = (float)acc;
-          // PHILOX_CLAMP: the base's layer-1 potentials are base1 (the fp64 sum rounded once), the
-          // value the kernels form for the zero perturbation (reading C23); this lane wrote it above
-          if (l == 1 && pert.kind == MLPV_PERT_PHILOX_CLAMP && ws.base1 != nullptr) u = ws.base1[(size_t)b * net.sizes[1] + i];
-          static_cast<float*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = u;
-          if (l < net.L) hn[i] = net.act == MLPV_ACT_SIGMOID ? 1.0 / (1.0 + exp(-acc)) : (acc > 0.0 ? acc : 0.0);
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+        if (lane < 4 && i0 + lane < nl) {
+          const int i = i0 + lane;
+          const double v = (lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3]) +
+                           (double)static_cast<const float*>(net.b[l - 1])[i];
+          static_cast<float*>(ws.trace)[(size_t)b * T + net.loff[l] + i] = (float)v;
+          if (l < net.L) hn[i] = net.act == MLPV_ACT_SIGMOID ? 1.0 / (1.0 + exp(-v)) : (v > 0.0 ? v : 0.0);
         }
       }
     }
