@@ -533,6 +533,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       auto issue_l3 = [&]() {                             // elected lane: block l3_kb of tile l3_tl
 #pragma unroll
         for (int kk = 0; kk < 4; kk++) {
+          if (MLPV_EXP == 105) break;
           const int g = 4 * l3_kb + kk;
           const uint64_t bd = sdesc_sw128(smem_u32(sW3 + (g >> 1) * kW3Chunk) + 32u * (g & 1));
           if (g < 15) {
@@ -741,8 +742,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           {
             const int j = 2 * kb;
             const uint4 z = make_uint4(0, 0, 0, 0);
+#if MLPV_EXP == 108
+            const uint4 w0 = make_uint4(c0 * 0x9E3779B9u + j, c0 ^ (uint32_t)j, c0 + 77u * j, c0 * 3u), z2 = z;
+            w1 = make_uint4(c0 * 0x85EBCA6Bu + j, c0 ^ (uint32_t)(j * 9), c0 + 33u * j, c0 * 5u + z2.x);
+#else
             const uint4 w0 = j < nblk ? philox(c0, c1, cb, (uint32_t)j, a.rk) : z;
             w1 = j + 1 < nblk ? philox(c0, c1, cb, (uint32_t)(j + 1), a.rk) : z;
+#endif
             out[0] = nibble_word(w0.x); out[1] = nibble_word(w0.y);
             out[2] = nibble_word(w0.z); out[3] = nibble_word(w0.w);
 #pragma unroll
@@ -966,9 +972,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       for (int pp = 0; pp < 4; pp += 2) {
         const int p = 4 * h + pp;
         uint32_t va[32], vb[32];
+#if MLPV_EXP == 106
+#pragma unroll
+        for (int j = 0; j < 32; j++) { va[j] = (uint32_t)j * lane; vb[j] = va[j] ^ 5u; }
+#else
         tmem_ld32(R2 + loff + 32u * p, va);
         tmem_ld32(R2 + loff + 32u * p + 32u, vb);
         tmem_ld_wait();
+#endif
         const uint32_t sa = sign32(va) ^ S.nb2[p], sb = sign32(vb) ^ S.nb2[p + 1];
         S.sc2[p][r] = sa;
         S.sc2[p + 1][r] = sb;
@@ -1008,8 +1019,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         for (int ip = 0; ip < 4; ip++) {
           const int g0 = h ? (ip == 0 ? 14 : 6 + 2 * ip) : 2 * ip;
           uint32_t v[32];
+#if MLPV_EXP == 106
+#pragma unroll
+          for (int j = 0; j < 32; j++) v[j] = (uint32_t)(j + ip) * lane;
+#else
           tmem_ld32(R2 + loff + 16u * g0, v);
           tmem_ld_wait();
+#endif
           if (h && ip == 0) {                              // group 15 has left TMEM: layer 3 may use its columns
             fence_before();
             __syncwarp();
@@ -1029,7 +1045,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             split_pair(__uint_as_float(v[16 + 2 * k]), __uint_as_float(v[16 + 2 * k + 1]), hl[16 + k], hl[24 + k]);
           }
           if (g0 < 14) {
-            tmem_st32(R2 + loff + 16u * g0, hl);
+            if (MLPV_EXP != 106) tmem_st32(R2 + loff + 16u * g0, hl);
+            else if (hl[3] == 0x12345u) S.sc2[0][r] = hl[5];
           } else {
             uint32_t h14[16];
 #pragma unroll

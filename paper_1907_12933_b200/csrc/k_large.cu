@@ -34,7 +34,7 @@
 // MLPV_EXP = 201: the weight tiles are not streamed (128 B per stage); 202: the epilogue skips its
 // per-column work (barriers only); 203: the generators skip the candidate generation;
 // 204: all three; 205: layer-1 chunk pairs share one accumulator; 206: two of the four MMAs per
-// layer-1 stage; 207: no activation stores to the scratch; 209: discard.global.L2 of the dead scratch
+// layer-1 stage; 207: no activation stores to the scratch
 
 namespace mlpv {
 using namespace tc;
@@ -124,6 +124,8 @@ struct LargeArgs {
   // PHILOX_CLAMP (reading C14): layer 1 contracts A = d 2^s (fp16, d = x' - x exact) against the fp16
   // copy of W1 (W1h, the layer-1 tile layout) and forms u1 = base1 + 2^-s acc
   int clamp;
+  int discard;                     // 1: every scratch line is rewritten by every tile (no K padding):
+                                   // the dead scratch is discarded from L2 at the output layer
   int gtab;                        // bytes of the generators' per-base table staged in shared memory
                                    // (PHILOX_CLAMP bounds / base pixels), 0: read from global
   float stepS;
@@ -575,8 +577,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
           const uint32_t buf = cseq & 1u, ph = (cseq >> 1) & 1u;
           mbar_wait(&acc_full[buf], ph);
           fence_after();
-          if (MLPV_EXP == 209 && l == L && ch == 0) {
-            // every layer's MMAs of this tile are complete: its activation scratch is dead
+          if (a.discard && l == L && ch == 0 && !eval) {
+            // every layer's MMAs of this tile are complete (the bulk copies of the activations
+            // finished before the last stages were issued): the CTA's scratch is dead until the
+            // next tile's epilogue rewrites every line of it, so its dirty L2 lines are dropped
+            // instead of being written back to HBM when evicted
             for (size_t o = (size_t)e * 128; o < a.scratch_per_cta; o += 256 * 128)
               asm volatile("discard.global.L2 [%0], 128;" ::"l"(scratch + o) : "memory");
           }
@@ -1404,9 +1409,23 @@ static bool geometry(const DevNet& net, LargeGeom* g, std::string* why) {
     if (d.n > 512 && l >= 2 && l < L) { /* upper layer of a pair: pending words cover 512 */ }
     if (l >= 2 && d.n > 512) { *why = "upper layer of a coverage pair wider than 512"; return false; }
   }
+  // H_l (the A operand of layer l + 1) may reuse H_(l-1)'s region: layer l's MMAs have read every
+  // K block of H_(l-1) (bulk copies complete before the issuer's last stage) by the time its
+  // accumulators are full and E_l starts writing, provided layer l runs its chunks in one pass
+  // (<= 2 chunks), both layers fill whole 64-neuron K blocks (no zero padding to preserve) and H_l
+  // fits.  It keeps the scratch of the float path L2-resident (cfg5 bf16: 768 -> 512 KB per CTA,
+  // 114 -> 76 MB over 148 CTAs; above the ~100 MB of usable L2 every activation byte went to HBM).
+  size_t prev_bytes = 0;
   for (int l = 1; l < L; l++) {
-    g->h_off[l] = off;
-    off += (size_t)(fl ? 2 : 1) * g->lay[l + 1].nkb * kABytes;   // float: hi blocks, then lo blocks
+    const size_t bytes = (size_t)(fl ? 2 : 1) * g->lay[l + 1].nkb * kABytes;   // float: hi blocks, then lo blocks
+    if (fl && l >= 2 && net.sizes[l - 1] % 64 == 0 && net.sizes[l] % 64 == 0 && g->lay[l].nchunks <= 2 &&
+        bytes <= prev_bytes) {
+      g->h_off[l] = g->h_off[l - 1];
+    } else {
+      g->h_off[l] = off;
+      off += bytes;
+    }
+    prev_bytes = bytes;
   }
   g->scratch_per_cta = (off + 1023) & ~size_t(1023);
   g->w_total = wo;
@@ -1559,6 +1578,19 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
   const uint64_t ncl = (uint64_t)(num_sms >= 4 ? num_sms / 2 : 1);     // CTA pairs (one CTA per SM)
   const int grid = 2 * (int)(a.n_tiles < ncl ? a.n_tiles : ncl);
   a.scratch_per_cta = g.scratch_per_cta;
+  {
+    // every hidden layer fills whole K blocks of its activation tiles (64 fp16 / 128 u8 neurons) and
+    // the regions tile the scratch exactly, so no zero padding would be lost by discarding
+    bool full = true;
+    size_t used = 0;
+    for (int l = 1; l < net.L; l++) {
+      full = full && net.sizes[l] % (net.numeric == MLPV_NUM_BF16 ? 64 : 128) == 0;
+      const size_t end = g.h_off[l] + (size_t)(net.numeric == MLPV_NUM_BF16 ? 2 : 1) * g.lay[l + 1].nkb * kABytes;
+      used = end > used ? end : used;
+    }
+    // (float path only: the u8 activations of the int8 path fit in L2 and gain nothing from it)
+    a.discard = net.numeric == MLPV_NUM_BF16 && full && used == g.scratch_per_cta ? 1 : 0;
+  }
   if (!scratch) return cudaErrorInvalidValue;     // the handle's scratch: num_sms x scratch_per_cta, K padding zero
   a.scratch = static_cast<uint8_t*>(scratch);
   {

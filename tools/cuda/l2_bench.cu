@@ -93,7 +93,7 @@ int main() {
   // coalesced loads, each byte once per pass: the L2 capacity knee and the HBM bandwidth
   for (size_t mb : {8, 16, 32, 48, 64, 80, 96, 112, 128, 160, 192, 256, 512, 1024}) {
     const size_t B = mb << 20, n16 = B / 16;
-    const int passes = (int)std::max<size_t>(2, (size_t)(8u << 30) / B);
+    const int passes = (int)std::max<size_t>(2, (size_t)(8ull << 30) / B);
     k_ldg<<<sms * 4, 512>>>(reinterpret_cast<const uint4*>(buf), n16, 2, sink);   // warm (fills L2)
     cudaEventRecord(e0);
     k_ldg<<<sms * 4, 512>>>(reinterpret_cast<const uint4*>(buf), n16, passes, sink);
