@@ -362,16 +362,24 @@ __device__ __forceinline__ uint32_t sign_fold(const uint32_t (&v)[16], uint32_t 
 }
 
 // layer-1 accumulators -> potentials: u1 = base1 + stepS * acc (reading C14b), in place
+// (packed fp32 pairs: one FFMA2 per two neurons, the same single rounding as fmaf)
+__device__ __forceinline__ void ffma2(uint32_t& x0, uint32_t& x1, uint64_t s2, float b0, float b1) {
+  uint64_t d;
+  const uint64_t x = (uint64_t)x0 | ((uint64_t)x1 << 32);
+  const uint64_t b = (uint64_t)__float_as_uint(b0) | ((uint64_t)__float_as_uint(b1) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(s2), "l"(b));
+  x0 = (uint32_t)d;
+  x1 = (uint32_t)(d >> 32);
+}
 template <int N>
 __device__ __forceinline__ void acc_to_u1(uint32_t (&v)[N], const float* b1, float stepS) {
   const float4* b4 = reinterpret_cast<const float4*>(b1);
+  const uint64_t s2 = (uint64_t)__float_as_uint(stepS) * 0x100000001ull;
 #pragma unroll
   for (int k = 0; k < N / 4; k++) {
     const float4 bb = b4[k];
-    v[4 * k] = __float_as_uint(fmaf(__uint_as_float(v[4 * k]), stepS, bb.x));
-    v[4 * k + 1] = __float_as_uint(fmaf(__uint_as_float(v[4 * k + 1]), stepS, bb.y));
-    v[4 * k + 2] = __float_as_uint(fmaf(__uint_as_float(v[4 * k + 2]), stepS, bb.z));
-    v[4 * k + 3] = __float_as_uint(fmaf(__uint_as_float(v[4 * k + 3]), stepS, bb.w));
+    ffma2(v[4 * k], v[4 * k + 1], s2, bb.x, bb.y);
+    ffma2(v[4 * k + 2], v[4 * k + 3], s2, bb.z, bb.w);
   }
 }
 // sign bits of 32 potentials as four independent funnel-shift chains (bit i = neuron i)

@@ -585,12 +585,113 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
             for (size_t o = (size_t)e * 128; o < a.scratch_per_cta; o += 256 * 128)
               asm volatile("discard.global.L2 [%0], 128;" ::"l"(scratch + o) : "memory");
           }
+          // ---- hot paths (staged base, hidden layer, whole 16-neuron groups, no pair-coverage words
+          // to record): short independent chains, no per-neuron guards.  Float: delta layer
+          // (PHILOX_CLAMP layer 1 or l >= 2); int8: reading C18, exact int32 potentials.
+          const bool hot_ok = a.staged && l < L && !eval && !pair_on && (!fl || off_is_ub);
+          // (pair_on is per row: the 32-column loads are taken only when the whole warp is hot --
+          // tcgen05.ld is .sync.aligned, every lane of the warp must issue the same load)
+          const bool hot_warp = __all_sync(0xffffffffu, hot_ok);
+          auto hot_f = [&](const uint32_t* v, const int j0) {
+            uint32_t uw[16];
+            lds16(sa_u + 4u * (uint32_t)j0, uw);
+            const uint2 gw = s_gl[j0 >> 4];
+            float u[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) u[i] = fmaf(__uint_as_float(v[i]), sS, __uint_as_float(uw[i]));
+            uint32_t n0 = 0, n1 = 0;               // sign words (reading C2: -0.0 counts as >= 0)
+#pragma unroll
+            for (int i = 7; i >= 0; i--) {
+              n0 = __funnelshift_l(__float_as_uint(u[i] + 0.0f), n0, 1);
+              n1 = __funnelshift_l(__float_as_uint(u[i + 8] + 0.0f), n1, 1);
+            }
+            const uint32_t scw = (n0 | (n1 << 8)) ^ gw.x;
+            nsc += __popc(scw);
+            if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
+            float mn[4], mx[4];                    // min |u| and max |acc| in four chains
+#pragma unroll
+            for (int q = 0; q < 4; q++) { mn[q] = fabsf(u[q]); mx[q] = fabsf(__uint_as_float(v[q])); }
+#pragma unroll
+            for (int i = 4; i < 16; i++) { mn[i & 3] = fminf(mn[i & 3], fabsf(u[i])); mx[i & 3] = fmaxf(mx[i & 3], fabsf(__uint_as_float(v[i]))); }
+            minab = fminf(minab, fminf(fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3])), __uint_as_float(gw.y)));
+            lacc = fmaxf(lacc, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));
+            uint32_t hw[8], lw[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {         // dh = ReLU(u) - ReLU(u_base) = hi + lo (reading C19)
+              const float h0 = fmaxf(u[2 * i], 0.f) - fmaxf(__uint_as_float(uw[2 * i]), 0.f);
+              const float h1 = fmaxf(u[2 * i + 1], 0.f) - fmaxf(__uint_as_float(uw[2 * i + 1]), 0.f);
+              const __half2 hi2 = __floats2half2_rn(h0, h1);
+              const float2 hf = __half22float2(hi2);
+              const __half2 lo2 = __floats2half2_rn(h0 - hf.x, h1 - hf.y);
+              hw[i] = *reinterpret_cast<const uint32_t*>(&hi2);
+              lw[i] = *reinterpret_cast<const uint32_t*>(&lo2);
+            }
+            if (MLPV_EXP != 207) {
+              const int kbh = j0 >> 6, byh = (2 * j0) & 127;
+              uint8_t* th = hdst + (size_t)kbh * kABytes;
+              uint8_t* tl = hdst + (size_t)(ld.lo_kb + kbh) * kABytes;
+#pragma unroll
+              for (int m = 0; m < 2; m++) {
+                *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
+                *reinterpret_cast<uint4*>(tl + sw128_off(r, byh + 16 * m)) = make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]);
+              }
+            }
+          };
+          auto hot_i = [&](const uint32_t* v, const int j0) {
+            uint32_t uw[16], bw[16];
+            lds16(sa_u + 4u * (uint32_t)j0, uw);
+            lds16(sa_b + 4u * (uint32_t)j0, bw);
+            const uint2 gw = s_gl[j0 >> 4];
+            int32_t u[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) u[i] = (int32_t)(v[i] + bw[i]);
+            uint32_t n0 = 0, n1 = 0;
+#pragma unroll
+            for (int i = 7; i >= 0; i--) {
+              n0 = __funnelshift_l((uint32_t)u[i], n0, 1);
+              n1 = __funnelshift_l((uint32_t)u[i + 8], n1, 1);
+            }
+            const uint32_t scw = (n0 | (n1 << 8)) ^ gw.x;
+            nsc += __popc(scw);
+            if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
+            int32_t mx[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) mx[q] = abs(u[q] - (int32_t)uw[q]);
+#pragma unroll
+            for (int i = 4; i < 16; i++) mx[i & 3] = max(mx[i & 3], abs(u[i] - (int32_t)uw[i]));
+            linf_i = max(linf_i, max(max(mx[0], mx[1]), max(mx[2], mx[3])));
+            const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
+            uint32_t hq[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {         // y = clamp((u + rr) >> sh, 0, 255), packed
+              uint32_t hi2, w4;
+              asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi2) : "r"((u[4 * q + 3] + rr) >> sh), "r"((u[4 * q + 2] + rr) >> sh));
+              asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(w4) : "r"((u[4 * q + 1] + rr) >> sh), "r"((u[4 * q] + rr) >> sh), "r"(hi2));
+              hq[q] = w4;
+            }
+            if (MLPV_EXP != 207) {
+              const int kbh = j0 >> 7, byh = j0 & 127;
+              *reinterpret_cast<uint4*>(hdst + (size_t)kbh * kABytes + sw128_off(r, byh)) = make_uint4(hq[0], hq[1], hq[2], hq[3]);
+            }
+          };
           const int c_lo = ld.nc >= 64 ? hh * (ld.nc >> 1) : 0;
           const int c_hi = ld.nc >= 64 ? c_lo + (ld.nc >> 1) : (hh == 0 ? ld.nc : 0);
           for (int pc = c_lo; pc < ((MLPV_EXP == 202 || MLPV_EXP == 204) ? c_lo : c_hi); pc += 16) {
             const int j0 = ch * ld.nc + pc;
             if (j0 >= ld.n && l == L) break;
             if (j0 >= ((ld.n + 63) & ~63) && l < L && fl) break;
+            if (hot_warp && !fl && pc + 32 <= c_hi && j0 + 32 <= ld.n) {
+              // int8: two hot groups per TMEM load -- one load latency per 32 columns, and two
+              // independent chains for the scheduler (cfg5 int8 kernel 5.08 -> 4.90 ms; the float
+              // groups are register-bound at 32 columns: 7.85 -> 7.91 ms, not taken)
+              uint32_t v2[32];
+              tmem_ld32(tbase + buf * 256u + (uint32_t)pc + lane_off, v2);
+              tmem_ld_wait();
+              hot_i(v2, j0);
+              hot_i(v2 + 16, j0 + 16);
+              pc += 16;
+              continue;
+            }
             uint32_t v[16];
             const int kst = (pc - c_lo) >> 4;
             KS(etl, l, ch, kst, 0);
@@ -605,92 +706,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
             }
 #endif
             KS(etl, l, ch, kst, 1);
-            // ---- hot path (float net, staged base, delta layer (PHILOX_CLAMP layer 1 or l >= 2),
-            // hidden layer, a whole 16-neuron group, no pair-coverage words to record): short
-            // independent chains, no per-neuron guards
-            if (fl && a.staged && off_is_ub && l < L && !eval && !pair_on && j0 + 16 <= ld.n) {
-              uint32_t uw[16];
-              lds16(sa_u + 4u * (uint32_t)j0, uw);
-              const uint2 gw = s_gl[j0 >> 4];
-              float u[16];
-#pragma unroll
-              for (int i = 0; i < 16; i++) u[i] = fmaf(__uint_as_float(v[i]), sS, __uint_as_float(uw[i]));
-              uint32_t n0 = 0, n1 = 0;               // sign words (reading C2: -0.0 counts as >= 0)
-#pragma unroll
-              for (int i = 7; i >= 0; i--) {
-                n0 = __funnelshift_l(__float_as_uint(u[i] + 0.0f), n0, 1);
-                n1 = __funnelshift_l(__float_as_uint(u[i + 8] + 0.0f), n1, 1);
-              }
-              const uint32_t scw = (n0 | (n1 << 8)) ^ gw.x;
-              nsc += __popc(scw);
-              if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
-              float mn[4], mx[4];                    // min |u| and max |acc| in four chains
-#pragma unroll
-              for (int q = 0; q < 4; q++) { mn[q] = fabsf(u[q]); mx[q] = fabsf(__uint_as_float(v[q])); }
-#pragma unroll
-              for (int i = 4; i < 16; i++) { mn[i & 3] = fminf(mn[i & 3], fabsf(u[i])); mx[i & 3] = fmaxf(mx[i & 3], fabsf(__uint_as_float(v[i]))); }
-              minab = fminf(minab, fminf(fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3])), __uint_as_float(gw.y)));
-              lacc = fmaxf(lacc, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));
-              uint32_t hw[8], lw[8];
-#pragma unroll
-              for (int i = 0; i < 8; i++) {         // dh = ReLU(u) - ReLU(u_base) = hi + lo (reading C19)
-                const float h0 = fmaxf(u[2 * i], 0.f) - fmaxf(__uint_as_float(uw[2 * i]), 0.f);
-                const float h1 = fmaxf(u[2 * i + 1], 0.f) - fmaxf(__uint_as_float(uw[2 * i + 1]), 0.f);
-                const __half2 hi2 = __floats2half2_rn(h0, h1);
-                const float2 hf = __half22float2(hi2);
-                const __half2 lo2 = __floats2half2_rn(h0 - hf.x, h1 - hf.y);
-                hw[i] = *reinterpret_cast<const uint32_t*>(&hi2);
-                lw[i] = *reinterpret_cast<const uint32_t*>(&lo2);
-              }
-              if (MLPV_EXP != 207) {
-                const int kbh = j0 >> 6, byh = (2 * j0) & 127;
-                uint8_t* th = hdst + (size_t)kbh * kABytes;
-                uint8_t* tl = hdst + (size_t)(ld.lo_kb + kbh) * kABytes;
-#pragma unroll
-                for (int m = 0; m < 2; m++) {
-                  *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
-                  *reinterpret_cast<uint4*>(tl + sw128_off(r, byh + 16 * m)) = make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]);
-                }
-              }
-              continue;
-            }
-            // ---- hot path, int8 net (same conditions; reading C18: exact int32 potentials)
-            if (!fl && a.staged && l < L && !eval && !pair_on && j0 + 16 <= ld.n) {
-              uint32_t uw[16], bw[16];
-              lds16(sa_u + 4u * (uint32_t)j0, uw);
-              lds16(sa_b + 4u * (uint32_t)j0, bw);
-              const uint2 gw = s_gl[j0 >> 4];
-              int32_t u[16];
-#pragma unroll
-              for (int i = 0; i < 16; i++) u[i] = (int32_t)(v[i] + bw[i]);
-              uint32_t n0 = 0, n1 = 0;
-#pragma unroll
-              for (int i = 7; i >= 0; i--) {
-                n0 = __funnelshift_l((uint32_t)u[i], n0, 1);
-                n1 = __funnelshift_l((uint32_t)u[i + 8], n1, 1);
-              }
-              const uint32_t scw = (n0 | (n1 << 8)) ^ gw.x;
-              nsc += __popc(scw);
-              if (istar < 0 && scw) istar = j0 + __ffs(scw) - 1;
-              int32_t mx[4];
-#pragma unroll
-              for (int q = 0; q < 4; q++) mx[q] = abs(u[q] - (int32_t)uw[q]);
-#pragma unroll
-              for (int i = 4; i < 16; i++) mx[i & 3] = max(mx[i & 3], abs(u[i] - (int32_t)uw[i]));
-              linf_i = max(linf_i, max(max(mx[0], mx[1]), max(mx[2], mx[3])));
-              const int32_t rr = sh > 0 ? (1 << (sh - 1)) : 0;
-              uint32_t hq[4];
-#pragma unroll
-              for (int q = 0; q < 4; q++) {         // y = clamp((u + rr) >> sh, 0, 255), packed
-                uint32_t hi2, w4;
-                asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi2) : "r"((u[4 * q + 3] + rr) >> sh), "r"((u[4 * q + 2] + rr) >> sh));
-                asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(w4) : "r"((u[4 * q + 1] + rr) >> sh), "r"((u[4 * q] + rr) >> sh), "r"(hi2));
-                hq[q] = w4;
-              }
-              if (MLPV_EXP != 207) {
-                const int kbh = j0 >> 7, byh = j0 & 127;
-                *reinterpret_cast<uint4*>(hdst + (size_t)kbh * kABytes + sw128_off(r, byh)) = make_uint4(hq[0], hq[1], hq[2], hq[3]);
-              }
+            if (hot_ok && j0 + 16 <= ld.n) {
+              if (fl) hot_f(v, j0);
+              else hot_i(v, j0);
               continue;
             }
             uint32_t hw[8];                          // fp16 hi pairs (float) or u8 quads (int8)
