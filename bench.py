@@ -66,6 +66,9 @@ def kernel_name(cfg):
         return "k_fused3"
     if cfg.pert.kind in (3, 4, 5):
         return "k_large"
+    if (cfg.net.numeric == M.NUM_INT8 and len(s) == 4 and s[1] <= 64 and s[2] <= 32 and s[3] <= 16
+            and cfg.pert.kind in (1, 2) and 1 <= len(cfg.pert.pixels) <= 32):
+        return "k_tc3"
     if (cfg.net.numeric == M.NUM_INT8 and len(s) == 4 and s[1] <= 64 and s[2] <= 32 and s[3] <= 32
             and cfg.pert.kind in (1, 2) and len(cfg.pert.pixels) >= 2):
         return "k_warp3"

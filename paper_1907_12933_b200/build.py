@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmlpv.so")
-SOURCES = ["mlpv.cu", "k_small.cu", "k_warp.cu", "k_large.cu", "k_fused3.cu", "k_util.cu"]
+SOURCES = ["mlpv.cu", "k_small.cu", "k_warp.cu", "k_tc3.cu", "k_large.cu", "k_fused3.cu", "k_util.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]

@@ -124,8 +124,6 @@ struct LargeArgs {
   // PHILOX_CLAMP (reading C14): layer 1 contracts A = d 2^s (fp16, d = x' - x exact) against the fp16
   // copy of W1 (W1h, the layer-1 tile layout) and forms u1 = base1 + 2^-s acc
   int clamp;
-  int discard;                     // 1: every scratch line is rewritten by every tile (no K padding):
-                                   // the dead scratch is discarded from L2 at the output layer
   int gtab;                        // bytes of the generators' per-base table staged in shared memory
                                    // (PHILOX_CLAMP bounds / base pixels), 0: read from global
   float stepS;
@@ -577,14 +575,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
           const uint32_t buf = cseq & 1u, ph = (cseq >> 1) & 1u;
           mbar_wait(&acc_full[buf], ph);
           fence_after();
-          if (a.discard && l == L && ch == 0 && !eval) {
-            // every layer's MMAs of this tile are complete (the bulk copies of the activations
-            // finished before the last stages were issued): the CTA's scratch is dead until the
-            // next tile's epilogue rewrites every line of it, so its dirty L2 lines are dropped
-            // instead of being written back to HBM when evicted
-            for (size_t o = (size_t)e * 128; o < a.scratch_per_cta; o += 256 * 128)
-              asm volatile("discard.global.L2 [%0], 128;" ::"l"(scratch + o) : "memory");
-          }
           // ---- hot paths (staged base, hidden layer, whole 16-neuron groups, no pair-coverage words
           // to record): short independent chains, no per-neuron guards.  Float: delta layer
           // (PHILOX_CLAMP layer 1 or l >= 2); int8: reading C18, exact int32 potentials.
@@ -1596,19 +1586,6 @@ cudaError_t launch_large(const DevNet& net, const void* const* Wt, void* scratch
   const uint64_t ncl = (uint64_t)(num_sms >= 4 ? num_sms / 2 : 1);     // CTA pairs (one CTA per SM)
   const int grid = 2 * (int)(a.n_tiles < ncl ? a.n_tiles : ncl);
   a.scratch_per_cta = g.scratch_per_cta;
-  {
-    // every hidden layer fills whole K blocks of its activation tiles (64 fp16 / 128 u8 neurons) and
-    // the regions tile the scratch exactly, so no zero padding would be lost by discarding
-    bool full = true;
-    size_t used = 0;
-    for (int l = 1; l < net.L; l++) {
-      full = full && net.sizes[l] % (net.numeric == MLPV_NUM_BF16 ? 64 : 128) == 0;
-      const size_t end = g.h_off[l] + (size_t)(net.numeric == MLPV_NUM_BF16 ? 2 : 1) * g.lay[l + 1].nkb * kABytes;
-      used = end > used ? end : used;
-    }
-    // (float path only: the u8 activations of the int8 path fit in L2 and gain nothing from it)
-    a.discard = net.numeric == MLPV_NUM_BF16 && full && used == g.scratch_per_cta ? 1 : 0;
-  }
   if (!scratch) return cudaErrorInvalidValue;     // the handle's scratch: num_sms x scratch_per_cta, K padding zero
   a.scratch = static_cast<uint8_t*>(scratch);
   {

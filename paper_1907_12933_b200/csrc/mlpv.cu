@@ -568,7 +568,9 @@ static mlpv_status run_kernel(mlpv_ctx* h, const void* bases, int n_base, const 
     dp.levels = plan.levels_dev;
     supported = false;
     e = cudaSuccess;
-    if (!eval_idx && !getenv("MLPV_NO_WARP3"))          // small int8 nets: one warp per candidate (k_warp)
+    if (!eval_idx && !getenv("MLPV_NO_TC3"))            // small int8 nets: tcgen05 per layer (k_tc3)
+      e = launch_tc3(h->net, bases, n_base, dp, dprop, dc, dr, plan.ws, h->num_sms, st, &supported);
+    if (!supported && !eval_idx && !getenv("MLPV_NO_WARP3"))   // ... else one warp per candidate (k_warp)
       e = launch_warp3(h->net, n_base, dp, dprop, dc, dr, plan.ws, h->num_sms, st, &supported);
     if (!supported)
       e = launch_small(h->net, bases, n_base, dp, dprop, dc, dr, plan.ws, eval_idx, eval_n, eval_base, eval_out,

@@ -110,6 +110,9 @@ cudaError_t launch_small(const DevNet& net, const void* bases, int n_base, const
                          int num_sms, cudaStream_t st, bool* supported);
 cudaError_t launch_warp3(const DevNet& net, int n_base, const DevPert& pert, const DevProp& prop, const DevCov& cov,
                          const DevResult& res, BaseWS ws, int num_sms, cudaStream_t st, bool* supported);
+cudaError_t launch_tc3(const DevNet& net, const void* bases, int n_base, const DevPert& pert, const DevProp& prop,
+                       const DevCov& cov, const DevResult& res, BaseWS ws, int num_sms, cudaStream_t st,
+                       bool* supported);
 cudaError_t launch_init_result(const DevResult& r, int n_base, uint32_t n_words, cudaStream_t st);
 constexpr int kMaxParts = 64;
 struct MergeParts { DevResult p[kMaxParts]; };
