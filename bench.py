@@ -58,6 +58,15 @@ def alg_ops_per_candidate(cfg):
     return 2 * (changed * s[1] + dense_rest)
 
 
+def epilogue_ops_per_candidate(cfg):
+    """Algorithmic CUDA-core ops per candidate when the contractions run on the tensor pipe (k_tc3):
+    2 per subset pixel (digit, value), per potential of every layer an offset / bias add and a sign
+    predicate, per hidden neuron a requantisation (round-shift, clamp), per output an argmax compare."""
+    s = cfg.net.sizes
+    hidden = sum(s[1:-1])
+    return 2 * len(cfg.pert.pixels) + 2 * sum(s[1:]) + 2 * hidden + s[-1]
+
+
 def kernel_name(cfg):
     """The enumeration kernel mlpv_check launches for this config (the dominant kernel)."""
     import mlpv_inputs as M
@@ -391,6 +400,16 @@ def main():
             else:
                 peak, peak_note = 2.0 * peak, peak_note + " x2 (int8 nominal ratio; measurement missing)"
         achieved = ops * per_launch / kern_avg_s / 1e12
+    elif kernel_name(cfg) == "k_tc3":
+        # the contractions run on the tensor pipe (a few % busy); the CUDA-core epilogue binds (ncu:
+        # the SMSPs' ALU pipe ~70 % of peak): algorithmic epilogue ops against the lane-op peak
+        bound, unit = "alu", "Gop/s"
+        peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+        peak_note = ("148 SM x 128 lanes x sm_max_mhz (one op per lane per clock); ops = the epilogue's "
+                     "algorithmic ops, the MACs run on the tensor pipe")
+        ops_mac = ops
+        ops = epilogue_ops_per_candidate(cfg)
+        achieved = ops * per_launch / kern_avg_s / 1e9
     else:
         bound, unit = "alu", "Gop/s"
         peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
@@ -404,6 +423,12 @@ def main():
                 "traffic": traffic, "kernel": kernel_name(cfg),
                 "kernel_ms": 1e3 * kern_avg_s, "peak_source": peak_note,
                 "alg_ops_per_candidate": ops, "candidates_per_launch": per_launch}
+    if kernel_name(cfg) == "k_tc3":
+        # the same launch against the int8 tensor peak, in the MAC ops (5,504 / candidate for cfg3)
+        p8 = os.path.join(ROOT, "profiles", "measured_peaks_r2.json")
+        if os.path.exists(p8):
+            t8 = float(json.load(open(p8))["int8_tops"])
+            roofline["tensor_frac_int8_peak"] = ops_mac * per_launch / kern_avg_s / 1e12 / t8
 
     if rank == 0:
         cpu = par = None

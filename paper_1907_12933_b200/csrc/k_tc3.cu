@@ -34,6 +34,10 @@ constexpr int kM = 128;                     // candidates per tile (TMEM lanes)
 constexpr int kWG = 4;                      // warpgroups per CTA
 constexpr int kMaxN1 = 64, kMaxN2 = 32, kMaxN3 = 16;
 constexpr uint32_t kTileA = kM * 32;        // one 32-byte K block of 128 rows (4 KB)
+#ifndef MLPV_T3_SLEEP
+#define MLPV_T3_SLEEP 96
+#endif
+constexpr uint32_t kSleepNs = MLPV_T3_SLEEP;  // between polls of a warpgroup's MMA barrier
 
 struct Args {
   DevNet net;
@@ -183,15 +187,19 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
     my_chk = 0; my_v = 0; my_cex = kNone;
   };
   auto wait_mma = [&]() {
-    if (lane == 0) mbar_wait_sleep(&W.mb, mph, 20);
+    if (lane == 0) mbar_wait_sleep(&W.mb, mph, kSleepNs);
     __syncwarp();
     mph ^= 1u;
     fence_after();
   };
 
-  for (uint64_t tl = t0; tl < t1; tl++) {
-    const int b = (int)(tl / a.tiles_per_base);
-    const uint64_t start = a.pert.begin + (tl % a.tiles_per_base) * kM;
+  // (base input and tile offset advanced incrementally: no 64-bit division per tile)
+  int tb = (int)(t0 / a.tiles_per_base);
+  uint64_t toff = t0 % a.tiles_per_base;
+  for (uint64_t tl = t0; tl < t1; tl++, toff++) {
+    if (toff == a.tiles_per_base) { toff = 0; tb++; }
+    const int b = tb;
+    const uint64_t start = a.pert.begin + toff * kM;
     const uint64_t rem = a.pert.end - start;
     const int nvalid = rem < (uint64_t)kM ? (int)rem : kM;
     const bool valid = r < nvalid;
@@ -236,10 +244,12 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
     // one byte per subset pixel (x'_k: the replacement value, or the clamped offset pixel)
     {
       const uint64_t cv = valid ? c : a.pert.begin;
+      // off32(r, k) = rowbase(r) + (k >> 4) * 128 + (k & 15)
+      uint8_t* arow = W.a1 + ((uint32_t)(r >> 3) * 256u + (uint32_t)(r & 7) * 16u);
       auto put = [&](int k, int d) {
         int v = S.lv[d];
         if (offs) v = max(0, min(255, W.xk[k] + v));
-        W.a1[off32(r, k)] = (uint8_t)v;
+        arow[(k >> 4) * 128 + (k & 15)] = (uint8_t)v;
       };
       if (pow2) {
         uint64_t cc = cv;
