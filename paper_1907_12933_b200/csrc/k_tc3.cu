@@ -84,6 +84,22 @@ __device__ __forceinline__ uint32_t pack_req(int32_t u0, int32_t u1, int32_t u2,
   return w4;
 }
 
+// 32 / 16 consecutive words of a shared-memory int32 array (broadcast loads: every lane the same)
+__device__ __forceinline__ void words32(const int32_t* p, uint32_t (&w)[32]) {
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int4 v = reinterpret_cast<const int4*>(p)[k];
+    w[4 * k] = (uint32_t)v.x; w[4 * k + 1] = (uint32_t)v.y; w[4 * k + 2] = (uint32_t)v.z; w[4 * k + 3] = (uint32_t)v.w;
+  }
+}
+__device__ __forceinline__ void words16(const int32_t* p, uint32_t (&w)[16]) {
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const int4 v = reinterpret_cast<const int4*>(p)[k];
+    w[4 * k] = (uint32_t)v.x; w[4 * k + 1] = (uint32_t)v.y; w[4 * k + 2] = (uint32_t)v.z; w[4 * k + 3] = (uint32_t)v.w;
+  }
+}
+
 __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -262,16 +278,29 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
         for (int k = K - 1; k >= 0; k--) { put(k, (int)(cc % (uint64_t)nq)); cc /= (uint64_t)nq; }
       }
     }
+    // the accumulators start from the offsets (C1, b2, b3 written into TMEM by tcgen05.st, the MMAs
+    // accumulate onto them): no per-neuron adds in the epilogues
+    {
+      uint32_t cw[32];
+      words32(W.c1, cw);
+      tmem_st32(D1 + loff, cw);
+      if (a.n1p > 32) {
+        words32(W.c1 + 32, cw);
+        tmem_st32(D1 + loff + 32u, cw);
+      }
+      tmem_st_wait();
+    }
     fence_proxy_async();
+    fence_before();
     wg_bar();
     if (issuer) {
       fence_after();
-      mma_i8_ss(D1, sdesc_none(smem_u32(W.a1), 128, 256), sdesc_none(smem_u32(S.w1), 128, 256), id1, 0u);
+      mma_i8_ss(D1, sdesc_none(smem_u32(W.a1), 128, 256), sdesc_none(smem_u32(S.w1), 128, 256), id1, 1u);
       mma_commit(&W.mb);
     }
     wait_mma();
 
-    // ---- E1: u1 = C1 + acc, sign changes, requantised h1 -> A2 rows
+    // ---- E1: u1 = C1 + acc (C1 preloaded), sign changes, requantised h1 -> A2 rows
     int32_t u1[64];
     {
       uint32_t v[32];
@@ -295,12 +324,6 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
 #pragma unroll
         for (int i = 16; i < 32; i++) u1[i] = 0;
       }
-    }
-    const int4* c14 = reinterpret_cast<const int4*>(W.c1);
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      const int4 cv = c14[k];
-      u1[4 * k] += cv.x; u1[4 * k + 1] += cv.y; u1[4 * k + 2] += cv.z; u1[4 * k + 3] += cv.w;
     }
     uint32_t ng1a = 0, ng1b = 0;
 #pragma unroll
@@ -339,12 +362,18 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
       }
     }
     const int istar1 = sc1a ? __ffs(sc1a) - 1 : (sc1b ? 32 + __ffs(sc1b) - 1 : -1);
+    {
+      uint32_t bw[32];
+      words32(S.b2, bw);
+      tmem_st32(D2 + loff, bw);
+      tmem_st_wait();
+    }
     fence_proxy_async();
     fence_before();
     wg_bar();
     if (issuer) {
       fence_after();
-      mma_i8_ss(D2, sdesc_none(smem_u32(W.a2), 128, 256), sdesc_none(smem_u32(S.w2[0]), 128, 256), id2, 0u);
+      mma_i8_ss(D2, sdesc_none(smem_u32(W.a2), 128, 256), sdesc_none(smem_u32(S.w2[0]), 128, 256), id2, 1u);
       if (a.n1p > 32)
         mma_i8_ss(D2, sdesc_none(smem_u32(W.a2 + kTileA), 128, 256), sdesc_none(smem_u32(S.w2[1]), 128, 256), id2, 1u);
       mma_commit(&W.mb);
@@ -357,13 +386,8 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
       uint32_t v[32];
       tmem_ld32(D2 + loff, v);
       tmem_ld_wait();
-      const int4* b24 = reinterpret_cast<const int4*>(S.b2);
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const int4 bv = b24[k];
-        u2[4 * k] = (int32_t)v[4 * k] + bv.x; u2[4 * k + 1] = (int32_t)v[4 * k + 1] + bv.y;
-        u2[4 * k + 2] = (int32_t)v[4 * k + 2] + bv.z; u2[4 * k + 3] = (int32_t)v[4 * k + 3] + bv.w;
-      }
+      for (int i = 0; i < 32; i++) u2[i] = (int32_t)v[i];
     }
     // (N = n2p columns were computed; columns >= n2p of the ld are not ours: mask them out)
 #pragma unroll
@@ -410,12 +434,18 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
         cond2 = d >= th2;
       }
     }
+    {
+      uint32_t bw[16];
+      words16(S.b3, bw);
+      tmem_st16(D3 + loff, bw);
+      tmem_st_wait();
+    }
     fence_proxy_async();
     fence_before();
     wg_bar();
     if (issuer) {
       fence_after();
-      mma_i8_ss(D3, sdesc_none(smem_u32(W.a3), 128, 256), sdesc_none(smem_u32(S.w3), 128, 256), id3, 0u);
+      mma_i8_ss(D3, sdesc_none(smem_u32(W.a3), 128, 256), sdesc_none(smem_u32(S.w3), 128, 256), id3, 1u);
       mma_commit(&W.mb);
     }
     wait_mma();
@@ -426,13 +456,8 @@ __global__ void __launch_bounds__(kWG * 128, 1) k_tc3(const __grid_constant__ Ar
       uint32_t v[16];
       tmem_ld16(D3 + loff, v);
       tmem_ld_wait();
-      const int4* b34 = reinterpret_cast<const int4*>(S.b3);
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const int4 bv = b34[k];
-        y[4 * k] = (int32_t)v[4 * k] + bv.x; y[4 * k + 1] = (int32_t)v[4 * k + 1] + bv.y;
-        y[4 * k + 2] = (int32_t)v[4 * k + 2] + bv.z; y[4 * k + 3] = (int32_t)v[4 * k + 3] + bv.w;
-      }
+      for (int i = 0; i < 16; i++) y[i] = (int32_t)v[i];
     }
     fence_before();                          // E3's TMEM reads precede the next tile's MMAs
     int cls = 0;
