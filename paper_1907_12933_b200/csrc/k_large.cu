@@ -64,9 +64,13 @@ constexpr int kM = 128;                   // candidates per tile = TMEM lanes
 // in the peer; the leader issues every MMA with cta_group::2 (M = 256), each CTA holding its own A
 // rows and half of every W tile (N / 2 rows), so each SM streams half the weight bytes per
 // candidate of the one-CTA design.
-constexpr int kSG = 3;                    // generator ring stages
+#ifndef MLPV_KL_SG
+#define MLPV_KL_SG 3
+#endif
+constexpr int kSG = MLPV_KL_SG;           // generator ring stages
 constexpr int kSP = 4;                    // producer ring stages, layers >= 2 (W half tile + A tile)
-constexpr int kSPA = 8;                   // producer ring stages, layer 1 (W half tiles; the same bytes)
+constexpr int kSPA = 11 - MLPV_KL_SG;     // producer ring stages, layer 1 (W half tiles; the generator ring's
+                                          // bytes traded against them)
 constexpr uint32_t kABytes = 128u * 128u; // A tile: 128 rows x 128 B
 constexpr uint32_t kWBytes = 128u * 128u; // W half tile: up to 128 rows x 128 B
 constexpr int kThreads = 640;                // 5 warpgroups: 2 x generator, 2 x epilogue (halves), control
@@ -84,12 +88,12 @@ static_assert(2 * kRegGenL + kRegCtlL + 2 * kRegEpiL <= 5 * kRegLaunchL, "setmax
 constexpr uint32_t kTmemCols = 512;       // two 256-column accumulator buffers
 constexpr int kPendWords = 32;            // per candidate: 16 sc + 16 vc words (upper width <= 512)
 constexpr int kXchWords = 2 * 4 * kM;     // epilogue halves' per-row partial results (4 words per row)
-constexpr size_t kRing = kSP * (kABytes + kWBytes);   // layer 1: kSPA W slots; layers >= 2: kSP (A, W) stages
+constexpr size_t kRing = (size_t)kSPA * kWBytes;      // layer 1: kSPA W slots; layers >= 2: kSP (A, W) / kSP2 stages
 // float layers >= 2: stages [A_hi | A_lo | W chunk c | W chunk c+1] (the hi and lo halves of the
 // activations share one W tile: no duplicated [W | W] K rows, and a chunk pair shares both A tiles)
 constexpr int kSP2 = 2;
 constexpr uint32_t kStage2 = 2 * kABytes + 2 * kWBytes;
-static_assert(kSPA * kWBytes <= kRing && kSP2 * kStage2 <= kRing, "ring region");
+static_assert(kSPA * kWBytes <= kRing && kSP2 * kStage2 <= kRing && kSP * (kABytes + kWBytes) <= kRing, "ring region");
 constexpr size_t kSmemBytes = 1024 + kSG * kABytes + kRing + (size_t)kM * kPendWords * 4 + 4 * kXchWords;
 
 struct LayerDesc {
