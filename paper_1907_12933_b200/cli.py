@@ -78,7 +78,7 @@ def _verify(P, a):
     chk = P.Checker(cfg.net)
     try:
         r = chk.check_incremental(_to_device(cfg.bases), cfg.pert, cfg.prop, cfg.cov, a.gamma, a.max_bound,
-                                  a.granularity)
+                                  a.granularity, early_exit=a.early_exit)
         torch.cuda.synchronize()
         n = cfg.n_base
         step = r["step"][:n].cpu().numpy()
@@ -87,7 +87,9 @@ def _verify(P, a):
         rep = {"command": "verify", "config": cfg.name, "bases": n, "steps": len(bounds),
                "violated": {str(b): {"step": int(step[b]), "bound": bounds[step[b] - 1], "index": int(first[b])}
                             for b in range(n) if step[b] > 0},
-               "safe_over_grid": int((step == 0).sum())}
+               "safe_over_grid": int((step == 0).sum()),
+               "early_exit": bool(a.early_exit),
+               "candidates_checked": int(r["checked"][:n].cpu().numpy().view(np.uint64).sum())}
     finally:
         chk.close()
     return rep, EXIT_VIOLATED if rep["violated"] else EXIT_OK
@@ -130,6 +132,8 @@ def main(argv=None) -> int:
             p.add_argument("--gamma", type=float, required=True)
             p.add_argument("--max-bound", type=int, required=True)
             p.add_argument("--granularity", type=int, default=1)
+            p.add_argument("--early-exit", action="store_true",
+                           help="the loop's own order: one shell per pass, a base input stops at its counterexample")
     p = sub.add_parser("cover")
     p.add_argument("--config", required=True)
     p.add_argument("--images", type=int, default=200)

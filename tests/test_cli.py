@@ -29,6 +29,12 @@ def test_cli_gpu(capsys, oracle_mod):
     want = {str(b): (int(o["step"][b]), int(o["first_cex"][b])) for b in range(50) if o["step"][b] > 0}
     assert {k: (v["step"], v["index"]) for k, v in rep["violated"].items()} == want
     assert rep["safe_over_grid"] == 50 - len(want)
+    # the same answers in the loop's own order with early exit, on fewer candidates
+    full = rep["candidates_checked"]
+    assert cli.main(["verify", "--config", "gamma", "--gamma", "3", "--max-bound", "12", "--early-exit"]) == cli.EXIT_VIOLATED
+    rep = json.loads(capsys.readouterr().out)
+    assert {k: (v["step"], v["index"]) for k, v in rep["violated"].items()} == want
+    assert rep["early_exit"] and rep["candidates_checked"] < full
     # check: cfg2 (no violation at eps = 0.1) holds
     assert cli.main(["check", "--config", "cfg2", "--bases", "2"]) == cli.EXIT_OK
     rep = json.loads(capsys.readouterr().out)
