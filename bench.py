@@ -280,10 +280,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MLPV_BENCH_GLOO=1 (tests only): the N > 1 path with gloo and every rank on the visible GPUs in
+    # turn -- exercises the sharding, the exchange and the max-over-ranks timing on a one-GPU box;
+    # the driver's multi-GPU runs use NCCL, one rank per GPU
+    gloo = bool(os.environ.get("MLPV_BENCH_GLOO"))
+    local = local % max(1, torch.cuda.device_count()) if gloo else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    tdev = torch.device("cpu") if gloo else dev          # device of the timing all-reduces
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if rank == 0:
         from paper_1907_12933_b200 import build as B
         B.build()                                # no-op when libmlpv.so is current
@@ -339,10 +348,14 @@ def main():
     launches = chk.profile(None, None) - launches0 + (args.steps if world > 1 else 0)
     total_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     total_cand = n_cand * world
+    if world > 1:                                # the shards of an enumerated space differ by <= 1 per base
+        t = torch.tensor([float(n_cand)], dtype=torch.float64, device=tdev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_cand = int(t.item())
     value = total_cand / (total_ms / 1e3)
 
     # ---- end to end through the public API: pinned host inputs -> device, check, results -> host
@@ -376,7 +389,7 @@ def main():
             barrier()
             e2e_cand += (e - b) * cfg.n_base
         if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=tdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": e2e_cand * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,

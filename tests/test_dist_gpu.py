@@ -108,3 +108,24 @@ def test_shard_invariance(name, n_base, begin, end):
         torch.cuda.synchronize()
         for k in ref:
             assert np.array_equal(m[k], ref[k]), (name, G, k)
+
+
+def test_bench_two_ranks_one_gpu():
+    """bench.py's N > 1 path as the driver launches it (torch.distributed.run, two ranks), with gloo
+    and both ranks on the one GPU of this box (MLPV_BENCH_GLOO, tests only): index-space shards, the
+    all-gather + merge exchange every step, the max-over-ranks timing and rank 0's single JSON line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MLPV_BENCH_GLOO="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2",
+           "--config", "cfg2", "--steps", "2", "--warmup", "1", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]          # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"].startswith("dp2") and d["value"] > 0
+    assert d["config"]["candidates_per_step"] == 10 * 390_625       # both shards of every base
