@@ -436,6 +436,10 @@ def main():
                 "traffic": traffic, "kernel": kernel_name(cfg),
                 "kernel_ms": 1e3 * kern_avg_s, "peak_source": peak_note,
                 "alg_ops_per_candidate": ops, "candidates_per_launch": per_launch}
+    if bound == "tensor" and cfg.net.numeric != M.NUM_INT8 and pk.get("bf16_tflops_sustained"):
+        # (context: the same rate against the pod's sustained bf16 figure -- cuBLAS back to back for
+        # 4 s, power-capped; the frac above uses the burst figure)
+        roofline["frac_vs_sustained_peak"] = achieved / float(pk["bf16_tflops_sustained"])
     if kernel_name(cfg) == "k_tc3":
         # the same launch against the int8 tensor peak, in the MAC ops (5,504 / candidate for cfg3)
         p8 = os.path.join(ROOT, "profiles", "measured_peaks_r2.json")
