@@ -93,3 +93,11 @@ def test_cfg3_tiles_across_bases(P, oracle_mod):
     straddle base inputs (counts flushed per base)."""
     cfg = M.make_config("cfg3").subset(n_base=7, base_start=20, begin=333, end=333 + 5_000)
     _both(P, cfg, oracle_mod)
+
+
+def test_tiny_spaces_many_bases(P, oracle_mod):
+    """300 base inputs with a 5-candidate space each: every tile is one base's only, mostly empty
+    tile (123 invalid rows), and each warpgroup's range crosses many bases (per-base count flushes)."""
+    cfg = _cfg([64, 32, 16, 10], 4, [8, 7], M.PERT_SUBSET_REPLACE, [9], [0, 60, 120, 180, 255], 300)
+    _both(P, cfg, oracle_mod)
+    _both(P, cfg.subset(begin=1, end=4), oracle_mod)
