@@ -642,62 +642,9 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   unsigned long long my_chk = 0, my_v = 0, my_f = 0, my_cex = kNone, my_cexu = kNone;
 
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nwork; t += stride) {
-    const uint64_t c = eval ? a.eval_idx[t] : begin + t;
-    // ---- a2 + a4: decode and incremental layer 1
-    P U1[M1], U2[M2], U3[M3 > 0 ? M3 : 1];
-#pragma unroll
-    for (int i = 0; i < M1; i++) U1[i] = i < n1 ? s_base[i] : P(0);
-    if (a.pert.kind == MLPV_PERT_TUPLE_REPLACE) {
-      if (a.pert.tuple == 2) {
-        const uint32_t pr = (uint32_t)(c / a.pert.q2);
-        const uint32_t rem = (uint32_t)(c % a.pert.q2);
-        const int li = rem / q, lj = rem % q;
-        int pi, pj;
-        unrank_pair(pr, n0, pi, pj);
-        const P* d0 = delta + ((size_t)pi * q + li) * a.ds;
-        const P* d1 = delta + ((size_t)pj * q + lj) * a.ds;
-#pragma unroll
-        for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i] + d1[i];
-      } else {
-        const int pi = (int)(c / q), li = (int)(c % q);
-        const P* d0 = delta + ((size_t)pi * q + li) * a.ds;
-#pragma unroll
-        for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i];
-      }
-    } else {
-      // mixed-radix digits, least significant first: shifts for a power-of-two q, 32-bit
-      // division when the index fits, 64-bit otherwise (warp-uniform choice)
-      const int qb = __ffs(q) - 1;
-      if ((q & (q - 1)) == 0) {
-        uint64_t cc = c;
-        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
-          const int d = (int)(cc & (uint64_t)(q - 1));
-          cc >>= qb;
-          const P* dk = delta + ((size_t)k * q + d) * a.ds;
-#pragma unroll
-          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
-        }
-      } else if (c < (1ull << 32)) {
-        uint32_t cc = (uint32_t)c;
-        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
-          const int d = (int)(cc % (uint32_t)q);
-          cc /= (uint32_t)q;
-          const P* dk = delta + ((size_t)k * q + d) * a.ds;
-#pragma unroll
-          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
-        }
-      } else {
-        uint64_t cc = c;
-        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
-          const int d = (int)(cc % (uint64_t)q);
-          cc /= (uint64_t)q;
-          const P* dk = delta + ((size_t)k * q + d) * a.ds;
-#pragma unroll
-          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
-        }
-      }
-    }
+  // one candidate from its layer-1 potentials U1 on (t: position in the range / the eval list)
+  auto cand = [&](const uint64_t t, const uint64_t c, P (&U1)[M1]) {
+    P U2[M2], U3[M3 > 0 ? M3 : 1];
     double rs2_f = 0.0;                                // squared distance to the base (restriction /
     long long rs2_i = 0;                               // incremental steps), float / fixed point
     if (a.pert.restrict_on && !eval) {
@@ -755,7 +702,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
           inside = s2 <= a.pert.r2_raw;
         }
       }
-      if (!inside) continue;                           // outside R: no verdict, no coverage
+      if (!inside) return;                           // outside R: no verdict, no coverage
     }
     // incremental bounds (NEXT-2): the step of the smallest ball b_i holding the candidate
     int cstep = 0;
@@ -763,7 +710,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
       cstep = 1;
       if constexpr (FL) { while (cstep < a.pert.n_steps && rs2_f > a.pert.step_r2_f[cstep - 1]) cstep++; }
       else { while (cstep < a.pert.n_steps && rs2_i > a.pert.step_r2_raw[cstep - 1]) cstep++; }
-      if (a.pert.shell > 0 && cstep != a.pert.shell) continue;   // early-exit pass: this shell only
+      if (a.pert.shell > 0 && cstep != a.pert.shell) return;   // early-exit pass: this shell only
     }
     // ---- a5/a6: hidden activations and dense layers
     {
@@ -786,7 +733,7 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
 #pragma unroll
         for (int i = 0; i < M3; i++) if (i < n3) o[net.loff[3] + i] = U3[i];
       }
-      continue;
+      return;
     }
     // ---- a7: argmax, margin, property
     const P* Y = (L == 3) ? U3 : U2;
@@ -839,6 +786,98 @@ __global__ void __launch_bounds__(256) k_small(SmallArgs a) {
         cover_pair<P, M2, (M3 > 0 ? M3 : 1)>(U2, U3, s_base + net.loff[2], s_base + net.loff[3], n2, n3, tg[2], th[1],
                                              tau[1], tau[2], s_cov, s_cert, poff[1], FL);
     }
+  };
+  // subset spaces: a thread takes whole runs of q consecutive indices, which share every digit but
+  // the last -- the prefix (base + the delta rows of those digits) is summed once per run, each
+  // candidate then adds one row (the order of the candidates does not change any result; fixed
+  // point only, where the regrouped integer sums are exact -- the fp32 path keeps its summation order)
+  const bool runs = !FL && !eval && (a.pert.kind == MLPV_PERT_SUBSET_OFFSET || a.pert.kind == MLPV_PERT_SUBSET_REPLACE) &&
+                    a.pert.n_pixels >= 2 && nwork > 0;
+  if (runs) {
+    const uint64_t h0 = begin / (uint64_t)q, nruns = (end - 1) / (uint64_t)q - h0 + 1;
+    const P* last = delta + (size_t)(a.pert.n_pixels - 1) * q * a.ds;
+    for (uint64_t ru = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ru < nruns; ru += stride) {
+      const uint64_t hi = h0 + ru;
+      P U1p[M1];
+#pragma unroll
+      for (int i = 0; i < M1; i++) U1p[i] = i < n1 ? s_base[i] : P(0);
+      uint64_t cc = hi;
+      for (int k = a.pert.n_pixels - 2; k >= 0; k--) {
+        const int d = (int)(cc % (uint64_t)q);
+        cc /= (uint64_t)q;
+        const P* dk = delta + ((size_t)k * q + d) * a.ds;
+#pragma unroll
+        for (int i = 0; i < M1; i++) if (i < n1) U1p[i] += dk[i];
+      }
+      const uint64_t c0 = hi * (uint64_t)q;
+      const int dlo = c0 < begin ? (int)(begin - c0) : 0;
+      const int dhi = c0 + (uint64_t)q > end ? (int)(end - c0) : q;
+      for (int dl = dlo; dl < dhi; dl++) {
+        const P* dk = last + (size_t)dl * a.ds;
+        P U1[M1];
+#pragma unroll
+        for (int i = 0; i < M1; i++) U1[i] = i < n1 ? U1p[i] + dk[i] : P(0);
+        cand(c0 + dl - begin, c0 + dl, U1);
+      }
+    }
+  } else
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nwork; t += stride) {
+    const uint64_t c = eval ? a.eval_idx[t] : begin + t;
+    // ---- a2 + a4: decode and incremental layer 1
+    P U1[M1];
+#pragma unroll
+    for (int i = 0; i < M1; i++) U1[i] = i < n1 ? s_base[i] : P(0);
+    if (a.pert.kind == MLPV_PERT_TUPLE_REPLACE) {
+      if (a.pert.tuple == 2) {
+        const uint32_t pr = (uint32_t)(c / a.pert.q2);
+        const uint32_t rem = (uint32_t)(c % a.pert.q2);
+        const int li = rem / q, lj = rem % q;
+        int pi, pj;
+        unrank_pair(pr, n0, pi, pj);
+        const P* d0 = delta + ((size_t)pi * q + li) * a.ds;
+        const P* d1 = delta + ((size_t)pj * q + lj) * a.ds;
+#pragma unroll
+        for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i] + d1[i];
+      } else {
+        const int pi = (int)(c / q), li = (int)(c % q);
+        const P* d0 = delta + ((size_t)pi * q + li) * a.ds;
+#pragma unroll
+        for (int i = 0; i < M1; i++) if (i < n1) U1[i] = U1[i] + d0[i];
+      }
+    } else {
+      // mixed-radix digits, least significant first: shifts for a power-of-two q, 32-bit
+      // division when the index fits, 64-bit otherwise (warp-uniform choice)
+      const int qb = __ffs(q) - 1;
+      if ((q & (q - 1)) == 0) {
+        uint64_t cc = c;
+        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
+          const int d = (int)(cc & (uint64_t)(q - 1));
+          cc >>= qb;
+          const P* dk = delta + ((size_t)k * q + d) * a.ds;
+#pragma unroll
+          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+        }
+      } else if (c < (1ull << 32)) {
+        uint32_t cc = (uint32_t)c;
+        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
+          const int d = (int)(cc % (uint32_t)q);
+          cc /= (uint32_t)q;
+          const P* dk = delta + ((size_t)k * q + d) * a.ds;
+#pragma unroll
+          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+        }
+      } else {
+        uint64_t cc = c;
+        for (int k = a.pert.n_pixels - 1; k >= 0; k--) {
+          const int d = (int)(cc % (uint64_t)q);
+          cc /= (uint64_t)q;
+          const P* dk = delta + ((size_t)k * q + d) * a.ds;
+#pragma unroll
+          for (int i = 0; i < M1; i++) if (i < n1) U1[i] += dk[i];
+        }
+      }
+    }
+    cand(t, c, U1);
   }
   if (eval) return;
   // ---- a9: block reduction
@@ -927,6 +966,14 @@ cudaError_t launch_small(const DevNet& net, const void* bases, int n_base, const
   a.eval_idx = eval_idx; a.eval_n = eval_n; a.eval_base = eval_base; a.eval_out = eval_out;
   *supported = true;
   const int L = net.L, n1 = net.sizes[1], n2 = net.sizes[2], n3 = L >= 3 ? net.sizes[3] : 0;
+  // exact-width instantiations for the BASELINE's small net (25-10-5, configs 1 and 2): the
+  // register arrays hold n_1 / n_2 values with no guarded padding iterations (the 16-wide form
+  // spent ~60 % of cfg2's instructions on predicated-off iterations of the dense loops)
+  if (L == 2 && n1 == 10 && n2 == 5) {
+    if (net.numeric == MLPV_NUM_FP32) return run_small<MLPV_NUM_FP32, 2, 10, 5, 0>(a, num_sms, st);
+    if (net.numeric == MLPV_NUM_Q4_12) return run_small<MLPV_NUM_Q4_12, 2, 10, 5, 0>(a, num_sms, st);
+    if (net.numeric == MLPV_NUM_INT8) return run_small<MLPV_NUM_INT8, 2, 10, 5, 0>(a, num_sms, st);
+  }
   if (L == 2 && n1 <= 16 && n2 <= 16) {
     if (net.numeric == MLPV_NUM_FP32) return run_small<MLPV_NUM_FP32, 2, 16, 16, 0>(a, num_sms, st);
     if (net.numeric == MLPV_NUM_Q4_12) return run_small<MLPV_NUM_Q4_12, 2, 16, 16, 0>(a, num_sms, st);
