@@ -245,42 +245,6 @@ __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
   }
   return make_uint4(c0, c1, c2, c3);
 }
-// The same function for a fixed (c0, c1, c2) and a varying block counter c3 = j, with everything
-// that does not depend on j hoisted out (computed once per generator row and tile): in round 0 both
-// products and the c0 lane; in round 1 the c0 product and the c2 / c3 lanes; in round 2 the c2
-// product.  Per call 4 fewer IMAD.WIDE and 2 fewer LOP3 than philox(); the output is identical.
-struct PhiloxRow { uint32_t d, k2, e, f5, g4, h; };
-__device__ __forceinline__ PhiloxRow philox_row(uint32_t c0, uint32_t c1, uint32_t c2, const uint32_t (&rk)[20]) {
-  PhiloxRow p;
-  const uint32_t hi0a = __umulhi(0xD2511F53u, c0), lo0a = 0xD2511F53u * c0;
-  const uint32_t hi1a = __umulhi(0xCD9E8D57u, c2), lo1a = 0xCD9E8D57u * c2;
-  const uint32_t s0 = hi1a ^ c1 ^ rk[0];                 // round 0: c0 lane (j-free), c2 lane = d ^ j
-  p.d = hi0a ^ rk[1];
-  p.k2 = lo1a ^ rk[2];                                   // round 1's c1 ^ key
-  const uint32_t hi0b = __umulhi(0xD2511F53u, s0), lo0b = 0xD2511F53u * s0;
-  p.e = hi0b ^ lo0a ^ rk[3];                             // round 1: c2 lane (j-free)
-  const uint32_t f = lo0b;                               // round 1: c3 lane
-  p.f5 = f ^ rk[5];
-  p.g4 = __umulhi(0xCD9E8D57u, p.e) ^ rk[4];             // round 2: product of the c2 lane
-  p.h = 0xCD9E8D57u * p.e;
-  return p;
-}
-__device__ __forceinline__ uint4 philox_j(const PhiloxRow& p, uint32_t j, const uint32_t (&rk)[20]) {
-  const uint32_t s2 = p.d ^ j;                           // round 0
-  const uint32_t hi1b = __umulhi(0xCD9E8D57u, s2), lo1b = 0xCD9E8D57u * s2;
-  const uint32_t t0 = hi1b ^ p.k2;                       // round 1 (c1 = lo1b, c2 = e, c3 = f)
-  const uint32_t hi0c = __umulhi(0xD2511F53u, t0), lo0c = 0xD2511F53u * t0;
-  uint32_t c0 = p.g4 ^ lo1b, c1 = p.h, c2 = hi0c ^ p.f5, c3 = lo0c;   // round 2
-#pragma unroll
-  for (int r = 3; r < 10; r++) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r], n2 = hi0 ^ c3 ^ rk[2 * r + 1];
-    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-  }
-  return make_uint4(c0, c1, c2, c3);
-}
-
 // The 8 levels of one Philox word (nibble n -> pixel n, LSB first) as the fp16 subnormals
 // l * 2^-24, two per 32-bit word: one PRMT per pixel pair (the zero high bytes come from PRMT's
 // sign replication of the nibble bytes).  The layer-1 MMA then computes 2^-24 * W1 l exactly in

@@ -279,10 +279,10 @@ __device__ __forceinline__ uint2 lds_u2(uint32_t saddr) {
 // ----------------------------------------------------------------------------- generator
 // gt: shared-memory address of the base's staged table (PHILOX_CLAMP bounds, or the base pixels),
 // 0 when the table is read from global memory
-__device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot, uint32_t gt) {
+__device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti, int r, int kb, uint8_t* slot, uint32_t gt,
+                                          const PhiloxRow& pr) {
   const int n0 = a.net.sizes[0];
-  const uint64_t c = row_index(a, ti, r);
-  const bool valid = r < ti.nvalid;
+  const bool valid = r < ti.nvalid;                    // pr: the row's Philox prefix (row_index)
   if (a.clamp) {
     const int nch = (n0 + 7) / 8;
     const uint4* tab = a.ws.clampc + (size_t)ti.b * 2 * nch;
@@ -290,7 +290,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
     for (int hb = 0; hb < 2; hb++) {
       const int j = 2 * kb + hb;
       uint4 w = make_uint4(0, 0, 0, 0);
-      if (32 * j < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, a.rk);
+      if (32 * j < n0 && valid) w = philox_j(pr, (uint32_t)j, a.rk);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int ww = 0; ww < 4; ww++) {
@@ -313,7 +313,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
       const int j = 2 * kb + hb;
       const int p0 = 32 * j;
       uint4 w = make_uint4(0, 0, 0, 0);
-      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, a.rk);
+      if (p0 < n0 && valid) w = philox_j(pr, (uint32_t)j, a.rk);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int ww = 0; ww < 4; ww++) {
@@ -351,7 +351,7 @@ __device__ __forceinline__ void gen_block(const LargeArgs& a, const TileInfo& ti
       const int j = 4 * kb + q;
       const int p0 = 32 * j;
       uint4 w = make_uint4(0, 0, 0, 0);
-      if (p0 < n0 && valid) w = philox((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, (uint32_t)j, a.rk);
+      if (p0 < n0 && valid) w = philox_j(pr, (uint32_t)j, a.rk);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
       if (p0 + 32 <= n0 && (n0 & 7) == 0 && s >= 0) {    // whole block in range: 16-bit-lane form
         const uint32_t c2 = (uint32_t)(256 + og) * 0x00010001u;
@@ -1345,6 +1345,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
       }
       const int gtl = (int)(t - t_begin);
       (void)gtl;
+      const uint64_t c = row_index(a, ti, r);              // this thread's row of every stage of the tile
+      const PhiloxRow pr = philox_row((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)ti.b, a.rk);
       const int passes = (l1.nchunks & 1) == 0 ? l1.nchunks / 2 : l1.nchunks;   // chunk pairs share A
       for (int ch = 0; ch < passes; ch++)
         for (int kb = 0; kb < l1.nkb; kb++) {
@@ -1356,7 +1358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
           if ((warp & 3) == 0) mbar_wait_sleep(&gempty[st], ph ^ 1u, 32);
           named_bar(ggrp ? 5 : 4, 128);
           KG(gtl, ch, kb, 1);
-          if (MLPV_EXP != 203 && MLPV_EXP != 204) gen_block(a, ti, r, kb, sG + st * kABytes, gt_addr);
+          if (MLPV_EXP != 203 && MLPV_EXP != 204) gen_block(a, ti, r, kb, sG + st * kABytes, gt_addr, pr);
           KG(gtl, ch, kb, 2);
           fence_proxy_async();
           named_bar(ggrp ? 3 : 1, 128);
