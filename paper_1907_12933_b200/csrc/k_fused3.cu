@@ -22,8 +22,9 @@
 //   E2       pass A: sign words sc2 and counts; pass B: u2 -> [hi | lo] in place, one piece per step
 //            (neurons 240-255 go to a small shared-memory tile so that their 16 columns can hold
 //            the layer-3 accumulator).  The layer-2 statistics are needed by < 1 % of the rows: a
-//            warp's single such row is evaluated by all 32 lanes from a shared-memory copy, warps
-//            with several compute them per lane.  Then the pair-(1,2) coverage words.
+//            warp's (up to 4) such rows are evaluated by all 32 lanes, one row at a time, from
+//            shared-memory copies; warps with more compute them per lane.  Then the pair-(1,2)
+//            coverage words.
 //   layer 3  N = 16 (n_3 <= 16): A = H2 from TMEM (and the tail tile), accumulator TMEM cols
 //            [496,512); issued by the MMA issuer between layer-1 stages of the next tile.
 //   E3       half 1: logits, pair (2,3), argmax / margin / property, counts, first counterexample.
@@ -95,8 +96,21 @@ __device__ unsigned long long g_trace_gen[2][2][4][13][5];
 #endif
 
 constexpr int kThreads = 768;
-constexpr int kSG = 6;                       // generator ring stages
-constexpr int kSW = 5;                       // weight ring stages
+// ring depths and E2's after-hand-off statistics rows are compile-time parameters (measured, cfg4,
+// 3 interleaved A/B runs each: 5 generator stages + up to 4 statistics rows per warp +1.5 % over the
+// round-2 6 stages + 1 row; 5 stages alone -0.5 %, 6 + 4 with a 4-stage W ring and 5 + 5: no better)
+#ifndef MLPV_F3_SG
+#define MLPV_F3_SG 5
+#endif
+#ifndef MLPV_F3_C1ROWS
+#define MLPV_F3_C1ROWS 4
+#endif
+constexpr int kSG = MLPV_F3_SG;              // generator ring stages
+constexpr int kC1Rows = MLPV_F3_C1ROWS;      // E2: statistics rows per warp evaluated after the hand-off
+#ifndef MLPV_F3_SW
+#define MLPV_F3_SW 5
+#endif
+constexpr int kSW = MLPV_F3_SW;              // weight ring stages
 constexpr uint32_t kBiasTile = 4096;         // 128 rows x K 16 (fp16), no-swizzle layout
 constexpr uint32_t kTile = 16384;            // 128 rows x 128 B
 constexpr int kN1 = 256, kN2 = 256, kN3P = 16;
@@ -109,7 +123,7 @@ constexpr int kMaxN0 = 1024;
 // "Multi-warp arbiter"), so the roles are stacked by how latency-critical they are: 20-23 control
 // (20 idle / trace observer, 21 weight producer, 23 MMA issuer for all three layers / TMEM owner),
 // 12-19 epilogue team (E1, E2, E3 -- on the tile's critical path; two warps per TMEM lane quadrant),
-// 0-11 generator (throughput work with a six-stage ring of slack; one warpgroup per stage group).
+// 0-11 generator (throughput work with a five-stage ring of slack; one warpgroup per stage group).
 #if MLPV_EXP == 31
 constexpr int kNGenGroups = 2, kWE = 12, kWIdle = 20, kWProd = 21, kWIss = 23;   // timing experiment: warps 8-11 idle
 #else
@@ -194,7 +208,7 @@ struct alignas(16) Smem {
   float xf[2][3][128];
   uint32_t sc2[8][128];                      // E2: sign-change words of layer 2
   uint16_t vc2[16][128];                     // E2 slow path: value-change bits of layer 2 (16 neurons)
-  alignas(16) float c1row[8][128];           // E2: the layer-2 potentials of a warp's single cond1 row
+  alignas(16) float c1row[8][kC1Rows][128];  // E2: the layer-2 potentials of a warp's few statistics rows
   alignas(16) uint4 ctab[kMaxN0 / 8][2];     // generators, PHILOX_CLAMP: the staged base's clamp bounds
   uint8_t stype[kMaxN0 / 64];                // ... and each stage's clamp type (kGen*)
 };
@@ -1008,15 +1022,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const bool slow2 = __any_sync(0xffffffffu, cond1 || (need23 && valid && nsc2 <= 1));
       // Layer-2 statistics (min |u|, L-inf, value-change words and their margin) are needed only
       // by rows with cond1 (pair (1, 2)) or with at most one layer-2 sign change (pair (2, 3)):
-      // under 1 % of the candidates.  A warp with exactly one such row copies that row's
-      // potentials to shared memory and its 32 lanes evaluate them together after the hand-off
-      // (c1 path); two or more rows take the per-lane path inside the group loop.
+      // under 1 % of the candidates.  A warp with one to kC1Rows such rows copies their
+      // potentials to shared memory and its 32 lanes evaluate them together, one row at a time,
+      // after the hand-off (c1 path); more rows take the per-lane path inside the group loop.
       const bool statrow = cond1 || (need23 && valid && nsc2 <= 1);
       const uint32_t smask = __ballot_sync(0xffffffffu, statrow);
-      const bool c1path = __popc(smask) == 1;
-      const bool statsB = __popc(smask) >= 2;
+      const int nstat = __popc(smask);
+      const bool c1path = nstat >= 1 && nstat <= kC1Rows;
+      const bool statsB = nstat > kC1Rows;
       const bool vcw_needed = statsB && __any_sync(0xffffffffu, cond1);
-      float* c1buf = S.c1row[warp - kWE];
+      // a statistics row's slot: its rank among the warp's statistics rows (lowest lane first)
+      float* c1buf = S.c1row[warp - kWE][0] + 128 * __popc(smask & ((1u << lane) - 1u));
       TRE(1, tl, 1);
       TRE2(tl, 1, 1);
       float linf2 = 0.f, minab2 = 3.0e38f, vcamb = 3.0e38f;
@@ -1162,9 +1178,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       if (et == 0) TR(tl, 11);
       TRE2(tl, 1, 6);
       if (c1path) {
-        // lane l: neurons 4l..4l+3 of this half, the same fp32 operations as the per-lane path
+        // one statistics row at a time (slot order = lane order); lane l: neurons 4l..4l+3 of this
+        // half, the same fp32 operations as the per-lane path
         __syncwarp();
-        const float4 u4 = reinterpret_cast<const float4*>(c1buf)[lane];
+        uint32_t rest = smask;
+#pragma unroll 1
+        for (int slot = 0; rest; slot++) {
+        const int owner = __ffs(rest) - 1;
+        rest &= rest - 1u;
+        const float4 u4 = reinterpret_cast<const float4*>(S.c1row[warp - kWE][slot])[lane];
         const float4 b4 = reinterpret_cast<const float4*>(S.ub2 + 128 * h)[lane];
         const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
         uint32_t nib = 0;
@@ -1186,7 +1208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 #pragma unroll
         for (int pp = 0; pp < 4; pp++)
           w[pp] = __reduce_or_sync(0xffffffffu, (lane >> 3) == pp ? nib << (4 * (lane & 7)) : 0u);
-        if (statrow) {
+        if (lane == owner) {
           minab2 = fminf(minab2, rmnu);
           vcamb = fminf(vcamb, rmnv);
           linf2 = fmaxf(linf2, rmxd);
@@ -1195,6 +1217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             S.vc2[8 * h + 2 * pp][r] = (uint16_t)w[pp];
             S.vc2[8 * h + 2 * pp + 1][r] = (uint16_t)(w[pp] >> 16);
           }
+        }
         }
       }
       if (slow2) pair_exchange_f(S, h, r, linf2, minab2, vcamb, 9 + q);
