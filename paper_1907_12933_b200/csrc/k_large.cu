@@ -65,6 +65,9 @@ constexpr int kM = 128;                   // candidates per tile = TMEM lanes
 // in the peer; the leader issues every MMA with cta_group::2 (M = 256), each CTA holding its own A
 // rows and half of every W tile (N / 2 rows), so each SM streams half the weight bytes per
 // candidate of the one-CTA design.
+#ifndef MLPV_KL_L2HINT
+#define MLPV_KL_L2HINT 1
+#endif
 #ifndef MLPV_KL_SG
 #define MLPV_KL_SG 3
 #endif
@@ -504,6 +507,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
   fence_after();
   const uint32_t tbase = s_tbase;
   uint8_t* scratch = a.scratch + (size_t)blockIdx.x * a.scratch_per_cta;
+  // the scratch is rewritten every tile: its stores and bulk loads carry an L2 evict_last policy so
+  // the dirty lines are not written back to HBM in between (MLPV_KL_L2HINT=0: plain accesses)
+#if MLPV_KL_L2HINT
+  const uint64_t l2_keep = l2_policy_evict_last();
+  auto st_scratch = [&](void* p, uint4 v) { stg128_hint(p, v, l2_keep); };
+  auto ld_scratch = [&](void* dst, const void* src, uint32_t bytes, uint64_t* bar) { bulk_g2s_hint(dst, src, bytes, bar, l2_keep); };
+#else
+  auto st_scratch = [&](void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; };
+  auto ld_scratch = [&](void* dst, const void* src, uint32_t bytes, uint64_t* bar) { bulk_g2s(dst, src, bytes, bar); };
+#endif
 
   if (warp >= 8 && warp < 16) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEpiL));
@@ -638,8 +651,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
               uint8_t* tl = hdst + (size_t)(ld.lo_kb + kbh) * kABytes;
 #pragma unroll
               for (int m = 0; m < 2; m++) {
-                *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
-                *reinterpret_cast<uint4*>(tl + sw128_off(r, byh + 16 * m)) = make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]);
+                st_scratch(th + sw128_off(r, byh + 16 * m), make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]));
+                st_scratch(tl + sw128_off(r, byh + 16 * m), make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]));
               }
             }
           };
@@ -677,7 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
             }
             if (MLPV_EXP != 207) {
               const int kbh = j0 >> 7, byh = j0 & 127;
-              *reinterpret_cast<uint4*>(hdst + (size_t)kbh * kABytes + sw128_off(r, byh)) = make_uint4(hq[0], hq[1], hq[2], hq[3]);
+              st_scratch(hdst + (size_t)kbh * kABytes + sw128_off(r, byh), make_uint4(hq[0], hq[1], hq[2], hq[3]));
             }
           };
           const int c_lo = ld.nc >= 64 ? hh * (ld.nc >> 1) : 0;
@@ -942,15 +955,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
                 uint8_t* tl = hdst + (size_t)(ld.lo_kb + kbh) * kABytes;
 #pragma unroll
                 for (int m = 0; m < 2; m++) {
-                  *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
-                  *reinterpret_cast<uint4*>(tl + sw128_off(r, byh + 16 * m)) = make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]);
+                  st_scratch(th + sw128_off(r, byh + 16 * m), make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]));
+                  st_scratch(tl + sw128_off(r, byh + 16 * m), make_uint4(lw[4 * m], lw[4 * m + 1], lw[4 * m + 2], lw[4 * m + 3]));
                 }
               } else {
                 const int kbh = j0 >> 7, byh = j0 & 127;
                 uint8_t* th = hdst + (size_t)kbh * kABytes;
 #pragma unroll
                 for (int m = 0; m < 1; m++)
-                  *reinterpret_cast<uint4*>(th + sw128_off(r, byh + 16 * m)) = make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]);
+                  st_scratch(th + sw128_off(r, byh + 16 * m), make_uint4(hw[4 * m], hw[4 * m + 1], hw[4 * m + 2], hw[4 * m + 3]));
               }
             }
           }
@@ -1083,8 +1096,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
                 uint8_t* sb = sR + st * kStage2;
                 mbar_wait(&pempty2[st], ph ^ 1u);
                 mbar_expect_tx(&pfull2[st], 2 * kABytes + pr * wb);
-                bulk_g2s(sb, hsrc + (size_t)kb * kABytes, kABytes, &pfull2[st]);
-                bulk_g2s(sb + kABytes, hsrc + (size_t)(ld.nkb + kb) * kABytes, kABytes, &pfull2[st]);
+                ld_scratch(sb, hsrc + (size_t)kb * kABytes, kABytes, &pfull2[st]);
+                ld_scratch(sb + kABytes, hsrc + (size_t)(ld.nkb + kb) * kABytes, kABytes, &pfull2[st]);
                 for (int c = 0; c < pr; c++) {
                   const int ch = pr * cp + c;
                   bulk_g2s(sb + 2 * kABytes + c * kWBytes, ld.W + ((size_t)ch * ld.nkb + kb) * wbytes + rank * (wbytes / 2), wb, &pfull2[st]);
@@ -1117,7 +1130,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
               mbar_wait(&pempty[st], ph ^ 1u);
               mbar_expect_tx(&pfull[st], wb + kABytes);
               bulk_g2s(sa + kABytes, ld.W + woff, wb, &pfull[st]);
-              bulk_g2s(sa, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
+              ld_scratch(sa, scratch + a.h_off[l - 1] + (size_t)kb * kABytes, kABytes, &pfull[st]);
               ps++;
             }
           }
