@@ -16,6 +16,7 @@ infrastructure) is run only in the cpu_baseline leg and in --impl reference.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -93,7 +94,7 @@ def peaks():
 
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -104,12 +105,14 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", self.idx], stdout=subprocess.PIPE,
+                                          "-lms", "100", "-i", self.idx], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
 
-    def stop(self):
+    def stop(self, t_begin: float = None, t_end: float = None):
+        """Median SM clock and the throttle reasons of the samples taken inside [t_begin, t_end]
+        (host time.time() bounds of the timed region; every sample when none falls inside)."""
         if self.proc is None:
             return None
         time.sleep(0.25)
@@ -119,12 +122,20 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            rows.append((ts, f))
+        inside = [f for ts, f in rows if ts is not None and t_begin is not None and t_begin - 0.05 <= ts <= t_end + 0.05]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for f in (inside or [f for _, f in rows]):
             try:
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
@@ -318,6 +329,13 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # the clock sampler (nvidia-smi -lms) starts before the warm-up so that its start-up (NVML
+    # initialisation) is not inside the timed region; only samples stamped inside it are reported
+    gpu_idx = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local)
+    clocks = ClockSampler(gpu_idx)
+    late = os.environ.get("MLPV_BENCH_SAMPLER") == "late"
+    if not late:
+        clocks.start()
     for k in range(args.warmup):
         one_step(k)
     torch.cuda.synchronize()
@@ -327,9 +345,9 @@ def main():
     kev1.record(stream)                          # re-records them around the enumeration kernel
     torch.cuda.synchronize()
     launches0 = chk.profile(kev0, kev1)
-    gpu_idx = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local)
-    clocks = ClockSampler(gpu_idx)
-    clocks.start()
+    if late:
+        clocks.start()
+    t_begin = time.time()
     step_ms, kern_ms, n_cand = [], [], 0
     for k in range(args.warmup, args.warmup + args.steps):
         flush.fill_(k & 0xFF)                   # L2 flush between timed steps (outside the events)
@@ -344,7 +362,7 @@ def main():
         step_ms.append(ev0.elapsed_time(ev1))
         kern_ms.append(kev0.elapsed_time(kev1))
         n_cand += per_base * cfg.n_base
-    clk = clocks.stop()
+    clk = clocks.stop(t_begin, time.time())
     launches = chk.profile(None, None) - launches0 + (args.steps if world > 1 else 0)
     total_ms = sum(step_ms)
     if world > 1:
