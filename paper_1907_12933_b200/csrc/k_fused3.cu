@@ -223,21 +223,33 @@ struct TileInfo {
   int nvalid;         // valid rows of the pair tile (0..256)
 };
 
-__device__ __forceinline__ TileInfo tile_info(const Args& a, uint64_t t) {
-  TileInfo ti;
-  if (a.eval_idx) {
-    ti.b = a.eval_base;
-    ti.start = t * 256;
-    const int64_t rem = a.eval_n - (int64_t)ti.start;
-    ti.nvalid = rem < 256 ? (int)rem : 256;
-  } else {
-    ti.b = (int)(t / a.tiles_per_base);
-    ti.start = a.pert.begin + (t % a.tiles_per_base) * 256;
-    const uint64_t rem = a.pert.end - ti.start;
-    ti.nvalid = rem < 256 ? (int)rem : 256;
+// The tile sequence of a cluster is contiguous, so (base, tile of the base) advance incrementally: one
+// 64-bit division per thread per launch (TileIter's constructor), none per tile.
+struct TileIter {
+  int b;              // range mode: base input of the current tile
+  uint64_t off;       // range mode: tile index inside the base's range
+  __device__ __forceinline__ TileIter(const Args& a, uint64_t t0) {
+    b = a.eval_idx ? a.eval_base : (int)(t0 / a.tiles_per_base);
+    off = a.eval_idx ? t0 : t0 % a.tiles_per_base;
   }
-  return ti;
-}
+  __device__ __forceinline__ void next(const Args& a) {
+    if (++off == a.tiles_per_base && !a.eval_idx) { off = 0; b++; }
+  }
+  __device__ __forceinline__ TileInfo info(const Args& a) const {
+    TileInfo ti;
+    ti.b = b;
+    if (a.eval_idx) {
+      ti.start = off * 256;
+      const int64_t rem = a.eval_n - (int64_t)ti.start;
+      ti.nvalid = rem < 256 ? (int)rem : 256;
+    } else {
+      ti.start = a.pert.begin + off * 256;
+      const uint64_t rem = a.pert.end - ti.start;
+      ti.nvalid = rem < 256 ? (int)rem : 256;
+    }
+    return ti;
+  }
+};
 
 // contiguous range of pair tiles owned by cluster c (base inputs change rarely inside a range)
 __device__ __forceinline__ void cluster_range(uint64_t n, uint64_t c, uint64_t nc, uint64_t& t0, uint64_t& t1) {
@@ -708,12 +720,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const int gt = 32 * gw + lane;                         // 0..383
     uint32_t tl = 0;
     const int nblk = (a.n0 + 31) / 32;                     // Philox blocks holding pixels
-    const int kneed = 16 * a.nk16;                         // K elements the MMA reads
     const bool clampk = a.clamp != 0;
     int gbase = -1;                                        // base whose clamp bounds are staged
-    for (uint64_t t = t_begin; t < t_end; t++, tl++) {
+    TileIter tit(a, t_begin);
+    for (uint64_t t = t_begin; t < t_end; t++, tl++, tit.next(a)) {
       if (gt == 0) TR(tl, 6);
-      const TileInfo ti = tile_info(a, t);
+      const TileInfo ti = tit.info(a);
       if (clampk && ti.b != gbase) {
         // every generator thread meets this barrier at the same tile (the tile sequence is the
         // cluster's), after all its stages of the previous base: then the table is free
@@ -784,16 +796,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           named_bar(6 + grp, 128);
           TRG(tl, kb, 2);
           uint8_t* slot = sG + st * kTile;
-          const int e0 = 64 * kb;
 #pragma unroll
-          for (int ch = 0; ch < 4; ch++)
-            if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)         // only the K steps the MMA reads
+          for (int ch = 0; ch < 4; ch++)                       // (K steps beyond nk16 are written too: the
+            if (MLPV_EXP != 21)                                //  MMA never reads them, the slot holds 64)
               *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = out[ch];
           const uint32_t w1w[4] = {w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
           for (int ch = 4; ch < 8; ch++) {
             const uint4 o = gen_chunk<TY>(nibble_word(w1w[ch - 4]), S.ctab[8 * kb + ch], a.cm2, a.cc2);
-            if (MLPV_EXP != 21 && kneed > e0 + 8 * ch)
+            if (MLPV_EXP != 21)
               *reinterpret_cast<uint4*>(slot + sw128_off(r, 16 * ch)) = o;
           }
           fence_proxy_async();
@@ -834,8 +845,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const float stepS = a.stepS;
     const bool clampk = a.clamp != 0;
     uint32_t tl = 0;
-    for (uint64_t t = t_begin; t < t_end; t++, tl++) {
-      const TileInfo ti = tile_info(a, t);
+    TileIter tit(a, t_begin);
+    for (uint64_t t = t_begin; t < t_end; t++, tl++, tit.next(a)) {
+      const TileInfo ti = tit.info(a);
       const int grow = 128 * (int)rank + r;
       // a row outside the restriction R (Philox spaces, k_restrict_mask) gets no verdict / coverage
       const bool valid = grow < ti.nvalid && (eval || in_restriction(a.pert, ti.b, ti.start + (uint64_t)grow));
