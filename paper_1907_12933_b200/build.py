@@ -24,6 +24,8 @@ def _stale(lib: str = LIB) -> bool:
 def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
     """trace=True builds the debug variant libmlpv_trace.so (k_fused3 timeline stamps, -DMLPV_TRACE)."""
     lib = LIB.replace(".so", "_trace.so") if trace else LIB
+    if os.environ.get("MLPV_LIB_OUT"):
+        lib = os.path.join(HERE, os.environ["MLPV_LIB_OUT"])
     if not force and not _stale(lib):
         return lib
     tmp = lib + f".tmp{os.getpid()}"
@@ -32,6 +34,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
         extra.append(f"-DMLPV_EXP={int(os.environ['MLPV_EXP'])}")
     if os.environ.get("MLPV_WAIT_TIMEOUT"):            # debug: trap instead of hanging on a lost arrive
         extra.append(f"-DMLPV_WAIT_TIMEOUT={int(os.environ['MLPV_WAIT_TIMEOUT'])}")
+    if os.environ.get("MLPV_EXTRA_DEFS"):              # A/B variants: extra -D flags, built to MLPV_LIB_OUT
+        extra += os.environ["MLPV_EXTRA_DEFS"].split()
     cmd = [NVCC, *FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

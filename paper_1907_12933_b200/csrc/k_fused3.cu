@@ -124,6 +124,9 @@ constexpr int kMaxN0 = 1024;
 // (20 idle / trace observer, 21 weight producer, 23 MMA issuer for all three layers / TMEM owner),
 // 12-19 epilogue team (E1, E2, E3 -- on the tile's critical path; two warps per TMEM lane quadrant),
 // 0-11 generator (throughput work with a five-stage ring of slack; one warpgroup per stage group).
+#ifndef MLPV_F3_GEN_SLEEP
+#define MLPV_F3_GEN_SLEEP 128
+#endif
 #if MLPV_EXP == 31
 constexpr int kNGenGroups = 2, kWE = 12, kWIdle = 20, kWProd = 21, kWIss = 23;   // timing experiment: warps 8-11 idle
 #else
@@ -792,7 +795,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           }
           const uint32_t st = gs % kSG, ph = (gs / kSG) & 1u;
           TRG(tl, kb, 1);
-          if ((gw & 3) == 0) mbar_wait_sleep(&S.g_empty[st], ph ^ 1u, 128);   // one poller per group
+          if ((gw & 3) == 0) mbar_wait_sleep(&S.g_empty[st], ph ^ 1u, MLPV_F3_GEN_SLEEP);   // one poller per group
           named_bar(6 + grp, 128);
           TRG(tl, kb, 2);
           uint8_t* slot = sG + st * kTile;
