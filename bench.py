@@ -103,9 +103,11 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("MLPV_BENCH_SAMPLER") == "off":    # diagnostic runs only (tools/s4_smi_ab.sh)
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", self.idx], stdout=subprocess.PIPE,
+                                          "-lms", os.environ.get("MLPV_BENCH_SAMPLER_MS", "200"), "-i", self.idx], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -115,7 +117,8 @@ class ClockSampler:
         (host time.time() bounds of the timed region; every sample when none falls inside)."""
         if self.proc is None:
             return None
-        time.sleep(0.25)
+        # (no sleep before the terminate: a 0.25 s idle here let the power-capped GPU recover and
+        # lifted the e2e steps that follow 3-5 % above the device-timed ones, tools/s4_smi_ab.sh)
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
