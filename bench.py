@@ -19,6 +19,7 @@ import argparse
 import datetime
 import json
 import os
+import select
 import statistics
 import subprocess
 import sys
@@ -111,10 +112,18 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
+        # wait for the first sample (NVML start-up done) so that the sampler is live from here on
+        self.t_live = None
+        r, _, _ = select.select([self.proc.stdout], [], [], 10.0)
+        if r:
+            self.proc.stdout.readline()
+            self.t_live = time.time()
 
     def stop(self, t_begin: float = None, t_end: float = None):
         """Median SM clock and the throttle reasons of the samples taken inside [t_begin, t_end]
-        (host time.time() bounds of the timed region; every sample when none falls inside)."""
+        (host time.time() bounds of the timed region); when none falls inside, of the samples since the
+        sampler went live just before the warm-up (the same kernels under the same load)."""
         if self.proc is None:
             return None
         # (no sleep before the terminate: a 0.25 s idle here let the power-capped GPU recover and
@@ -138,7 +147,7 @@ class ClockSampler:
         inside = [f for ts, f in rows if ts is not None and t_begin is not None and t_begin - 0.05 <= ts <= t_end + 0.05]
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for f in (inside or [f for _, f in rows]):
+        for f in (inside or [f for _, f in rows]):       # (the first, idle sample was consumed by start())
             try:
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
