@@ -23,6 +23,7 @@ import select
 import statistics
 import subprocess
 import sys
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -94,6 +95,76 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+REASON_BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
+
+
+class NvmlSampler:
+    """In-process NVML sampler (the library nvidia-smi itself reads): SM clock and the active clock-event
+    reasons every `period` seconds from a thread, so that even a 40 ms timed region (cfg5) holds
+    samples; the nvidia-smi -lms 200 sampler below is the fallback when NVML is not importable."""
+
+    def __init__(self, nvml, handle, period: float = 0.02):
+        self.nvml, self.h, self.period = nvml, handle, period
+        self.rows, self.halt, self.thread = [], threading.Event(), None
+
+    @classmethod
+    def open(cls, uuid: str, index: str):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            try:
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid) if uuid else pynvml.nvmlDeviceGetHandleByIndex(int(index))
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(int(index))
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            return cls(pynvml, h)
+        except Exception:
+            return None
+
+    def _reasons(self) -> int:
+        try:
+            return int(self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        except Exception:
+            return int(self.nvml.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+
+    def _run(self):
+        while not self.halt.is_set():
+            try:
+                self.rows.append((time.time(), float(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM)),
+                                  self._reasons()))
+            except Exception:
+                pass
+            self.halt.wait(self.period)
+
+    def start(self):
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def stop(self, t_begin: float = None, t_end: float = None):
+        self.halt.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        try:
+            mx = float(self.nvml.nvmlDeviceGetMaxClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+        except Exception:
+            mx = 0.0
+        return self.summarise(self.rows, mx, t_begin, t_end, self.period)
+
+    @staticmethod
+    def summarise(rows, mx, t_begin, t_end, period):
+        """[(time, sm_mhz, reason bits)] -> the clocks object: samples inside [t_begin, t_end] (all when none)."""
+        inside = [r for r in rows if t_begin is not None and t_begin <= r[0] <= t_end]
+        use = inside or rows
+        if not use:
+            return None
+        bits = 0
+        for r in use:
+            bits |= r[2]
+        return {"sm_mhz": statistics.median(r[1] for r in use), "sm_max_mhz": mx,
+                "reasons": sorted(nm for nm, b in REASON_BITS if bits & b), "samples": len(use),
+                "source": f"nvml, {int(1e3 * period)} ms period" + ("" if inside else " (no sample inside the timed region: all samples)")}
+
+
 class ClockSampler:
     FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -126,14 +197,22 @@ class ClockSampler:
         sampler went live just before the warm-up (the same kernels under the same load)."""
         if self.proc is None:
             return None
-        # (no sleep before the terminate: a 0.25 s idle here let the power-capped GPU recover and
-        # lifted the e2e steps that follow 3-5 % above the device-timed ones, tools/s4_smi_ab.sh)
+        # (no sleep before the terminate unless the timed region was too short to hold a 200 ms
+        # sample: a 0.25 s idle here lets the power-capped GPU recover and lifts the e2e steps that
+        # follow 3-5 % above the device-timed ones, tools/s4_smi_ab.sh)
+        if t_begin is not None and t_end - t_begin < 0.45:
+            time.sleep(0.25)
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
             out, _ = self.proc.communicate()
+        return self.summarise(out, t_begin, t_end)
+
+    @staticmethod
+    def summarise(out: str, t_begin: float = None, t_end: float = None):
+        """nvidia-smi csv lines (FIELDS order) -> {"sm_mhz": median, "sm_max_mhz", "reasons", "samples"}."""
         rows = []
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -344,7 +423,11 @@ def main():
     # the clock sampler (nvidia-smi -lms) starts before the warm-up so that its start-up (NVML
     # initialisation) is not inside the timed region; only samples stamped inside it are reported
     gpu_idx = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local)
-    clocks = ClockSampler(gpu_idx)
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    except Exception:
+        uuid = ""
+    clocks = (None if os.environ.get("MLPV_BENCH_SAMPLER") in ("smi", "off") else NvmlSampler.open(uuid, gpu_idx)) or ClockSampler(gpu_idx)
     late = os.environ.get("MLPV_BENCH_SAMPLER") == "late"
     if not late:
         clocks.start()

@@ -45,3 +45,43 @@ def test_cli_gpu(capsys, oracle_mod):
     assert code == (cli.EXIT_VIOLATED if not all(rep["literal"].values()) else cli.EXIT_OK)
     # an invalid argument value reaching the ABI is a usage error
     assert cli.main(["verify", "--config", "gamma", "--gamma", "-1", "--max-bound", "4"]) == cli.EXIT_USAGE
+
+
+def test_bench_clock_sampler_summary():
+    """bench.py's clock line: only the samples stamped inside the timed region count; the throttle
+    reasons are those active in them; every sample serves when none falls inside."""
+    import datetime
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    t0 = datetime.datetime(2026, 1, 2, 3, 4, 5).timestamp()
+
+    def row(dt, sm, cap):
+        ts = datetime.datetime.fromtimestamp(t0 + dt).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        return f"{ts}, {sm}, 1965, 900.0, 0x0000000000000004, Not Active, Not Active, Not Active, {cap}"
+
+    out = "\n".join([row(-1.0, 300, "Not Active"), row(0.1, 1700, "Active"), row(0.3, 1800, "Active"),
+                     row(0.5, 1750, "Not Active"), row(2.0, 1965, "Not Active"), "garbage line"])
+    c = bench.ClockSampler.summarise(out, t0, t0 + 0.6)
+    assert c == {"sm_mhz": 1750.0, "sm_max_mhz": 1965.0, "reasons": ["sw_power_cap"], "samples": 3}
+    c = bench.ClockSampler.summarise(out, t0 + 10, t0 + 11)      # nothing inside: every sample
+    assert c["samples"] == 5 and c["sm_mhz"] == 1750.0
+    assert bench.ClockSampler.summarise("", t0, t0 + 1) is None
+
+
+def test_bench_nvml_sampler_summary():
+    """The in-process NVML sampler's clocks object: median over the samples inside the timed region,
+    reasons = union of their clock-event bits (0x4 power cap, 0x8 hw slowdown, 0x20 / 0x40 thermal)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench_mod2", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    rows = [(9.0, 210.0, 0x1), (10.01, 1700.0, 0x4), (10.03, 1720.0, 0x4), (10.05, 1800.0, 0x0), (10.2, 1965.0, 0x40)]
+    c = bench.NvmlSampler.summarise(rows, 1965.0, 10.0, 10.1, 0.02)
+    assert (c["sm_mhz"], c["sm_max_mhz"], c["reasons"], c["samples"]) == (1720.0, 1965.0, ["sw_power_cap"], 3)
+    c = bench.NvmlSampler.summarise(rows, 1965.0, 20.0, 21.0, 0.02)
+    assert c["samples"] == 5 and "hw_thermal_slowdown" in c["reasons"] and "all samples" in c["source"]
+    assert bench.NvmlSampler.summarise([], 1965.0, 0.0, 1.0, 0.02) is None
