@@ -1031,8 +1031,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_large
           p_amb = false;
         }
         if (l < L) {
+          // the scratch stores must be performed at the L2 (device scope), where the producer's bulk
+          // copies read them, before the hand-off: with a CTA-scope fence a few 16-byte words were
+          // occasionally still in flight (cfg5 bf16: ~1 % of runs differed in a verdict count or a
+          // coverage bit from run to run, tools/s4_determinism.py)
+          __threadfence();
           fence_proxy_async_global();
-          __threadfence_block();
           named_bar(2, 256);
           if (e == 0) mbar_arrive(&h_ready[l]);
           if (e == 0) KT(etl, 17 + l);
