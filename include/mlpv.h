@@ -17,7 +17,10 @@
  *   - argument errors are detected synchronously, before any GPU work, and described by
  *     mlpv_last_error(handle) (mlpv_last_error(NULL) for errors of mlpv_create / mlpv_decode);
  *   - a CUDA failure is sticky: the handle reports MLPV_E_CUDA from then on;
- *   - a handle is bound to one device and is not thread-safe (one host thread at a time);
+ *   - a handle is bound to one device and is not thread-safe (one host thread at a time); its
+ *     workspace and activation scratch are per handle, so the calls of one handle must be ordered
+ *     on the device as well: use one stream per handle, or order its streams with events
+ *     (independent handles may run concurrently on different streams);
  *   - "device" pointers are CUDA global-memory pointers on the handle's device; "host" pointers
  *     are ordinary process memory; `stream` is a cudaStream_t (NULL = legacy default stream).
  *
