@@ -545,7 +545,7 @@ static mlpv_status prepare(mlpv_ctx* h, const void* bases, int n_base, const mlp
     for (int l = 0; l < n.L; l++) any |= dc->tau[l] < 0;
     if (any) {
       CUDA_TRY(h, launch_tau(n, plan->ws.trace, n_base, plan->tau_dev, st), "tau");
-      h->launches++;
+      h->launches += 2;                           // k_tau_max + k_tau_final
     }
   }
   return MLPV_OK;
