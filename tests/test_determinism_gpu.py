@@ -24,3 +24,30 @@ def test_run_to_run_determinism(name, nb, end, runs):
         g = run_gpu(chk, cfg)
         diff = {k: int(np.count_nonzero(g[k] != ref[k])) for k in KEYS if not np.array_equal(g[k], ref[k])}
         assert not diff, f"{name}: run {i} differs from run 0 in {diff}"
+
+
+def _irregular_results(name, end, handles=12, runs=4):
+    """Checks with irregular timing around them: fresh handles (allocation, weight upload, scratch
+    memset before the first check) and host work between the checks."""
+    import collections
+    import paper_1907_12933_b200 as P
+    cfg = M.make_config(name).subset(n_base=16, begin=0, end=end)
+    sig = []
+    for _ in range(handles):
+        chk = P.Checker(cfg.net)
+        for _ in range(runs):
+            g = run_gpu(chk, cfg)
+            sig.append(tuple(g[k].tobytes() for k in KEYS))
+    return collections.Counter(sig)
+
+
+@pytest.mark.parametrize("name,end", [("cfg4", 1 << 14), ("cfg3", 1 << 14), ("cfg5_int8", 1 << 12)])
+def test_reproducible_under_irregular_timing(name, end):
+    c = _irregular_results(name, end)
+    assert len(c) == 1, f"{name}: {len(c)} distinct results over {sum(c.values())} checks"
+
+
+@pytest.mark.xfail(strict=False, reason="open defect (DESIGN.md §6): k_large's float path depends on launch timing")
+def test_cfg5_bf16_reproducible_under_irregular_timing():
+    c = _irregular_results("cfg5_bf16", 1 << 12)
+    assert len(c) == 1, f"cfg5_bf16: {len(c)} distinct results over {sum(c.values())} checks"
